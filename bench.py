@@ -1,0 +1,367 @@
+"""Benchmark: fwd+bwd raster iterations/s at 1M Gaussians 1080p (BASELINE config 2).
+
+One step = one training iteration of the hot path per GPU on one view:
+render (preprocess + tile sort + forward) -> fused loss (L1 + 0.2 D-SSIM) ->
+backward (splat-parallel + chain) -> fused Adam (+ densify statistics),
+i.e. pipeline.py:_train_one_iteration on device.  With N GPUs every rank
+trains its own view each step and the 59-float-per-Gaussian gradients are
+summed with one NCCL all-reduce before the identical Adam step (view-sharded
+semi-global batch, weak scaling: value = N * steps / time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config C]
+
+--impl reference times the CPU reference path instead: the float64 C port of
+the reference rasterizer (oracle/, OpenMP over every host core) on the same
+workload and metric; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd raster iters/s at 1M Gaussians 1080p"
+FLOP_FWD_PER_PAIR = 30.0  # forward ~30 flops per walked pair
+FLOP_BWD_PER_PAIR = 80.0  # backward ~80 flops per walked pair (incl. reduction)
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--views", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _workload(cfg):
+    from paper_2503_13086_b200 import scenes
+
+    c = scenes.CONFIGS[cfg]
+    return (f"config{cfg}: {c['n']:,} Gaussians SH{c['sh_degree']} {c['width']}x{c['height']}, "
+            "one view per GPU per step: render + L1/D-SSIM loss + splat-parallel backward + Adam")
+
+
+def _views(args):
+    # spread the ring cameras of config 2 over the circle
+    return [v * (64 // max(args.views, 1)) for v in range(args.views)]
+
+
+class ClockSampler:
+    """nvidia-smi equivalent via NVML, sampled during the timed region."""
+
+    def __init__(self, dev_index=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop, self._t = period, threading.Event(), None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    _BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+             0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._BITS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _dist():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def _oracle_iteration(orc, P, opt, cam, target, weights):
+    out = orc.render(P, cam)
+    br = orc.total_loss(out["image"], target, out["soft_count"], out["hard_count"], weights)
+    g = orc.backward(P, out, br["d_image"], br["d_soft"])
+    opt.step(P, g, position_rate=1.6e-4)
+    return br["total"]
+
+
+def _cpu_setup(cfg, views):
+    from oracle import oracle as orc
+    from paper_2503_13086_b200 import scenes
+
+    orc.build()
+    hp = scenes.make_params(cfg, seed=0)
+    P = orc.Params(*(getattr(hp, k).astype(np.float64) for k in (
+        "positions", "rotations", "log_scales", "opacity_logits", "sh")))
+    tp = scenes.make_params(cfg, seed=1)
+    TP = orc.Params(*(getattr(tp, k).astype(np.float64) for k in (
+        "positions", "rotations", "log_scales", "opacity_logits", "sh")))
+    cams = [scenes.camera(cfg, view=v) for v in views[:2]]
+    targets = [orc.render(TP, c)["image"] for c in cams]
+    opt = orc.Optimizer(P, scene_extent=6.6)
+    return orc, P, opt, cams, targets
+
+
+def cpu_baseline(cfg, views, budget_s=25.0, min_iters=1, max_iters=3):
+    orc, P, opt, cams, targets = _cpu_setup(cfg, views)
+    w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
+    n, t0 = 0, time.perf_counter()
+    while n < max_iters and (n < min_iters or time.perf_counter() - t0 < budget_s / 2):
+        _oracle_iteration(orc, P, opt, cams[n % len(cams)], targets[n % len(cams)], w)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "iters/s", "cores": orc.num_threads(), "kind": "port",
+            "sample": f"{n} full iteration(s) (render+loss+backward+Adam) of {_workload(cfg).split(',')[0]}, "
+                      f"float64 C port of the reference (oracle/), OpenMP"}
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    views = _views(args)
+    orc, P, opt, cams, targets = _cpu_setup(args.config, views)
+    w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
+    for i in range(args.warmup and 1):  # one warm-up iteration is enough for the C port
+        _oracle_iteration(orc, P, opt, cams[i % 2], targets[i % 2], w)
+    t0 = time.perf_counter()
+    k = 0
+    budget = 150.0
+    while k < args.steps:
+        _oracle_iteration(orc, P, opt, cams[k % 2], targets[k % 2], w)
+        k += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    dt = time.perf_counter() - t0
+    val = k / dt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s", "n_gpus": world,
+            "steps": k, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": dt / k * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config generator, seeded)",
+            "config": {"workload": _workload(args.config), "parallelism": "host threads"},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": orc.num_threads(), "kind": "port",
+                             "sample": f"{k} iteration(s), float64 C port of the reference, "
+                                       f"{orc.num_threads()} OpenMP threads"},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_13086_b200 import GaussianField, _lib, scenes
+    from paper_2503_13086_b200.losses import LossWeights, total_loss
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.rasterize import backward, render
+    from paper_2503_13086_b200.rasterize.backward import FieldGrads
+    from paper_2503_13086_b200.train import TrainState, allreduce_grads
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = args.config
+    views = _views(args)
+    hp = scenes.make_params(cfg, seed=0)
+    tp = scenes.make_params(cfg, seed=1)
+    cams = [scenes.camera(cfg, view=v) for v in views]
+    tfield = GaussianField.from_host(tp)
+    targets = [render(tfield, c).image.clone() for c in cams]
+    del tfield
+    field = GaussianField.from_host(hp)
+    state = TrainState(field=field, optimizer=FieldOptimizer(field, scene_extent=6.6),
+                       weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), scene_extent=6.6)
+    rate = 1.6e-4
+    n = len(field)
+
+    def step(k, target=None):
+        cam_i = (k * world + rank) % len(cams)
+        cam = cams[cam_i]
+        out = render(state.field, cam)
+        br = total_loss(out.image, targets[cam_i] if target is None else target, out, state.weights)
+        if world > 1:
+            grads = FieldGrads.zeros(n, field.sh_degree, dev)
+            backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=True)
+            allreduce_grads(grads.flat)
+            s = 11 + 3 * field.n_sh_coeffs
+            state.stats[:n] += grads.flat[s * n:(s + 1) * n]
+            state.stats[n:] += grads.flat[(s + 1) * n:]
+        else:
+            grads = backward(state.field, out, br.d_image, br.d_soft, stats=state.stats)
+        state.optimizer.step(state.field, grads, position_rate=rate)
+        state.global_iteration += 1
+        return br
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    # ---------------- timed region (device time, CUDA events on the launching stream)
+    _lib.enable_timers(True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for k in range(args.steps):
+            step(args.warmup + k)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    stage_ms = _lib.timer_ms()
+    _lib.enable_timers(False)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * args.steps / (ms / 1e3)
+
+    # ---------------- end to end through the public API with host buffers
+    pinned = [t.cpu().pin_memory() for t in targets]
+    dbuf = torch.empty_like(targets[0])
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for k in range(args.steps):
+        i = ((args.warmup + args.steps + k) * world + rank) % len(cams)
+        dbuf.copy_(pinned[i], non_blocking=True)
+        br = step(args.warmup + args.steps + k, target=dbuf)
+        _ = br.values.cpu()  # loss terms back to the host (40 bytes)
+    f1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_val = world * args.steps / (float(e2e_ms.item()) / 1e3)
+
+    # ---------------- kernel launches of one step (CUPTI via torch.profiler)
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(0)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"
+                 and ("ssr" in e.name or "cub" in e.name.lower())]
+        launches = len(names) * args.steps
+    except Exception:
+        pass
+
+    if rank != 0:
+        return
+    # ---------------- roofline of the dominant kernel
+    P = 0
+    for c in cams:
+        P += int(render(state.field, c).n_walk.sum().item())
+    P_mean = P / len(cams)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = sm_count * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s (no measured fp32 peak exists)
+    fwd_ms = stage_ms.get("ssr_forward", 0.0)
+    bwd_ms = stage_ms.get("ssr_backward", 0.0)
+    if bwd_ms >= fwd_ms:
+        dom, flops, dms = "ssr_backward (k_backward_splat + k_backward_fixup)", FLOP_BWD_PER_PAIR * P_mean, bwd_ms
+    else:
+        dom, flops, dms = "ssr_forward (k_forward + k_forward_fixup)", FLOP_FWD_PER_PAIR * P_mean, fwd_ms
+    achieved = flops / (dms / 1e3) / 1e12
+    traffic = None
+    try:
+        prof_sum = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof_sum.get(dom.split(" ")[0])
+    except Exception:
+        pass
+    roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic,
+                "peak_source": f"nominal {sm_count} SMs x 128 FMA/clk x 2 x {sm_max:.0f} MHz "
+                               "(MEASURED_PEAKS.json has no fp32 figure)",
+                "work": f"{flops / 1e9:.2f} GFLOP per launch = {FLOP_BWD_PER_PAIR if 'backward' in dom else FLOP_FWD_PER_PAIR:.0f}"
+                        f" flop x {P_mean / 1e6:.1f} M walked pairs"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, views)
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "error": str(ex)}
+    h2d = int(targets[0].numel() * 4)
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE config generator, seeded; targets = "
+                                                      "renders of a second seed's field)",
+        "config": {"workload": _workload(cfg), "n_gaussians": n, "width": cams[0].width, "height": cams[0].height,
+                   "views": len(cams), "parallelism": f"view-sharded dp{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (field + Adam moments 708 MB, per-step working set > 1 GB)",
+                   "walked_pairs_per_view": P_mean},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if not k.endswith("workspace")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

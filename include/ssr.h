@@ -1,0 +1,183 @@
+/*
+ * ssr.h -- C ABI of the B200 (sm_100a) splat rasterizer ("splatstream raster").
+ *
+ * Drop-in boundary for the reference package's Python operator API
+ * (/root/reference/pkg/src/splatstream/...):
+ *
+ *   render(field, cam, bg, workers)            rasterize/forward.py:66-114
+ *     = ssr_preprocess -> ssr_scan_tiles -> ssr_bin_tiles -> ssr_forward
+ *   project_field(field, cam)                  rasterize/projection.py:69-191
+ *     = ssr_preprocess -> ssr_scan_tiles -> ssr_bin_tiles (+ ssr_project_aux)
+ *   backward(field, out, d_image, d_soft, ...) rasterize/backward.py:41-129
+ *     = ssr_backward (kernels.py:106-353) -> ssr_chain (backward.py:110-259)
+ *   FieldOptimizer.step(fld, grads, rate)      optim.py:113-130  = ssr_adam
+ *   GaussianField.densify_and_prune(...)       field.py:303-375
+ *     = ssr_densify_masks -> ssr_densify_apply (+ optim.py:101-111 remap)
+ *   total_loss(rendered, target, out, w)       losses.py:147-173 = ssr_loss
+ *
+ * Rules: every pointer is DEVICE memory unless documented otherwise; buffers
+ * are caller-owned (workspace sizes come from the *_workspace queries); no
+ * function allocates, frees or synchronises (except where a host-visible
+ * result is documented); all work is ordered on `stream` (a cudaStream_t);
+ * the only global state is the per-thread error string.  Every function
+ * returns 0 on success, non-zero on failure; ssr_last_error() describes it.
+ * `workers` of the reference API has no counterpart (the GPU grid is fixed).
+ */
+#ifndef SSR_H
+#define SSR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSR_OK 0
+#define SSR_ERR_INVALID 1 /* maps to InvalidParameter */
+#define SSR_ERR_CUDA 2    /* a CUDA launch/runtime failure */
+#define SSR_ERR_CAPACITY 3 /* instance count overflow etc. */
+
+#define SSR_TILE 16
+#define SSR_BUCKET 32 /* splats per backward bucket / checkpoint interval */
+
+/* Pinhole camera, world-to-camera x_cam = R x_world + t (camera.py:11-52).
+ * Kept in float64 end to end (the reference rejects fp32-rounded poses). */
+typedef struct ssr_camera {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy;
+  double center[3]; /* -R^T t */
+  int32_t width, height;
+} ssr_camera;
+
+/* Per-Gaussian preprocess outputs (indexed by field row, N entries each).
+ * Rows with tiles[i] == 0 are culled (projection.py:76-133) and left unwritten. */
+typedef struct ssr_splats {
+  double* mean;        /* N x 2  projected mean (u, v), fp64 */
+  float* conic_opa;    /* N x 4  (conic a, b, c, opacity), fp32 */
+  float* color;        /* N x 4  clamped SH colour (r, g, b, 0), fp32 */
+  double* conic_opa64; /* N x 4  fp64 copies for the guard-band fix-up */
+  double* color64;     /* N x 4 */
+  double* depth;       /* N      camera-space z, fp64 */
+  int32_t* rect;       /* N x 4  tile rect (tx0, ty0, tx1, ty1), exclusive upper */
+  uint32_t* tiles;     /* N      tiles touched (0 = culled) */
+  uint32_t* offset;    /* N      exclusive scan of tiles = first instance id */
+} ssr_splats;
+
+/* Render-time per-pixel / per-tile state retained for the backward. */
+typedef struct ssr_frame {
+  int32_t width, height, tiles_x, tiles_y;
+  float bg[3];
+  float* image;        /* H x W x 3 */
+  float* t_final;      /* H x W */
+  int32_t* n_walk;     /* H x W */
+  uint8_t* terminated; /* H x W */
+  int32_t* hard_count; /* H x W */
+  double* soft_count;  /* H x W  float64: counts reach 10^4, the bar is 1e-4 absolute */
+  uint8_t* flagged;    /* H x W  1 = pixel re-walked in fp64 (guard band) */
+  int32_t* tile_info;  /* n_tiles x 2  (max n_walk, flagged pixel count) */
+  float* ckpt;         /* ssr_ckpt_floats(M, n_tiles) floats: (T, C_front rgb) per bucket/pixel */
+} ssr_frame;
+
+const char* ssr_last_error(void);
+int ssr_version(void);
+/* sm count / compute capability of the current device (host-visible). */
+int ssr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---------------------------------------------------------- stage 1 */
+/* projection.py:69-162 + sh.py:114-132: EWA projection, conic, radius, tile
+ * rect, SH colour; float64 arithmetic on float32 storage. */
+int ssr_preprocess(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
+                   const float* rotations, const float* log_scales, const float* opacity_logits,
+                   const float* sh, ssr_splats splats, void* stream);
+
+/* Retained intermediates of ProjectedSplats (projection.py:40-48), N-indexed,
+ * fp64; for API completeness -- the hot path recomputes them in ssr_chain. */
+int ssr_project_aux(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
+                    const float* rotations, const float* log_scales, const float* sh,
+                    const uint32_t* tiles, double* cam_points, double* clamp_mul, double* cov2d,
+                    double* cov3d_cam, double* sh_dirs, double* sh_radii, uint8_t* sh_lo,
+                    uint8_t* sh_hi, double* radii, void* stream);
+
+/* ---------------------------------------------------------- stage 2 */
+/* Exclusive scan of splats.tiles into splats.offset; *total_dev (device) gets M. */
+int ssr_scan_workspace(int64_t n, int64_t* bytes);
+int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int64_t workspace_bytes,
+                   uint32_t* total_dev, void* stream);
+
+/* projection.py:165-191: duplicate each visible splat per overlapped tile,
+ * 64-bit (tile << 32 | fp32 depth bits) stable radix sort, tie-fix of equal
+ * keys by (fp64 depth, index), searchsorted tile ranges.  Outputs:
+ *   inst_gauss[M]   field row of each sorted instance
+ *   tile_ranges[2*n_tiles]  (start, end) per tile, searchsorted semantics */
+int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes);
+int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tiles_y, ssr_splats splats,
+                  uint32_t* inst_gauss, int32_t* tile_ranges, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
+/* Floats needed for the checkpoint buffer of a frame with M instances. */
+int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles);
+
+/* ---------------------------------------------------------- stage 3 */
+/* kernels.py:31-103: 16x16-tile front-to-back blend (fp32) with an fp64
+ * guard-band re-walk of pixels whose discrete decisions sit within `band`
+ * (relative) of a threshold. */
+int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
+                const int32_t* tile_ranges, ssr_frame frame, float band, void* stream);
+
+/* ---------------------------------------------------------- stage 4 */
+/* kernels.py:106-353: per-instance rows [dcolor rgb, dlogit, dmu xy,
+ * dconic abc] (9 floats) stored at the instance's splat-major position
+ * (splats.offset[g] + local tile index).  layout 0 = splat-parallel
+ * (Taming-style warp per 32-splat bucket), 1 = pixel-parallel.  Rows of
+ * guard-band pixels are added by an fp64 pixel walk. */
+int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
+                 const int32_t* tile_ranges, ssr_frame frame, const float* d_image,
+                 const float* d_soft, float* inst_rows, void* stream);
+
+/* backward.py:110-259 + sh.py:135-152: merge rows per splat (bincount
+ * order) and chain through projection/SH in fp64.  grads is the flat
+ * FieldGrads buffer [pos 3N | rot 4N | logscale 3N | logit N | sh 3KN |
+ * screen_norm N | visible N].  accumulate!=0 adds into it (view batches);
+ * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible. */
+int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
+              const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
+              const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream);
+
+/* ---------------------------------------------------------- stage 5 */
+/* optim.py:29-47,113-130: dense bias-corrected Adam over the flat parameter
+ * buffer [pos | rot | logscale | logit | sh] (n rows, K sh coeffs).
+ * lr[5] = (pos, rot, scale, opacity, sh_dc), sh rest lr = lr_sh_rest;
+ * bc1/bc2[5] = 1 - beta^step per class. */
+int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, float* m, float* v,
+             const double* lr, double lr_sh_rest, const double* bc1, const double* bc2, void* stream);
+
+/* field.py:303-375: per-row flags (bit0 keep, bit1 clone, bit2 split) and
+ * counts[3] = (n_clone, n_split, n_prune) in device memory. stats = the
+ * already averaged grad_accum / max(count, 1) (pipeline.py:209-210). */
+int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degree, const float* stats,
+                      double grad_threshold, double big_threshold, double prune_opacity,
+                      uint8_t* flags, int32_t* counts, void* stream);
+int ssr_densify_workspace(int64_t n, int64_t* bytes);
+/* Compacts params (+ Adam m, v when non-null) into the new buffers: kept rows,
+ * clones, split pairs (field.py:329-372, optim.py:49-54).  eps = (2*n_split)x3
+ * standard normals drawn on the host from the session RNG (field.py:340). */
+int ssr_densify_apply(int64_t n, int64_t n_new, int32_t sh_degree, const float* params,
+                      const float* m, const float* v, const uint8_t* flags, const double* eps,
+                      double log_shrink, float* new_params, float* new_m, float* new_v,
+                      void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------- loss */
+/* losses.py:55-173: w_l1 * L1 + w_ssim * (1 - SSIM) + w_load * std(soft).
+ * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,
+ * total, hard_count_std) as float64 in device memory. */
+int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes);
+int ssr_loss(int32_t width, int32_t height, const float* image, const float* target,
+             const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim,
+             double w_load, float* d_image, float* d_soft, double* out, void* workspace,
+             int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSR_H */

@@ -1,0 +1,323 @@
+// Shared device code for the sm_100a splat rasterizer.
+//
+// Two numeric regimes live here:
+//  * float64 per-Gaussian math (projection, SH, chain) that restates the
+//    reference op-for-op (rasterize/projection.py:69-162, sh.py:36-152) so
+//    culling, tile rects, depth order and clamp masks come out identical;
+//    TUs using it are compiled with -fmad=false.
+//  * float32 per-pair blend math used by the forward and both backward
+//    layouts; every rounding step is pinned with __f*_rn intrinsics so the
+//    backward replays the forward's discrete decisions bit-for-bit.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ssr.h"
+
+namespace ssr {
+
+constexpr int TILE = 16;
+constexpr int TILE_PX = TILE * TILE;
+constexpr int BUCKET = 32;
+constexpr double ZNEAR = 0.2;
+constexpr double COV2D_DILATION = 0.3;
+constexpr double FRUSTUM_EXPAND = 1.3;
+constexpr double ALPHA_MIN = 1.0 / 255.0;
+constexpr double ALPHA_CAP = 0.99;
+constexpr double T_EPS = 1e-4;
+constexpr double SOFT_TAU = 0.01;
+constexpr float ALPHA_MIN_F = 1.0f / 255.0f;
+constexpr float ALPHA_CAP_F = 0.99f;
+constexpr float T_EPS_F = 1e-4f;
+
+void set_error(const std::string& msg);
+int check_cuda(cudaError_t e, const char* what);
+int check_launch(const char* what);
+
+#define SSR_TRY(expr)          \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != SSR_OK) return _rc; \
+  } while (0)
+
+struct Cam {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy;
+  double center[3];
+  int width, height;
+};
+
+inline Cam to_cam(const ssr_camera& c) {
+  Cam o;
+  for (int i = 0; i < 9; i++) o.R[i] = c.R[i];
+  for (int i = 0; i < 3; i++) {
+    o.t[i] = c.t[i];
+    o.center[i] = c.center[i];
+  }
+  o.fx = c.fx;
+  o.fy = c.fy;
+  o.cx = c.cx;
+  o.cy = c.cy;
+  o.width = c.width;
+  o.height = c.height;
+  return o;
+}
+
+// ------------------------------------------------------------------ fp64 SH
+// sh.py:36-65
+__device__ __forceinline__ void sh_basis64(int deg, const double d[3], double* out) {
+  const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                        -1.0925484305920792, 0.5462742152960396};
+  const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                        0.3731763325901154,  -0.4570457994644658, 1.445305721320277,
+                        -0.5900435899266435};
+  out[0] = 0.28209479177387814;
+  if (deg >= 1) {
+    double x = d[0], y = d[1], z = d[2];
+    out[1] = -0.4886025119029199 * y;
+    out[2] = 0.4886025119029199 * z;
+    out[3] = -0.4886025119029199 * x;
+    if (deg >= 2) {
+      double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+      out[4] = C2[0] * xy;
+      out[5] = C2[1] * yz;
+      out[6] = C2[2] * (2.0 * zz - xx - yy);
+      out[7] = C2[3] * xz;
+      out[8] = C2[4] * (xx - yy);
+      if (deg >= 3) {
+        out[9] = C3[0] * y * (3.0 * xx - yy);
+        out[10] = C3[1] * xy * z;
+        out[11] = C3[2] * y * (4.0 * zz - xx - yy);
+        out[12] = C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+        out[13] = C3[4] * x * (4.0 * zz - xx - yy);
+        out[14] = C3[5] * z * (xx - yy);
+        out[15] = C3[6] * x * (xx - 3.0 * yy);
+      }
+    }
+  }
+}
+
+// sh.py:68-111 ; g[k*3+d]
+__device__ __forceinline__ void sh_basis_grad64(int deg, const double dd[3], double* g) {
+  const double C1 = 0.4886025119029199;
+  const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                        -1.0925484305920792, 0.5462742152960396};
+  const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                        0.3731763325901154,  -0.4570457994644658, 1.445305721320277,
+                        -0.5900435899266435};
+  const int K = (deg + 1) * (deg + 1);
+  for (int i = 0; i < K * 3; i++) g[i] = 0.0;
+  if (deg < 1) return;
+  double x = dd[0], y = dd[1], z = dd[2];
+  g[1 * 3 + 1] = -C1;
+  g[2 * 3 + 2] = C1;
+  g[3 * 3 + 0] = -C1;
+  if (deg >= 2) {
+    g[4 * 3 + 0] = C2[0] * y;
+    g[4 * 3 + 1] = C2[0] * x;
+    g[5 * 3 + 1] = C2[1] * z;
+    g[5 * 3 + 2] = C2[1] * y;
+    g[6 * 3 + 0] = C2[2] * (-2.0 * x);
+    g[6 * 3 + 1] = C2[2] * (-2.0 * y);
+    g[6 * 3 + 2] = C2[2] * (4.0 * z);
+    g[7 * 3 + 0] = C2[3] * z;
+    g[7 * 3 + 2] = C2[3] * x;
+    g[8 * 3 + 0] = C2[4] * (2.0 * x);
+    g[8 * 3 + 1] = C2[4] * (-2.0 * y);
+  }
+  if (deg >= 3) {
+    double xx = x * x, yy = y * y, zz = z * z;
+    g[9 * 3 + 0] = C3[0] * 6.0 * x * y;
+    g[9 * 3 + 1] = C3[0] * (3.0 * xx - 3.0 * yy);
+    g[10 * 3 + 0] = C3[1] * y * z;
+    g[10 * 3 + 1] = C3[1] * x * z;
+    g[10 * 3 + 2] = C3[1] * x * y;
+    g[11 * 3 + 0] = C3[2] * (-2.0 * x * y);
+    g[11 * 3 + 1] = C3[2] * (4.0 * zz - xx - 3.0 * yy);
+    g[11 * 3 + 2] = C3[2] * (8.0 * y * z);
+    g[12 * 3 + 0] = C3[3] * (-6.0 * x * z);
+    g[12 * 3 + 1] = C3[3] * (-6.0 * y * z);
+    g[12 * 3 + 2] = C3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    g[13 * 3 + 0] = C3[4] * (4.0 * zz - 3.0 * xx - yy);
+    g[13 * 3 + 1] = C3[4] * (-2.0 * x * y);
+    g[13 * 3 + 2] = C3[4] * (8.0 * x * z);
+    g[14 * 3 + 0] = C3[5] * (2.0 * x * z);
+    g[14 * 3 + 1] = C3[5] * (-2.0 * y * z);
+    g[14 * 3 + 2] = C3[5] * (xx - yy);
+    g[15 * 3 + 0] = C3[6] * (3.0 * xx - 3.0 * yy);
+    g[15 * 3 + 1] = C3[6] * (-6.0 * x * y);
+  }
+}
+
+// field.py:40-60
+__device__ __forceinline__ void quat_rotmat64(const double q[4], double r[9], double qn[4], double* nrm_out) {
+  double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
+  r[0] = 1 - 2 * (y * y + z * z);
+  r[1] = 2 * (x * y - w * z);
+  r[2] = 2 * (x * z + w * y);
+  r[3] = 2 * (x * y + w * z);
+  r[4] = 1 - 2 * (x * x + z * z);
+  r[5] = 2 * (y * z - w * x);
+  r[6] = 2 * (x * z - w * y);
+  r[7] = 2 * (y * z + w * x);
+  r[8] = 1 - 2 * (x * x + y * y);
+  qn[0] = w;
+  qn[1] = x;
+  qn[2] = y;
+  qn[3] = z;
+  *nrm_out = nrm;
+}
+
+__device__ __forceinline__ long long trunc_i64(double v) {
+  // numpy astype(int64) on x86: truncation toward zero, INT64_MIN when out of range
+  if (!(v > -9.2e18 && v < 9.2e18)) return (long long)(-9223372036854775807LL - 1);
+  return (long long)v;
+}
+__device__ __forceinline__ long long clip_ll(long long v, long long lo, long long hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+struct Proj64 {
+  double cp[3];     // camera-space point
+  double u, v;      // projected mean
+  double mulx, muly, txc, tyc;
+  double cc[9];     // camera-space covariance
+  double A, B, C;   // dilated 2D covariance
+  double qa, qb, qc; // conic
+  double radius;
+  int rect[4];
+  double rot[9], qn[4], qnorm, sc[3];
+};
+
+// projection.py:76-128 for one Gaussian.  Returns true when the splat is kept.
+__device__ __forceinline__ bool project64(const Cam& cam, const float* pos, const float* quat,
+                                          const float* ls, int tiles_x, int tiles_y, Proj64& o) {
+  const double* R = cam.R;
+  double p[3] = {(double)pos[0], (double)pos[1], (double)pos[2]};
+  for (int j = 0; j < 3; j++)
+    o.cp[j] = p[0] * R[j * 3 + 0] + p[1] * R[j * 3 + 1] + p[2] * R[j * 3 + 2] + cam.t[j];
+  if (!(o.cp[2] > ZNEAR)) return false;
+  const double x = o.cp[0], y = o.cp[1], z = o.cp[2];
+  o.u = cam.fx * x / z + cam.cx;
+  o.v = cam.fy * y / z + cam.cy;
+  const double limx = FRUSTUM_EXPAND * (cam.width / (2.0 * cam.fx));
+  const double limy = FRUSTUM_EXPAND * (cam.height / (2.0 * cam.fy));
+  const double tx = x / z, ty = y / z;
+  o.mulx = (tx > -limx && tx < limx) ? 1.0 : 0.0;
+  o.muly = (ty > -limy && ty < limy) ? 1.0 : 0.0;
+  o.txc = tx < -limx ? -limx : (tx > limx ? limx : tx);
+  o.tyc = ty < -limy ? -limy : (ty > limy ? limy : ty);
+  // field.py:71-75  Sigma = M M^T, M = R(q) diag(exp(s))
+  double q[4] = {(double)quat[0], (double)quat[1], (double)quat[2], (double)quat[3]};
+  quat_rotmat64(q, o.rot, o.qn, &o.qnorm);
+  double m[9], cw[9];
+  for (int j = 0; j < 3; j++) o.sc[j] = exp((double)ls[j]);
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) m[i * 3 + j] = o.rot[i * 3 + j] * o.sc[j];
+  for (int i = 0; i < 3; i++)
+    for (int k = 0; k < 3; k++) {
+      double acc = 0.0;
+      for (int j = 0; j < 3; j++) acc += m[i * 3 + j] * m[k * 3 + j];
+      cw[i * 3 + k] = acc;
+    }
+  // einsum("ij,njk,lk->nil", R, Sigma, R)
+  for (int a = 0; a < 3; a++)
+    for (int l = 0; l < 3; l++) {
+      double acc = 0.0;
+      for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++) acc += R[a * 3 + j] * cw[j * 3 + k] * R[l * 3 + k];
+      o.cc[a * 3 + l] = acc;
+    }
+  const double fx_z = cam.fx / z, fy_z = cam.fy / z;
+  const double j02 = -cam.fx * o.txc / z, j12 = -cam.fy * o.tyc / z;
+  const double c00 = o.cc[0], c01 = o.cc[1], c02 = o.cc[2], c11 = o.cc[4], c12 = o.cc[5], c22 = o.cc[8];
+  o.A = fx_z * (fx_z * c00 + j02 * c02) + j02 * (fx_z * c02 + j02 * c22) + COV2D_DILATION;
+  o.B = fx_z * (fy_z * c01 + j12 * c02) + j02 * (fy_z * c12 + j12 * c22);
+  o.C = fy_z * (fy_z * c11 + j12 * c12) + j12 * (fy_z * c12 + j12 * c22) + COV2D_DILATION;
+  const double det = o.A * o.C - o.B * o.B;
+  bool ok = det > 0.0;
+  const double inv_det = ok ? 1.0 / det : 0.0;
+  o.qa = o.C * inv_det;
+  o.qb = -o.B * inv_det;
+  o.qc = o.A * inv_det;
+  const double mid = 0.5 * (o.A + o.C);
+  const double mm = mid * mid - det;
+  const double lam = mid + sqrt(mm > 0.1 ? mm : 0.1);
+  o.radius = ceil(3.0 * sqrt(lam));
+  long long tx0 = clip_ll(trunc_i64((o.u - o.radius) / TILE), 0, tiles_x);
+  long long ty0 = clip_ll(trunc_i64((o.v - o.radius) / TILE), 0, tiles_y);
+  long long tx1 = clip_ll(trunc_i64((o.u + o.radius) / TILE) + 1, 0, tiles_x);
+  long long ty1 = clip_ll(trunc_i64((o.v + o.radius) / TILE) + 1, 0, tiles_y);
+  long long wx = tx1 - tx0 > 0 ? tx1 - tx0 : 0, wy = ty1 - ty0 > 0 ? ty1 - ty0 : 0;
+  ok = ok && (o.radius > 0) && (wx * wy > 0);
+  o.rect[0] = (int)tx0;
+  o.rect[1] = (int)ty0;
+  o.rect[2] = (int)tx1;
+  o.rect[3] = (int)ty1;
+  return ok;
+}
+
+// sh.py:114-132: direction, basis, clamped colour and masks.
+__device__ __forceinline__ void sh_color64(const Cam& cam, int deg, const float* pos, const float* shrow,
+                                           double dir[3], double* rs, double basis[16], double col[3],
+                                           bool lo[3], bool hi[3]) {
+  const int K = (deg + 1) * (deg + 1);
+  double off[3];
+  for (int j = 0; j < 3; j++) off[j] = (double)pos[j] - cam.center[j];
+  double r = sqrt(off[0] * off[0] + off[1] * off[1] + off[2] * off[2]);
+  *rs = r > 1e-12 ? r : 1e-12;
+  for (int j = 0; j < 3; j++) dir[j] = off[j] / *rs;
+  sh_basis64(deg, dir, basis);
+  for (int c = 0; c < 3; c++) {
+    double acc = 0.0;
+    for (int k = 0; k < K; k++) acc += (double)shrow[c * K + k] * basis[k];
+    double raw = acc + 0.5;
+    lo[c] = raw < 0.0;
+    hi[c] = raw > 1.0;
+    col[c] = raw < 0.0 ? 0.0 : (raw > 1.0 ? 1.0 : raw);
+  }
+}
+
+// ------------------------------------------------------------------ fp32 pair math
+// kernels.py:72-80.  Rounding pinned so forward and backward agree bitwise.
+__device__ __forceinline__ float pair_power(float dx, float dy, float a, float b, float c, float& q1) {
+  const float dxx = __fmul_rn(dx, dx), dyy = __fmul_rn(dy, dy), dxy = __fmul_rn(dx, dy);
+  q1 = __fmaf_rn(c, dyy, __fmul_rn(a, dxx));
+  return __fmaf_rn(-0.5f, q1, -__fmul_rn(b, dxy));
+}
+
+__device__ __forceinline__ float pair_alpha(float opa, float power) { return __fmul_rn(opa, expf(power)); }
+
+// Soft count of the forward (kernels.py:83) is accumulated as
+//   n_small * S0 + sum(y * p(y)) + sum(sigmoid(alpha) for alpha >= 2.5e-3),
+// y = alpha / SOFT_TAU, S0 = sigmoid(-ALPHA_MIN / SOFT_TAU) in float64 and p a
+// degree-5 fit of (sigmoid(y - ALPHA_MIN/TAU) - S0) / y on [0, 0.25]
+// (max abs error 1e-11; 5e-9 after fp32 Horner).  Long walks (10^4 slots)
+// would otherwise accumulate the fp32 rounding of the same ~0.403 term.
+constexpr double SOFT_S0 = 0.4031981879117929;
+constexpr float SOFT_Y0 = 0.25f;
+__device__ __forceinline__ float soft_dev_poly(float y) {
+  float p = 3.799443657e-04f;
+  p = __fmaf_rn(p, y, 1.492375741e-03f);
+  p = __fmaf_rn(p, y, -3.667983459e-03f);
+  p = __fmaf_rn(p, y, -1.779736020e-02f);
+  p = __fmaf_rn(p, y, 2.329335734e-02f);
+  p = __fmaf_rn(p, y, 2.406294048e-01f);
+  return __fmul_rn(y, p);
+}
+
+__device__ __forceinline__ float soft_sigmoid_accurate(float alpha) {
+  return 1.0f / (1.0f + expf(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f)));
+}
+
+__device__ __forceinline__ float soft_sigmoid(float alpha) {
+  // 1 / (1 + exp(-(alpha - 1/255) / 0.01))   (kernels.py:83)
+  const float e = __expf(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f));
+  return __fdividef(1.0f, 1.0f + e);
+}
+
+}  // namespace ssr

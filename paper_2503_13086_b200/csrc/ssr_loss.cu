@@ -1,0 +1,291 @@
+// Fused training objective on device (losses.py:55-173):
+//   w_l1 * L1 + w_ssim * (1 - SSIM) + w_load * std(soft_count)
+// with the analytic SSIM gradient (11-tap sigma=1.5 separable Gaussian,
+// zero padding, mean over the interior crop, channel-averaged).
+//
+// k_ssim_fwd: 32x32 output tile per CTA with a 5-pixel halo in shared
+// memory; computes the five blurred moments, the SSIM map and the three
+// per-pixel adjoint maps (d_mu, d_gx2, d_gxy), plus L1 / SSIM / soft-count
+// partial sums (fp64 atomics).  k_loss_finalize turns the sums into the
+// scalars.  k_ssim_bwd blurs the adjoint maps (the window is self-adjoint)
+// and writes d_image and d_soft.
+#include "ssr_common.cuh"
+
+namespace ssr {
+
+constexpr int LT = 32;           // output tile edge
+constexpr int HALO = 5;          // (11 - 1) / 2
+constexpr int LH = LT + 2 * HALO; // 42
+
+struct LossAcc {
+  double l1_sum, ssim_sum, soft_d, soft_d2, hard_d, hard_d2, soft0, hard0;
+  double mean_soft, std_soft;
+};
+
+__constant__ float c_win[11];
+
+__device__ __forceinline__ double block_sum64(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) s += red[i];
+  return s;
+}
+
+__global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
+                                                  const float* __restrict__ tgt, const double* __restrict__ soft,
+                                                  const int32_t* __restrict__ hard, float* __restrict__ dmaps,
+                                                  LossAcc* acc) {
+  __shared__ float sx[LH][LH + 1], sy[LH][LH + 1];
+  __shared__ float hz[5][LH][LT];
+  __shared__ double red[8];
+  const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
+  const int tid = threadIdx.x;
+  const size_t HW = (size_t)W * H;
+  const int n_crop_w = W - 2 * HALO, n_crop_h = H - 2 * HALO;
+  const double mw = 1.0 / ((double)n_crop_w * n_crop_h * 3.0);
+  const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+  double l1 = 0.0, ss = 0.0;
+  for (int ch = 0; ch < 3; ch++) {
+    for (int e = tid; e < LH * LH; e += blockDim.x) {
+      const int r = e / LH, c = e % LH;
+      const int gr = r0 - HALO + r, gc = c0 - HALO + c;
+      const bool in = gr >= 0 && gr < H && gc >= 0 && gc < W;
+      const size_t pi = (size_t)gr * W + gc;
+      sx[r][c] = in ? img[pi * 3 + ch] : 0.f;
+      sy[r][c] = in ? tgt[pi * 3 + ch] : 0.f;
+    }
+    __syncthreads();
+    for (int e = tid; e < LH * LT; e += blockDim.x) {
+      const int r = e / LT, c = e % LT;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; t++) {
+        const float x = sx[r][c + t], y = sy[r][c + t], w = c_win[t];
+        a0 += w * x;
+        a1 += w * y;
+        a2 += w * x * x;
+        a3 += w * y * y;
+        a4 += w * x * y;
+      }
+      hz[0][r][c] = a0;
+      hz[1][r][c] = a1;
+      hz[2][r][c] = a2;
+      hz[3][r][c] = a3;
+      hz[4][r][c] = a4;
+    }
+    __syncthreads();
+    for (int e = tid; e < LT * LT; e += blockDim.x) {
+      const int r = e / LT, c = e % LT;
+      const int gr = r0 + r, gc = c0 + c;
+      if (gr >= H || gc >= W) continue;
+      float mx = 0.f, my = 0.f, gx2 = 0.f, gy2 = 0.f, gxy = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; t++) {
+        const float w = c_win[t];
+        mx += w * hz[0][r + t][c];
+        my += w * hz[1][r + t][c];
+        gx2 += w * hz[2][r + t][c];
+        gy2 += w * hz[3][r + t][c];
+        gxy += w * hz[4][r + t][c];
+      }
+      const float vx = gx2 - mx * mx, vy = gy2 - my * my, cv = gxy - mx * my;
+      const float a1 = 2.f * mx * my + C1, a2 = 2.f * cv + C2;
+      const float b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
+      const float smap = (a1 * a2) / (b1 * b2);
+      const bool crop = gr >= HALO && gr < H - HALO && gc >= HALO && gc < W - HALO;
+      const size_t pi = (size_t)gr * W + gc;
+      float dmu = 0.f, dg2 = 0.f, dxy = 0.f;
+      if (crop) {
+        ss += (double)smap;
+        const float m = (float)mw;
+        dmu = m * (2.f * my * (a2 - a1) / (b1 * b2) - 2.f * mx * smap * (1.f / b1 - 1.f / b2));
+        dg2 = m * (-smap / b2);
+        dxy = m * (2.f * a1 / (b1 * b2));
+      }
+      dmaps[(size_t)(ch * 3 + 0) * HW + pi] = dmu;
+      dmaps[(size_t)(ch * 3 + 1) * HW + pi] = dg2;
+      dmaps[(size_t)(ch * 3 + 2) * HW + pi] = dxy;
+      l1 += (double)fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
+    }
+    __syncthreads();
+  }
+  double sd = 0.0, sd2 = 0.0, hd = 0.0, hd2 = 0.0;
+  const double s0 = soft[0];
+  const int32_t h0 = hard[0];
+  for (int e = tid; e < LT * LT; e += blockDim.x) {
+    const int gr = r0 + e / LT, gc = c0 + e % LT;
+    if (gr >= H || gc >= W) continue;
+    const size_t pi = (size_t)gr * W + gc;
+    const double d = soft[pi] - s0;
+    sd += d;
+    sd2 += d * d;
+    const double dh = (double)(hard[pi] - h0);
+    hd += dh;
+    hd2 += dh * dh;
+  }
+  double v;
+  v = block_sum64(l1, red);
+  if (tid == 0) atomicAdd(&acc->l1_sum, v);
+  v = block_sum64(ss, red);
+  if (tid == 0) atomicAdd(&acc->ssim_sum, v);
+  v = block_sum64(sd, red);
+  if (tid == 0) atomicAdd(&acc->soft_d, v);
+  v = block_sum64(sd2, red);
+  if (tid == 0) atomicAdd(&acc->soft_d2, v);
+  v = block_sum64(hd, red);
+  if (tid == 0) atomicAdd(&acc->hard_d, v);
+  v = block_sum64(hd2, red);
+  if (tid == 0) atomicAdd(&acc->hard_d2, v);
+}
+
+__global__ void k_loss_finalize(int W, int H, double w_l1, double w_ssim, double w_load, const double* soft,
+                                LossAcc* acc, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double n = (double)W * H;
+  const double n_crop = (double)(W - 2 * HALO) * (H - 2 * HALO);
+  const double l1 = acc->l1_sum / (n * 3.0);
+  const double ssim = acc->ssim_sum / (n_crop * 3.0);
+  const double md = acc->soft_d / n;
+  double var = acc->soft_d2 / n - md * md;
+  double sd = var > 0.0 ? sqrt(var) : 0.0;
+  const double mh = acc->hard_d / n;
+  double varh = acc->hard_d2 / n - mh * mh;
+  acc->mean_soft = soft[0] + md;
+  acc->std_soft = sd;
+  const double load = w_load > 0.0 ? sd : 0.0;
+  out[0] = l1;
+  out[1] = 1.0 - ssim;
+  out[2] = load;
+  out[3] = w_l1 * l1 + w_ssim * (1.0 - ssim) + w_load * load;
+  out[4] = varh > 0.0 ? sqrt(varh) : 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __restrict__ img,
+                                                  const float* __restrict__ tgt, const double* __restrict__ soft,
+                                                  const float* __restrict__ dmaps, const LossAcc* __restrict__ acc,
+                                                  double w_l1, double w_ssim, double w_load,
+                                                  float* __restrict__ d_image, float* __restrict__ d_soft) {
+  __shared__ float sm[3][LH][LH + 1];
+  __shared__ float hz[3][LH][LT];
+  const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
+  const int tid = threadIdx.x;
+  const size_t HW = (size_t)W * H;
+  const float gl1 = (float)(w_l1 / (double)(HW * 3));
+  const float gss = (float)w_ssim;
+  for (int ch = 0; ch < 3; ch++) {
+    for (int e = tid; e < LH * LH; e += blockDim.x) {
+      const int r = e / LH, c = e % LH;
+      const int gr = r0 - HALO + r, gc = c0 - HALO + c;
+      const bool in = gr >= 0 && gr < H && gc >= 0 && gc < W;
+      const size_t pi = (size_t)gr * W + gc;
+      for (int k = 0; k < 3; k++) sm[k][r][c] = in ? dmaps[(size_t)(ch * 3 + k) * HW + pi] : 0.f;
+    }
+    __syncthreads();
+    for (int e = tid; e < LH * LT; e += blockDim.x) {
+      const int r = e / LT, c = e % LT;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; t++) {
+        const float w = c_win[t];
+        a0 += w * sm[0][r][c + t];
+        a1 += w * sm[1][r][c + t];
+        a2 += w * sm[2][r][c + t];
+      }
+      hz[0][r][c] = a0;
+      hz[1][r][c] = a1;
+      hz[2][r][c] = a2;
+    }
+    __syncthreads();
+    for (int e = tid; e < LT * LT; e += blockDim.x) {
+      const int r = e / LT, c = e % LT;
+      const int gr = r0 + r, gc = c0 + c;
+      if (gr >= H || gc >= W) continue;
+      float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; t++) {
+        const float w = c_win[t];
+        b0 += w * hz[0][r + t][c];
+        b1 += w * hz[1][r + t][c];
+        b2 += w * hz[2][r + t][c];
+      }
+      const size_t pi = (size_t)gr * W + gc;
+      const float x = img[pi * 3 + ch], y = tgt[pi * 3 + ch];
+      const float gs = b0 + 2.f * x * b1 + y * b2;  // d SSIM / d x
+      const float diff = x - y;
+      const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+      d_image[pi * 3 + ch] = gl1 * sgn - gss * gs;
+    }
+    __syncthreads();
+  }
+  if (d_soft) {
+    const double sd = acc->std_soft, mean = acc->mean_soft;
+    const double scale = (w_load > 0.0 && sd > 0.0) ? w_load / ((double)HW * sd) : 0.0;
+    for (int e = tid; e < LT * LT; e += blockDim.x) {
+      const int gr = r0 + e / LT, gc = c0 + e % LT;
+      if (gr >= H || gc >= W) continue;
+      const size_t pi = (size_t)gr * W + gc;
+      d_soft[pi] = (float)((soft[pi] - mean) * scale);
+    }
+  }
+}
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+static int ensure_window() {
+  static bool done = false;
+  if (done) return SSR_OK;
+  float w[11];
+  double g[11], s = 0.0;
+  for (int t = 0; t < 11; t++) {
+    const double tt = t - 5;
+    g[t] = exp(-(tt * tt) / (2.0 * 1.5 * 1.5));
+    s += g[t];
+  }
+  for (int t = 0; t < 11; t++) w[t] = (float)(g[t] / s);
+  SSR_TRY(check_cuda(cudaMemcpyToSymbol(c_win, w, sizeof(w)), "ssim window"));
+  done = true;
+  return SSR_OK;
+}
+
+}  // namespace ssr
+
+using namespace ssr;
+
+extern "C" int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes) {
+  *bytes = align_up((int64_t)9 * width * height * 4, 256) + align_up(sizeof(LossAcc), 256);
+  return SSR_OK;
+}
+
+extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const float* target,
+                        const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim, double w_load,
+                        float* d_image, float* d_soft, double* out, void* workspace, int64_t workspace_bytes,
+                        void* stream) {
+  if (width < 11 || height < 11) {
+    set_error("ssr_loss: image smaller than the 11-tap SSIM window");
+    return SSR_ERR_INVALID;
+  }
+  int64_t need = 0;
+  ssr_loss_workspace(width, height, &need);
+  if (workspace_bytes < need) {
+    set_error("ssr_loss: workspace too small");
+    return SSR_ERR_INVALID;
+  }
+  SSR_TRY(ensure_window());
+  cudaStream_t st = (cudaStream_t)stream;
+  float* dmaps = (float*)workspace;
+  LossAcc* acc = (LossAcc*)((char*)workspace + align_up((int64_t)9 * width * height * 4, 256));
+  SSR_TRY(check_cuda(cudaMemsetAsync(acc, 0, sizeof(LossAcc), st), "loss acc"));
+  dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
+  k_ssim_fwd<<<grid, 256, 0, st>>>(width, height, image, target, soft_count, hard_count, dmaps, acc);
+  SSR_TRY(check_launch("k_ssim_fwd"));
+  k_loss_finalize<<<1, 32, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, acc, out);
+  SSR_TRY(check_launch("k_loss_finalize"));
+  k_ssim_bwd<<<grid, 256, 0, st>>>(width, height, image, target, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
+                                   d_image, d_soft);
+  return check_launch("k_ssim_bwd");
+}

@@ -1,0 +1,706 @@
+// Stages 3 and 4: 16x16-tile alpha-blend forward and the two backward layouts
+// (rasterize/kernels.py:31-353), plus the float64 guard-band fix-up.
+//
+// Forward: one CTA per tile, one thread per pixel, splat batches staged in
+// shared memory, block-wide early exit on transmittance.  Every 32 walked
+// slots each live pixel checkpoints (T, C_front) so the splat-parallel
+// backward can start any 32-splat bucket without replaying the tile.
+//
+// Guard band: the fp32 walk flags a pixel when any discrete
+// decision (power>0 skip, alpha >= 1/255 gate, alpha > 0.99 cap, T(1-a) < 1e-4
+// termination) is within `band` (relative) of its threshold.  Flagged pixels
+// are re-walked in float64 by one warp each (forward fix-up) and their
+// gradient rows are added by an fp64 pixel walk (backward fix-up); the fp32
+// backward kernels skip them, so fp32 never has to agree with fp64 near a
+// threshold.
+#include "ssr_common.cuh"
+
+namespace ssr {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct RasterArgs {
+  int width, height, tiles_x, tiles_y;
+  float bg[3];
+  double bg64[3];
+  float band;
+  const double2* mean;
+  const float4* conic_opa;
+  const float4* color;
+  const double2* conic_opa64;
+  const double2* color64;
+  const int4* rect;
+  const uint32_t* offset;
+  const uint32_t* inst;
+  const int2* ranges;
+  float* image;
+  float* t_final;
+  int* n_walk;
+  uint8_t* term;
+  int* hard;
+  double* soft;
+  uint8_t* flagged;
+  int2* tile_info;
+  float4* ckpt;
+};
+
+// Splat-major position of the instance of field row g in tile (tx, ty).
+__device__ __forceinline__ uint32_t inst_row(const RasterArgs& a, uint32_t g, int tx, int ty) {
+  const int4 r = a.rect[g];
+  return a.offset[g] + (uint32_t)((ty - r.y) * (r.z - r.x) + (tx - r.x));
+}
+
+__device__ __forceinline__ size_t ckpt_base(int s0, int t) { return ((size_t)(s0 >> 5) + (size_t)t) * TILE_PX; }
+
+// ------------------------------------------------------------------ forward (fp32)
+__global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int x00 = tx * TILE, y00 = ty * TILE;
+  const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
+  const bool inside = px < a.width && py < a.height;
+  const int2 rg = a.ranges[t];
+  const int s0 = rg.x, s1 = rg.y;
+  const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
+  const float band = a.band;
+
+  __shared__ float4 sA[TILE_PX];
+  __shared__ float4 sB[TILE_PX];
+  __shared__ float sC[TILE_PX];
+  __shared__ int sMax[8];
+
+  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, sdev = 0.f;
+  double sbig = 0.0;
+  int hard = 0, nwk = s1 - s0, scnt = 0;
+  bool term = false, flag = false, done = !inside;
+  float4* ck = a.ckpt + ckpt_base(s0, t) + tid;
+
+  for (int base = s0; base < s1; base += TILE_PX) {
+    if (__syncthreads_count(done) == TILE_PX) break;
+    const int s = base + tid;
+    if (s < s1) {
+      const uint32_t g = a.inst[s];
+      const double2 m = a.mean[g];
+      const float4 co = a.conic_opa[g];
+      const float4 col = a.color[g];
+      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), co.x, co.y);
+      sB[tid] = make_float4(co.z, co.w, col.x, col.y);
+      sC[tid] = col.z;
+    }
+    __syncthreads();
+    if (!done) {
+      const int n = min(TILE_PX, s1 - base);
+      const int k0 = base - s0;
+      for (int j = 0; j < n; j++) {
+        const int k = k0 + j;
+        if ((k & 31) == 0 && k) {
+          ck[(size_t)(k >> 5) * TILE_PX] = make_float4(T, c0, c1, c2);
+          sbig += (double)sdev;
+          sdev = 0.f;
+        }
+        const float4 A = sA[j];
+        const float4 B = sB[j];
+        const float dx = fpx - A.x, dy = fpy - A.y;
+        float q1;
+        const float power = pair_power(dx, dy, A.z, A.w, B.x, q1);
+        if (power > -1e-6f * q1 && q1 != 0.f) {  // near the power > 0 skip decision
+          flag = true;
+          break;
+        }
+        if (power > 0.f) continue;
+        float alpha = pair_alpha(B.y, power);
+        if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
+          flag = true;
+          break;
+        }
+        alpha = fminf(alpha, ALPHA_CAP_F);
+        const float y = __fmul_rn(alpha, 100.f);
+        if (y < SOFT_Y0) {
+          scnt++;
+          sdev += soft_dev_poly(y);
+        } else {
+          sbig += (double)soft_sigmoid_accurate(alpha);
+        }
+        if (alpha < ALPHA_MIN_F) continue;
+        const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
+        if (fabsf(test - T_EPS_F) < T_EPS_F * 2.f * band) {
+          flag = true;
+          break;
+        }
+        if (test < T_EPS_F) {
+          term = true;
+          nwk = k + 1;
+          break;
+        }
+        const float w = __fmul_rn(alpha, T);
+        c0 = __fmaf_rn(B.z, w, c0);
+        c1 = __fmaf_rn(B.w, w, c1);
+        c2 = __fmaf_rn(sC[j], w, c2);
+        hard++;
+        T = test;
+      }
+      if (flag || term) done = true;
+    }
+  }
+  if (inside) {
+    const size_t pix = (size_t)py * a.width + px;
+    a.image[pix * 3 + 0] = c0 + a.bg[0] * T;
+    a.image[pix * 3 + 1] = c1 + a.bg[1] * T;
+    a.image[pix * 3 + 2] = c2 + a.bg[2] * T;
+    a.t_final[pix] = T;
+    a.n_walk[pix] = nwk;
+    a.term[pix] = term ? 1 : 0;
+    a.hard[pix] = hard;
+    a.soft[pix] = (double)scnt * SOFT_S0 + (sbig + (double)sdev);
+    a.flagged[pix] = flag ? 1 : 0;
+  }
+  // per-tile (max n_walk over unflagged pixels, flagged count)
+  int mw = (inside && !flag) ? nwk : 0;
+  for (int o = 16; o > 0; o >>= 1) mw = max(mw, __shfl_xor_sync(FULL, mw, o));
+  if ((tid & 31) == 0) sMax[tid >> 5] = mw;
+  const int nflag = __syncthreads_count(inside && flag);
+  if (tid == 0) {
+    int m = 0;
+    for (int w = 0; w < 8; w++) m = max(m, sMax[w]);
+    a.tile_info[t] = make_int2(m, nflag);
+  }
+}
+
+// ------------------------------------------------------------------ fp64 pixel walk (warp)
+__device__ __forceinline__ double warp_sum64(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+struct Slot64 {
+  bool valid, skip, capped, cand;
+  double alpha, sv, dx, dy, qa, qb, qc, opa, col[3];
+  uint32_t g;
+};
+
+// kernels.py:68-89 for one slot in float64, mirroring the reference's op order.
+__device__ __forceinline__ void slot64(const RasterArgs& a, int s, int s1, double xx, double yy, Slot64& q) {
+  q.valid = s < s1;
+  q.skip = true;
+  q.cand = false;
+  q.capped = false;
+  q.alpha = 0.0;
+  q.sv = 0.0;
+  if (!q.valid) return;
+  q.g = a.inst[s];
+  const double2 m = a.mean[q.g];
+  const double2 c0 = a.conic_opa64[2 * q.g], c1 = a.conic_opa64[2 * q.g + 1];
+  q.qa = c0.x;
+  q.qb = c0.y;
+  q.qc = c1.x;
+  q.opa = c1.y;
+  q.dx = __dsub_rn(xx, m.x);
+  q.dy = __dsub_rn(yy, m.y);
+  const double t1 = __dmul_rn(__dmul_rn(q.qa, q.dx), q.dx);
+  const double t2 = __dmul_rn(__dmul_rn(q.qc, q.dy), q.dy);
+  const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), __dmul_rn(__dmul_rn(q.qb, q.dx), q.dy));
+  if (power > 0.0) return;
+  q.skip = false;
+  double alpha = __dmul_rn(q.opa, exp(power));
+  q.capped = alpha > ALPHA_CAP;
+  if (q.capped) alpha = ALPHA_CAP;
+  q.alpha = alpha;
+  q.sv = 1.0 / (1.0 + exp(-(alpha - ALPHA_MIN) / SOFT_TAU));
+  q.cand = alpha >= ALPHA_MIN;
+  const double2 k0 = a.color64[2 * q.g], k1 = a.color64[2 * q.g + 1];
+  q.col[0] = k0.x;
+  q.col[1] = k0.y;
+  q.col[2] = k1.x;
+}
+
+struct Pix64 {
+  double T, C[3], soft;
+  int hard, nw, term;
+};
+
+// Front-to-back walk of one pixel by one warp (lanes = 32 consecutive slots).
+__device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, double yy, Pix64& r) {
+  const int lane = threadIdx.x & 31;
+  double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, soft = 0.0;
+  int hard = 0, nw = s1 - s0, term = 0;
+  for (int cb = s0; cb < s1; cb += 32) {
+    Slot64 q;
+    slot64(a, cb + lane, s1, xx, yy, q);
+    const double f = q.cand ? (1.0 - q.alpha) : 1.0;
+    double P = f;
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(FULL, P, d);
+      if (lane >= d) P *= o;
+    }
+    double Pex = __shfl_up_sync(FULL, P, 1);
+    if (lane == 0) Pex = 1.0;
+    const double Tb = T * Pex;
+    const bool tc = q.cand && (Tb * (1.0 - q.alpha) < T_EPS);
+    const unsigned tm = __ballot_sync(FULL, tc);
+    const int tl = tm ? __ffs(tm) - 1 : 32;
+    const bool bl = q.cand && lane < tl;
+    const double wgt = bl ? q.alpha * Tb : 0.0;
+    C0 += warp_sum64(bl ? q.col[0] * wgt : 0.0);
+    C1 += warp_sum64(bl ? q.col[1] * wgt : 0.0);
+    C2 += warp_sum64(bl ? q.col[2] * wgt : 0.0);
+    soft += warp_sum64((!q.skip && lane <= tl) ? q.sv : 0.0);
+    hard += __popc(__ballot_sync(FULL, bl));
+    if (tm) {
+      term = 1;
+      nw = cb - s0 + tl + 1;
+      T = __shfl_sync(FULL, Tb, tl);
+      break;
+    }
+    T = T * __shfl_sync(FULL, P, 31);
+  }
+  r.T = T;
+  r.C[0] = C0;
+  r.C[1] = C1;
+  r.C[2] = C2;
+  r.soft = soft;
+  r.hard = hard;
+  r.nw = nw;
+  r.term = term;
+}
+
+// Forward fix-up: one warp per tile, flagged pixels re-walked in float64.
+__global__ void __launch_bounds__(32) k_forward_fixup(RasterArgs a) {
+  const int t = blockIdx.x;
+  const int2 info = a.tile_info[t];
+  if (info.y == 0) return;
+  const int lane = threadIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int2 rg = a.ranges[t];
+  int maxw = info.x;
+  for (int p = 0; p < TILE_PX; p++) {
+    const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
+    if (px >= a.width || py >= a.height) continue;
+    const size_t pix = (size_t)py * a.width + px;
+    if (!a.flagged[pix]) continue;
+    Pix64 r;
+    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r);
+    if (lane == 0) {
+      a.image[pix * 3 + 0] = (float)(r.C[0] + a.bg64[0] * r.T);
+      a.image[pix * 3 + 1] = (float)(r.C[1] + a.bg64[1] * r.T);
+      a.image[pix * 3 + 2] = (float)(r.C[2] + a.bg64[2] * r.T);
+      a.t_final[pix] = (float)r.T;
+      a.n_walk[pix] = r.nw;
+      a.term[pix] = (uint8_t)r.term;
+      a.hard[pix] = r.hard;
+      a.soft[pix] = r.soft;
+    }
+    maxw = max(maxw, r.nw);
+  }
+  if (lane == 0) a.tile_info[t].x = maxw;
+}
+
+// ------------------------------------------------------------------ backward, splat-parallel (fp32)
+// Taming-style: one warp per (tile, 32-splat bucket); lane l owns slot
+// 32b+l and accumulates its 9 gradient terms in registers while the 256
+// pixels stream through the warp as a systolic pipeline: at step i lane l
+// handles pixel i-l and receives that pixel's running (T, H = w.C_front)
+// from lane l-1 by shuffle.  Lane 0 seeds each pixel from the forward's
+// bucket checkpoint.  No atomics; each instance row is written once.
+__global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
+                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int2 rg = a.ranges[t];
+  const int s0 = rg.x, len = rg.y - rg.x;
+  if (len == 0) return;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int x00 = tx * TILE, y00 = ty * TILE;
+  const int maxw = a.tile_info[t].x;
+
+  __shared__ float4 sW[TILE_PX];  // (dL/dr, dL/dg, dL/db, dL/dsoft)
+  __shared__ float sWimg[TILE_PX];  // w . image
+  __shared__ int sNW[TILE_PX];  // n_walk << 1 | terminated  (0 = skip pixel)
+  __shared__ float4 sCk[8][TILE_PX];
+  {
+    const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
+    int nwt = 0;
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+    float wimg = 0.f;
+    if (px < a.width && py < a.height) {
+      const size_t pix = (size_t)py * a.width + px;
+      if (!a.flagged[pix]) nwt = (a.n_walk[pix] << 1) | (a.term[pix] ? 1 : 0);
+      w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
+      wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
+    }
+    sW[tid] = w;
+    sWimg[tid] = wimg;
+    sNW[tid] = nwt;
+  }
+  __syncthreads();
+
+  const int nb = (maxw + 31) >> 5;
+  const float4* ckt = a.ckpt + ckpt_base(s0, t);
+  for (int b = warp; b < nb; b += 8) {
+    if (b > 0) {
+      for (int p = lane; p < TILE_PX; p += 32) sCk[warp][p] = ckt[(size_t)b * TILE_PX + p];
+    }
+    __syncwarp();
+    const int k = b * 32 + lane;
+    const bool live = k < maxw;
+    float mrx = 0.f, mry = 0.f, ca = 0.f, cb = 0.f, cc = 0.f, opa = 0.f, cr = 0.f, cg = 0.f, cbl = 0.f;
+    uint32_t orow = 0;
+    if (live) {
+      const uint32_t g = a.inst[s0 + k];
+      const double2 m = a.mean[g];
+      const float4 co = a.conic_opa[g];
+      const float4 col = a.color[g];
+      mrx = (float)(m.x - (double)x00);
+      mry = (float)(m.y - (double)y00);
+      ca = co.x;
+      cb = co.y;
+      cc = co.z;
+      opa = co.w;
+      cr = col.x;
+      cg = col.y;
+      cbl = col.z;
+      orow = inst_row(a, g, tx, ty);
+    }
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
+    float T = 1.f, H = 0.f;
+    for (int i = 0; i < TILE_PX + 31; i++) {
+      float Tin = __shfl_up_sync(FULL, T, 1);
+      float Hin = __shfl_up_sync(FULL, H, 1);
+      if (lane == 0 && i < TILE_PX) {
+        if (b == 0) {
+          Tin = 1.f;
+          Hin = 0.f;
+        } else {
+          const float4 c = sCk[warp][i];
+          const float4 w = sW[i];
+          Tin = c.x;
+          Hin = w.x * c.y + w.y * c.z + w.z * c.w;
+        }
+      }
+      T = Tin;
+      H = Hin;
+      const int p = i - lane;
+      if (!live || p < 0 || p >= TILE_PX) continue;
+      const int nwt = sNW[p];
+      const int nw = nwt >> 1;
+      if (k >= nw) continue;
+      const float dx = (float)(p & 15) - mrx, dy = (float)(p >> 4) - mry;
+      float q1;
+      const float power = pair_power(dx, dy, ca, cb, cc, q1);
+      if (power > 0.f) continue;
+      const float araw = pair_alpha(opa, power);
+      const bool capped = araw > ALPHA_CAP_F;
+      const float alpha = capped ? ALPHA_CAP_F : araw;
+      const bool blended = alpha >= ALPHA_MIN_F && !((nwt & 1) && k == nw - 1);
+      const float4 w = sW[p];
+      float dlda = 0.f;
+      if (blended) {
+        const float wc = w.x * cr + w.y * cg + w.z * cbl;
+        const float aT = alpha * T;
+        g0 += aT * w.x;
+        g1 += aT * w.y;
+        g2 += aT * w.z;
+        const float one_m = __fsub_rn(1.f, alpha);
+        const float sdot = sWimg[p] - H - aT * wc;  // w . (colour behind this splat)
+        dlda = T * wc - __fdividef(sdot, one_m);
+        H += aT * wc;
+        T = __fmul_rn(T, one_m);
+      }
+      if (!capped) {
+        const float sv = soft_sigmoid(alpha);
+        const float gsoft = w.w * sv * (1.f - sv) * 100.f;
+        g3 += (dlda + gsoft) * alpha * (1.f - opa);
+        if (blended) {
+          const float gp = dlda * alpha;
+          g4 += gp * (ca * dx + cb * dy);
+          g5 += gp * (cb * dx + cc * dy);
+          g6 += gp * (-0.5f * dx * dx);
+          g7 += gp * (-dx * dy);
+          g8 += gp * (-0.5f * dy * dy);
+        }
+      }
+    }
+    if (live) {
+      float* r = rows + (size_t)orow * 9;
+      r[0] = g0;
+      r[1] = g1;
+      r[2] = g2;
+      r[3] = g3;
+      r[4] = g4;
+      r[5] = g5;
+      r[6] = g6;
+      r[7] = g7;
+      r[8] = g8;
+    }
+  }
+  // rows of slots no pixel walked
+  for (int k = maxw + tid; k < len; k += blockDim.x) {
+    const uint32_t g = a.inst[s0 + k];
+    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
+    for (int c = 0; c < 9; c++) r[c] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ backward, pixel-parallel (fp32)
+// The no_splat_parallel ablation (pipeline.py:130-131): thread per pixel,
+// each slot's 9 terms reduced across the warp by shuffles, per-warp partials
+// summed in a fixed order (deterministic), one row write per slot.
+__global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const float* __restrict__ d_image,
+                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int2 rg = a.ranges[t];
+  const int s0 = rg.x, len = rg.y - rg.x;
+  if (len == 0) return;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int x00 = tx * TILE, y00 = ty * TILE;
+  const int maxw = a.tile_info[t].x;
+  __shared__ float4 sA[32], sB[32];
+  __shared__ float sC[32];
+  __shared__ uint32_t sRow[32];
+  __shared__ float part[8][32][9];
+
+  const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
+  int nw = 0, term = 0;
+  float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+  float wimg = 0.f;
+  if (px < a.width && py < a.height) {
+    const size_t pix = (size_t)py * a.width + px;
+    if (!a.flagged[pix]) {
+      nw = a.n_walk[pix];
+      term = a.term[pix];
+    }
+    w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
+    wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
+  }
+  const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
+  float T = 1.f, H = 0.f;
+  for (int kb = 0; kb < maxw; kb += 32) {
+    if (tid < 32 && kb + tid < maxw) {
+      const uint32_t g = a.inst[s0 + kb + tid];
+      const double2 m = a.mean[g];
+      const float4 co = a.conic_opa[g];
+      const float4 col = a.color[g];
+      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), co.x, co.y);
+      sB[tid] = make_float4(co.z, co.w, col.x, col.y);
+      sC[tid] = col.z;
+      sRow[tid] = inst_row(a, g, tx, ty);
+    }
+    __syncthreads();
+    const int nc = min(32, maxw - kb);
+    for (int j = 0; j < nc; j++) {
+      const int k = kb + j;
+      float c[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (k < nw) {
+        const float4 A = sA[j], B = sB[j];
+        const float dx = fpx - A.x, dy = fpy - A.y;
+        float q1;
+        const float power = pair_power(dx, dy, A.z, A.w, B.x, q1);
+        if (power <= 0.f) {
+          const float araw = pair_alpha(B.y, power);
+          const bool capped = araw > ALPHA_CAP_F;
+          const float alpha = capped ? ALPHA_CAP_F : araw;
+          const bool blended = alpha >= ALPHA_MIN_F && !(term && k == nw - 1);
+          float dlda = 0.f;
+          if (blended) {
+            const float wc = w.x * B.z + w.y * B.w + w.z * sC[j];
+            const float aT = alpha * T;
+            c[0] = aT * w.x;
+            c[1] = aT * w.y;
+            c[2] = aT * w.z;
+            const float one_m = __fsub_rn(1.f, alpha);
+            dlda = T * wc - __fdividef(wimg - H - aT * wc, one_m);
+            H += aT * wc;
+            T = __fmul_rn(T, one_m);
+          }
+          if (!capped) {
+            const float sv = soft_sigmoid(alpha);
+            c[3] = (dlda + w.w * sv * (1.f - sv) * 100.f) * alpha * (1.f - B.y);
+            if (blended) {
+              const float gp = dlda * alpha;
+              c[4] = gp * (A.z * dx + A.w * dy);
+              c[5] = gp * (A.w * dx + B.x * dy);
+              c[6] = gp * (-0.5f * dx * dx);
+              c[7] = gp * (-dx * dy);
+              c[8] = gp * (-0.5f * dy * dy);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 9; q++) {
+        float v = c[q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        c[q] = v;
+      }
+      if (lane == 0)
+        for (int q = 0; q < 9; q++) part[warp][j][q] = c[q];
+    }
+    __syncthreads();
+    for (int e = tid; e < nc * 9; e += blockDim.x) {
+      const int j = e / 9, q = e % 9;
+      float v = 0.f;
+      for (int ww = 0; ww < 8; ww++) v += part[ww][j][q];
+      rows[(size_t)sRow[j] * 9 + q] = v;
+    }
+    __syncthreads();
+  }
+  for (int k = maxw + tid; k < len; k += blockDim.x) {
+    const uint32_t g = a.inst[s0 + k];
+    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
+    for (int c = 0; c < 9; c++) r[c] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ backward fix-up (fp64)
+// One warp per tile with flagged pixels; pixels in order, lanes over slots.
+// Adds the float64 pixel-walk gradient terms (kernels.py:149-193 semantics,
+// front-to-back) into the rows the fp32 kernel wrote.  Sequential over pixels
+// and lane-disjoint within a pixel, so no atomics and deterministic.
+__global__ void __launch_bounds__(32) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
+                                                       const float* __restrict__ d_soft, float* __restrict__ rows) {
+  const int t = blockIdx.x;
+  if (a.tile_info[t].y == 0) return;
+  const int lane = threadIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int2 rg = a.ranges[t];
+  const int s0 = rg.x, s1 = rg.y;
+  for (int p = 0; p < TILE_PX; p++) {
+    const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
+    if (px >= a.width || py >= a.height) continue;
+    const size_t pix = (size_t)py * a.width + px;
+    if (!a.flagged[pix]) continue;
+    Pix64 r;
+    const double xx = (double)px, yy = (double)py;
+    walk_pixel64(a, s0, s1, xx, yy, r);
+    const double w0 = d_image[pix * 3], w1 = d_image[pix * 3 + 1], w2 = d_image[pix * 3 + 2];
+    const double ws = d_soft ? (double)d_soft[pix] : 0.0;
+    const double wimg = w0 * (r.C[0] + a.bg64[0] * r.T) + w1 * (r.C[1] + a.bg64[1] * r.T) +
+                        w2 * (r.C[2] + a.bg64[2] * r.T);
+    double T = 1.0, H = 0.0;
+    const int send = s0 + r.nw;
+    for (int cb = s0; cb < send; cb += 32) {
+      Slot64 q;
+      const int s = cb + lane;
+      slot64(a, s, send, xx, yy, q);
+      const int k = s - s0;
+      const bool bl = q.cand && !(r.term && k == r.nw - 1);
+      const double f = bl ? (1.0 - q.alpha) : 1.0;
+      double P = f;
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(FULL, P, d);
+        if (lane >= d) P *= o;
+      }
+      double Pex = __shfl_up_sync(FULL, P, 1);
+      if (lane == 0) Pex = 1.0;
+      const double Tb = T * Pex;
+      const double wc = bl ? (w0 * q.col[0] + w1 * q.col[1] + w2 * q.col[2]) : 0.0;
+      const double e = bl ? q.alpha * Tb * wc : 0.0;
+      double E = e;  // inclusive prefix sum of w.(c alpha T)
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(FULL, E, d);
+        if (lane >= d) E += o;
+      }
+      const double Hb = H + (E - e);
+      if (q.valid && !q.skip) {
+        double c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        double dlda = 0.0;
+        if (bl) {
+          const double aT = q.alpha * Tb;
+          c[0] = aT * w0;
+          c[1] = aT * w1;
+          c[2] = aT * w2;
+          dlda = Tb * wc - (wimg - Hb - aT * wc) / (1.0 - q.alpha);
+        }
+        if (!q.capped) {
+          c[3] = (dlda + ws * q.sv * (1.0 - q.sv) / SOFT_TAU) * q.alpha * (1.0 - q.opa);
+          if (bl) {
+            const double gp = dlda * q.alpha;
+            c[4] = gp * (q.qa * q.dx + q.qb * q.dy);
+            c[5] = gp * (q.qb * q.dx + q.qc * q.dy);
+            c[6] = gp * (-0.5 * q.dx * q.dx);
+            c[7] = gp * (-q.dx * q.dy);
+            c[8] = gp * (-0.5 * q.dy * q.dy);
+          }
+        }
+        float* row = rows + (size_t)inst_row(a, q.g, tx, ty) * 9;
+        for (int j = 0; j < 9; j++) row[j] += (float)c[j];
+      }
+      H += __shfl_sync(FULL, E, 31);
+      T *= __shfl_sync(FULL, P, 31);
+      __syncwarp();
+    }
+  }
+}
+
+static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* ranges, const ssr_frame& f,
+                            float band) {
+  RasterArgs a;
+  a.width = f.width;
+  a.height = f.height;
+  a.tiles_x = f.tiles_x;
+  a.tiles_y = f.tiles_y;
+  for (int i = 0; i < 3; i++) {
+    a.bg[i] = f.bg[i];
+    a.bg64[i] = (double)f.bg[i];
+  }
+  a.band = band;
+  a.mean = (const double2*)sp.mean;
+  a.conic_opa = (const float4*)sp.conic_opa;
+  a.color = (const float4*)sp.color;
+  a.conic_opa64 = (const double2*)sp.conic_opa64;
+  a.color64 = (const double2*)sp.color64;
+  a.rect = (const int4*)sp.rect;
+  a.offset = sp.offset;
+  a.inst = inst;
+  a.ranges = (const int2*)ranges;
+  a.image = f.image;
+  a.t_final = f.t_final;
+  a.n_walk = f.n_walk;
+  a.term = f.terminated;
+  a.hard = f.hard_count;
+  a.soft = f.soft_count;
+  a.flagged = f.flagged;
+  a.tile_info = (int2*)f.tile_info;
+  a.ckpt = (float4*)f.ckpt;
+  return a;
+}
+
+}  // namespace ssr
+
+using namespace ssr;
+
+extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss, const int32_t* tile_ranges,
+                           ssr_frame frame, float band, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_tiles = frame.tiles_x * frame.tiles_y;
+  if (n_tiles <= 0 || frame.width <= 0 || frame.height <= 0 || m < 0 || !(band >= 0.f)) {
+    set_error("ssr_forward: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, band);
+  k_forward<<<n_tiles, TILE_PX, 0, st>>>(a);
+  SSR_TRY(check_launch("k_forward"));
+  k_forward_fixup<<<n_tiles, 32, 0, st>>>(a);
+  return check_launch("k_forward_fixup");
+}
+
+extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
+                            const int32_t* tile_ranges, ssr_frame frame, const float* d_image, const float* d_soft,
+                            float* inst_rows, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_tiles = frame.tiles_x * frame.tiles_y;
+  if (n_tiles <= 0 || (layout != 0 && layout != 1) || !d_image) {
+    set_error("ssr_backward: invalid argument (layout must be 0=splat or 1=pixel)");
+    return SSR_ERR_INVALID;
+  }
+  if (m == 0) return SSR_OK;
+  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f);
+  if (layout == 0)
+    k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+  else
+    k_backward_pixel<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+  SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
+  k_backward_fixup<<<n_tiles, 32, 0, st>>>(a, d_image, d_soft, inst_rows);
+  return check_launch("k_backward_fixup");
+}

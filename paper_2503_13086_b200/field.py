@@ -1,0 +1,269 @@
+"""GPU-resident Gaussian field (mirrors field.py:164-375 of the reference).
+
+Parameters live in ONE flat float32 CUDA buffer, class-major:
+``[positions 3N | rotations 4N | log_scales 3N | opacity_logits N | sh 3KN]``.
+The reference attribute names (``positions``, ``rotations``, ``log_scales``,
+``opacity_logits``, ``sh``) are views into it with the reference shapes
+((N,3), (N,4), (N,3), (N,), (N,3,K) channel-major).  ``generation`` counts
+structural changes exactly like the reference so stale renders are rejected.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidParameter
+
+SH_C0 = 0.28209479177387814
+CLASSES = ("positions", "rotations", "log_scales", "opacity_logits", "sh")
+
+
+def row_floats(sh_degree: int) -> int:
+    """Parameter floats per Gaussian: 11 + 3K (59 at SH3)."""
+    return 11 + 3 * (sh_degree + 1) ** 2
+
+
+def class_slices(n: int, k: int):
+    """(start, width) of each class inside the flat buffer of n rows."""
+    w = (3, 4, 3, 1, 3 * k)
+    out, off = [], 0
+    for wi in w:
+        out.append((off, wi))
+        off += wi * n
+    return out
+
+
+@dataclass
+class DensifyOptions:
+    grad_threshold: float = 2e-4
+    percent_dense: float = 0.01
+    scene_extent: float = 1.0
+    prune_opacity: float = 0.005
+    split_scale_shrink: float = 1.6
+
+
+@dataclass
+class DensifySummary:
+    cloned: int
+    split: int
+    pruned: int
+    keep_mask: np.ndarray  # over the pre-call rows; False = removed
+    n_added: int
+
+    @property
+    def changed(self) -> bool:
+        return self.cloned > 0 or self.split > 0 or self.pruned > 0
+
+
+@dataclass
+class SparsePoint:
+    position: np.ndarray
+    color: np.ndarray
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64).reshape(3)
+        self.color = np.asarray(self.color, dtype=np.float64).reshape(3)
+
+    @property
+    def finite(self) -> bool:
+        return bool(np.isfinite(self.position).all() and np.isfinite(self.color).all())
+
+
+class GaussianField:
+    """Growable set of Gaussians stored struct-of-arrays in one flat CUDA buffer."""
+
+    def __init__(self, sh_degree: int = 0, device=None):
+        if not 0 <= sh_degree <= 3:
+            raise InvalidParameter(f"sh_degree must be in 0..3, got {sh_degree}")
+        self.sh_degree = int(sh_degree)
+        self.device = _lib.require_cuda() if device is None else torch.device(device)
+        self._n = 0
+        self._flat = torch.zeros(0, dtype=torch.float32, device=self.device)
+        self.generation = 0
+
+    # ------------------------------------------------------------ construction
+    @classmethod
+    def from_arrays(cls, positions, rotations, log_scales, opacity_logits, sh, device=None) -> "GaussianField":
+        sh_t = torch.as_tensor(np.asarray(sh) if not torch.is_tensor(sh) else sh)
+        k = sh_t.shape[2]
+        deg = int(round(math.sqrt(k))) - 1
+        f = cls(sh_degree=deg, device=device)
+        arrs = [torch.as_tensor(a if torch.is_tensor(a) else np.asarray(a)) for a in
+                (positions, rotations, log_scales, opacity_logits, sh)]
+        n = arrs[0].shape[0]
+        f._flat = torch.cat([a.reshape(-1).to(device=f.device, dtype=torch.float32) for a in arrs]).contiguous()
+        f._n = n
+        if f._flat.numel() != n * row_floats(deg):
+            raise InvalidParameter("parameter arrays have inconsistent shapes")
+        return f
+
+    @classmethod
+    def from_host(cls, hp, device=None) -> "GaussianField":
+        """From a scenes.HostParams / any object with the five attributes."""
+        return cls.from_arrays(*(getattr(hp, k) for k in CLASSES), device=device)
+
+    # ------------------------------------------------------------ views
+    def __len__(self):
+        return self._n
+
+    @property
+    def n_sh_coeffs(self) -> int:
+        return (self.sh_degree + 1) ** 2
+
+    @property
+    def flat(self) -> torch.Tensor:
+        return self._flat
+
+    def _view(self, i):
+        n, k = self._n, self.n_sh_coeffs
+        off, w = class_slices(n, k)[i]
+        v = self._flat[off: off + w * n]
+        shape = ((n, 3), (n, 4), (n, 3), (n,), (n, 3, k))[i]
+        return v.view(shape)
+
+    def _assign(self, i, value):
+        dst = self._view(i)
+        src = torch.as_tensor(value if torch.is_tensor(value) else np.asarray(value))
+        if tuple(src.shape) != tuple(dst.shape):
+            raise InvalidParameter(f"{CLASSES[i]} must have shape {tuple(dst.shape)}, got {tuple(src.shape)}")
+        dst.copy_(src.to(dtype=torch.float32))
+
+    positions = property(lambda s: s._view(0), lambda s, v: s._assign(0, v))
+    rotations = property(lambda s: s._view(1), lambda s, v: s._assign(1, v))
+    log_scales = property(lambda s: s._view(2), lambda s, v: s._assign(2, v))
+    opacity_logits = property(lambda s: s._view(3), lambda s, v: s._assign(3, v))
+    sh = property(lambda s: s._view(4), lambda s, v: s._assign(4, v))
+
+    def opacities(self):
+        return torch.sigmoid(self.opacity_logits)
+
+    def scales(self):
+        return torch.exp(self.log_scales)
+
+    def covariances(self):
+        """Sigma = R S S^T R^T per Gaussian (field.py:71-75), float64."""
+        q = self.rotations.double()
+        q = q / q.norm(dim=1, keepdim=True)
+        w, x, y, z = q.unbind(1)
+        r = torch.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                         2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                         2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], 1).view(-1, 3, 3)
+        m = r * torch.exp(self.log_scales.double())[:, None, :]
+        return m @ m.transpose(1, 2)
+
+    def to_numpy(self) -> dict:
+        return {k: getattr(self, k).detach().cpu().numpy() for k in CLASSES}
+
+    def checksum(self) -> str:
+        h = hashlib.sha256()
+        for k in CLASSES:
+            h.update(np.ascontiguousarray(getattr(self, k).detach().cpu().numpy()).tobytes())
+        return h.hexdigest()
+
+    def _check_finite(self):
+        if not bool(torch.isfinite(self._flat).all()):
+            raise InvalidParameter("non-finite values in field parameters")
+
+    # ------------------------------------------------------------ structure
+    def insert_points(self, points, init_opacity: float = 0.1) -> int:
+        """Append one Gaussian per sparse point (field.py:258-301).
+
+        Scale init = mean distance to the 3 nearest points of the union of the
+        existing centres and the new points (exact, brute force on the GPU in
+        row blocks); identity rotation; logit(init_opacity); DC from colour.
+        """
+        usable = [p for p in points if p.finite]
+        n_new = len(usable)
+        if n_new == 0:
+            return 0
+        dev = self.device
+        new_pos = torch.tensor(np.stack([p.position for p in usable]), dtype=torch.float64, device=dev)
+        pool = torch.cat([self.positions.double(), new_pos]) if self._n else new_pos
+        if pool.shape[0] > 1:
+            k = min(4, pool.shape[0])
+            dists = []
+            for s in range(0, n_new, 4096):
+                d = torch.cdist(new_pos[s:s + 4096], pool)
+                dists.append(torch.topk(d, k, dim=1, largest=False).values[:, 1:].mean(dim=1))
+            mean_d = torch.clamp(torch.cat(dists), min=1e-7)
+        else:
+            mean_d = torch.full((n_new,), 0.1, dtype=torch.float64, device=dev)
+        K = self.n_sh_coeffs
+        log_scales = torch.log(mean_d)[:, None].repeat(1, 3)
+        rot = torch.zeros(n_new, 4, dtype=torch.float64, device=dev)
+        rot[:, 0] = 1.0
+        logit = torch.full((n_new,), math.log(init_opacity / (1.0 - init_opacity)), dtype=torch.float64, device=dev)
+        sh = torch.zeros(n_new, 3, K, dtype=torch.float64, device=dev)
+        cols = torch.tensor(np.stack([p.color for p in usable]), dtype=torch.float64, device=dev)
+        sh[:, :, 0] = (cols - 0.5) / SH_C0
+        self._append([new_pos, rot, log_scales, logit, sh])
+        self.generation += 1
+        self._check_finite()
+        return n_new
+
+    def _append(self, parts):
+        old = [getattr(self, k) for k in CLASSES] if self._n else None
+        n_add = parts[0].shape[0]
+        cat = []
+        for i, p in enumerate(parts):
+            p = p.to(dtype=torch.float32).reshape(n_add, -1)
+            if old is not None:
+                p = torch.cat([old[i].reshape(self._n, -1), p])
+            cat.append(p.reshape(-1))
+        self._flat = torch.cat(cat).contiguous()
+        self._n += n_add
+
+    def densify_and_prune(self, grad_stats, opts: DensifyOptions, rng, optimizer=None) -> DensifySummary:
+        """Clone/split hot Gaussians and prune transparent ones (field.py:303-375).
+
+        ``grad_stats`` is the averaged screen-gradient statistic (N,).  Split
+        children draw ``rng.standard_normal((2*n_split, 3))`` from the session
+        generator on the host (field.py:340) so RNG streams stay aligned.  When
+        ``optimizer`` is given its moments are remapped in the same kernel pass
+        (equivalent to optimizer.sync(...)).
+        """
+        stats = torch.as_tensor(grad_stats if torch.is_tensor(grad_stats) else np.asarray(grad_stats))
+        if stats.shape[0] != self._n:
+            raise InvalidParameter(f"grad_stats length {stats.shape[0]} != field size {self._n}")
+        n = self._n
+        if n == 0:
+            return DensifySummary(0, 0, 0, np.ones(0, dtype=bool), 0)
+        stats = stats.to(device=self.device, dtype=torch.float32).contiguous()
+        flags = torch.empty(n, dtype=torch.uint8, device=self.device)
+        counts = torch.empty(3, dtype=torch.int32, device=self.device)
+        st = _lib.stream_ptr()
+        _lib.call("ssr_densify_masks", n, self._flat.data_ptr(), self.sh_degree, stats.data_ptr(),
+                  float(opts.grad_threshold), float(opts.percent_dense * opts.scene_extent),
+                  float(opts.prune_opacity), flags.data_ptr(), counts.data_ptr(), st)
+        cl, sp, pr = (int(v) for v in counts.cpu().tolist())
+        keep = (flags & 1).bool()
+        keep_np = keep.cpu().numpy()
+        n_added = cl + 2 * sp
+        if not (cl or sp or pr):
+            return DensifySummary(0, 0, 0, keep_np, 0)
+        eps = torch.as_tensor(rng.standard_normal((2 * sp, 3)) if sp else np.zeros((1, 3)),
+                              dtype=torch.float64).to(self.device)
+        n_new = int(keep_np.sum()) + n_added
+        new = torch.empty(n_new * row_floats(self.sh_degree), dtype=torch.float32, device=self.device)
+        ws = torch.empty(_lib.query("ssr_densify_workspace", n), dtype=torch.uint8, device=self.device)
+        m_old = v_old = new_m = new_v = None
+        if optimizer is not None:
+            m_old, v_old = optimizer.m, optimizer.v
+            new_m, new_v = torch.empty_like(new), torch.empty_like(new)
+        _lib.call("ssr_densify_apply", n, n_new, self.sh_degree, self._flat.data_ptr(), _lib.ptr(m_old),
+                  _lib.ptr(v_old), flags.data_ptr(), eps.data_ptr(), float(math.log(opts.split_scale_shrink)),
+                  new.data_ptr(), _lib.ptr(new_m), _lib.ptr(new_v), ws.data_ptr(), ws.numel(), st)
+        self._flat = new
+        self._n = n_new
+        self.generation += 1
+        if optimizer is not None:
+            optimizer._adopt(self, new_m, new_v)
+        self._check_finite()
+        return DensifySummary(cl, sp, pr, keep_np, n_added)

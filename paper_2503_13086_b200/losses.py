@@ -1,0 +1,93 @@
+"""Training objective on device (mirrors losses.py:37-182 of the reference).
+
+``total_loss`` runs the fused L1 + (1 - SSIM) + load-balance kernels and
+returns device gradients; the scalar terms stay in a device buffer until read
+(reading a property synchronises), so a training loop needs no host round
+trip per iteration.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import InvalidParameter
+
+
+@dataclass
+class LossWeights:
+    l1: float = 0.47
+    ssim: float = 0.12
+    load: float = 0.41
+
+    def __post_init__(self):
+        for name in ("l1", "ssim", "load"):
+            v = getattr(self, name)
+            if not math.isfinite(v) or v < 0:
+                raise InvalidParameter(f"loss weight {name} must be finite and >= 0, got {v}")
+
+
+class LossBreakdown:
+    """d_image (H,W,3) / d_soft (H,W) device tensors plus lazily-read scalars."""
+
+    def __init__(self, values: torch.Tensor, d_image: torch.Tensor, d_soft: torch.Tensor):
+        self.values = values  # float64 device: l1, ssim_loss, load, total, hard_count_std
+        self.d_image = d_image
+        self.d_soft = d_soft
+        self._host = None
+
+    def _get(self, i):
+        if self._host is None:
+            self._host = self.values.cpu().tolist()
+        return float(self._host[i])
+
+    l1 = property(lambda s: s._get(0))
+    ssim_loss = property(lambda s: s._get(1))
+    load = property(lambda s: s._get(2))
+    total = property(lambda s: s._get(3))
+    hard_count_std = property(lambda s: s._get(4))
+
+
+class _Workspace:
+    cache = {}
+
+    @classmethod
+    def get(cls, w, h, dev):
+        key = (w, h, str(dev))
+        if key not in cls.cache:
+            cls.cache[key] = torch.empty(_lib.query("ssr_loss_workspace", w, h), dtype=torch.uint8, device=dev)
+        return cls.cache[key]
+
+
+def total_loss(rendered, target, output, weights: LossWeights) -> LossBreakdown:
+    """Weighted objective over one rendered view (losses.py:147-173)."""
+    rendered = torch.as_tensor(rendered)
+    target = torch.as_tensor(target)
+    if tuple(rendered.shape) != tuple(target.shape) or rendered.dim() != 3 or rendered.shape[2] != 3:
+        raise InvalidParameter(f"shape mismatch {tuple(rendered.shape)} vs {tuple(target.shape)}")
+    h, w = int(rendered.shape[0]), int(rendered.shape[1])
+    if h < 11 or w < 11:
+        raise InvalidParameter(f"image {h}x{w} smaller than the 11-tap SSIM window")
+    dev = output.image.device
+    x = rendered.to(device=dev, dtype=torch.float32).contiguous()
+    y = target.to(device=dev, dtype=torch.float32).contiguous()
+    soft = output.soft_count.to(dtype=torch.float64).contiguous()
+    hard = output.hard_count.to(dtype=torch.int32).contiguous()
+    d_image = torch.empty_like(x)
+    d_soft = torch.empty(soft.shape, dtype=torch.float32, device=dev)
+    vals = torch.empty(5, dtype=torch.float64, device=dev)
+    ws = _Workspace.get(w, h, dev)
+    _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), soft.data_ptr(), hard.data_ptr(), float(weights.l1),
+              float(weights.ssim), float(weights.load), d_image.data_ptr(), d_soft.data_ptr(), vals.data_ptr(),
+              ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    return LossBreakdown(vals, d_image, d_soft)
+
+
+def psnr(rendered, target) -> float:
+    rendered = torch.as_tensor(rendered).double()
+    target = torch.as_tensor(target).to(rendered.device).double()
+    mse = float(((rendered - target) ** 2).mean())
+    return float("inf") if mse == 0.0 else -10.0 * math.log10(mse)

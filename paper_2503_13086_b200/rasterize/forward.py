@@ -1,0 +1,76 @@
+"""Stage 3 host wrapper: ``render`` (forward.py:21-114 of the reference)."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..camera import CameraFrame
+from ..errors import InvalidParameter
+from .projection import ProjectedSplats, project_field
+
+# Relative guard band of the fp32 walk's discrete decisions; pixels inside it
+# are re-walked in float64.  The termination band is 2x this.
+GUARD_BAND = 1e-4
+
+
+@dataclass
+class RenderOutput:
+    """Rendered image plus the retained state the backward pass replays."""
+
+    image: torch.Tensor  # (H, W, 3) float32
+    t_final: torch.Tensor  # (H, W)
+    n_walk: torch.Tensor  # (H, W) int32
+    terminated: torch.Tensor  # (H, W) uint8
+    hard_count: torch.Tensor  # (H, W) int32
+    soft_count: torch.Tensor  # (H, W) float64
+    splats: ProjectedSplats
+    cam: CameraFrame
+    bg: np.ndarray
+    generation: int
+    workers: int = dc_field(default=1, repr=False)
+    flagged: torch.Tensor = dc_field(default=None, repr=False)  # (H, W) uint8 guard-band pixels
+    tile_info: torch.Tensor = dc_field(default=None, repr=False)  # (n_tiles, 2) int32
+    ckpt: torch.Tensor = dc_field(default=None, repr=False)  # bucket checkpoints (T, C_front)
+
+    @property
+    def n_visible(self) -> int:
+        return self.splats.n_visible
+
+    def frame_struct(self) -> _lib.SsrFrame:
+        f = _lib.SsrFrame()
+        f.width, f.height = self.cam.width, self.cam.height
+        f.tiles_x, f.tiles_y = self.splats.tiles_x, self.splats.tiles_y
+        for i in range(3):
+            f.bg[i] = float(self.bg[i])
+        for k in ("image", "t_final", "n_walk", "terminated", "hard_count", "soft_count", "flagged", "tile_info",
+                  "ckpt"):
+            t = getattr(self, k)
+            setattr(f, k, t.data_ptr() if t.numel() else None)
+        return f
+
+
+def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: float = GUARD_BAND) -> RenderOutput:
+    """Render the field from ``cam`` over a constant background colour."""
+    if workers < 1:
+        raise InvalidParameter(f"workers must be >= 1, got {workers}")
+    bg = np.asarray(bg, dtype=np.float64).reshape(3)
+    splats = project_field(field, cam)
+    dev = splats.tile_ranges.device
+    h, w = cam.height, cam.width
+    n_tiles = splats.tiles_x * splats.tiles_y
+    m = splats.n_instances
+    e = lambda *s, dt=torch.float32: torch.empty(s, dtype=dt, device=dev)
+    out = RenderOutput(
+        image=e(h, w, 3), t_final=e(h, w), n_walk=e(h, w, dt=torch.int32), terminated=e(h, w, dt=torch.uint8),
+        hard_count=e(h, w, dt=torch.int32), soft_count=e(h, w, dt=torch.float64), splats=splats, cam=cam, bg=bg,
+        generation=field.generation, workers=workers, flagged=e(h, w, dt=torch.uint8),
+        tile_info=e(n_tiles, 2, dt=torch.int32),
+        ckpt=e(int(_lib.load().ssr_ckpt_floats(m, n_tiles))),
+    )
+    _lib.call("ssr_forward", m, splats.struct(), splats.inst_gauss.data_ptr() if m else None,
+              splats.tile_ranges.data_ptr(), out.frame_struct(), float(band), _lib.stream_ptr())
+    return out

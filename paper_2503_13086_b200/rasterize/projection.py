@@ -1,0 +1,170 @@
+"""Stage 1-2 host wrapper: preprocess + tile binning (projection.py:24-191).
+
+``project_field`` returns a ``ProjectedSplats`` whose reference-named fields
+(``gauss_index``, ``means2d``, ``conics``, ``inst_splat``, ``tile_starts`` ...)
+are computed lazily from the device buffers the kernels use; the hot path
+itself only touches the N-indexed device arrays and the sorted instance list.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import torch
+
+from .. import _lib
+from ..camera import CameraFrame
+from ..errors import InvalidParameter
+
+TILE = 16
+ZNEAR = 0.2
+COV2D_DILATION = 0.3
+FRUSTUM_EXPAND = 1.3
+
+
+def tile_grid(width: int, height: int):
+    return (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
+
+
+@dataclass
+class ProjectedSplats:
+    """Device state of one projection (N-indexed) plus the sorted instances."""
+
+    n: int
+    sh_degree: int
+    tiles_x: int
+    tiles_y: int
+    bufs: dict  # name -> tensor (see ssr_splats in include/ssr.h)
+    inst_gauss: torch.Tensor  # (M,) int32 field row per sorted instance
+    tile_ranges: torch.Tensor  # (n_tiles, 2) int32 (start, end)
+    cam: CameraFrame
+    _src: tuple = dc_field(default=None, repr=False)  # (flat params, n, K) for aux
+    _cache: dict = dc_field(default_factory=dict, repr=False)
+
+    def struct(self) -> _lib.SsrSplats:
+        s = _lib.SsrSplats()
+        for k in ("mean", "conic_opa", "color", "conic_opa64", "color64", "depth", "rect", "tiles", "offset"):
+            setattr(s, k, self.bufs[k].data_ptr() if self.bufs[k].numel() else None)
+        return s
+
+    # ---------------------------------------------------------- reference-named views
+    @property
+    def n_instances(self) -> int:
+        return int(self.inst_gauss.numel())
+
+    @property
+    def visible_mask(self) -> torch.Tensor:
+        return self.bufs["tiles"][: self.n] > 0
+
+    @property
+    def gauss_index(self) -> torch.Tensor:
+        if "gi" not in self._cache:
+            self._cache["gi"] = torch.nonzero(self.visible_mask).flatten()
+        return self._cache["gi"]
+
+    @property
+    def n_visible(self) -> int:
+        return int(self.gauss_index.numel())
+
+    def _rows(self, name, cols, dtype=None):
+        t = self.bufs[name].view(self.n, -1)[self.gauss_index][:, cols]
+        return t if dtype is None else t.to(dtype)
+
+    means2d = property(lambda s: s._rows("mean", slice(0, 2)))
+    conics = property(lambda s: s._rows("conic_opa64", slice(0, 3)))
+    opacities = property(lambda s: s._rows("conic_opa64", 3))
+    colors = property(lambda s: s._rows("color64", slice(0, 3)))
+    depths = property(lambda s: s.bufs["depth"][s.gauss_index])
+
+    @property
+    def inst_splat(self) -> torch.Tensor:
+        """Visible-splat index per sorted instance (projection.py:50)."""
+        rank = torch.cumsum(self.visible_mask.to(torch.int64), 0) - 1
+        return rank[self.inst_gauss.long()]
+
+    @property
+    def tile_starts(self) -> torch.Tensor:
+        return self.tile_ranges[:, 0].long()
+
+    @property
+    def tile_ends(self) -> torch.Tensor:
+        return self.tile_ranges[:, 1].long()
+
+    def _aux(self):
+        if "aux" in self._cache:
+            return self._cache["aux"]
+        flat, n, k = self._src
+        from ..field import class_slices
+
+        sl = class_slices(n, k)
+        dev = flat.device
+        f64 = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)
+        a = dict(cam_points=f64(n, 3), clamp_mul=f64(n, 2), cov2d=f64(n, 3), cov3d_cam=f64(n, 3, 3),
+                 sh_dirs=f64(n, 3), sh_radii=f64(n), sh_lo=torch.zeros(n, 3, dtype=torch.uint8, device=dev),
+                 sh_hi=torch.zeros(n, 3, dtype=torch.uint8, device=dev), radii=f64(n))
+        cam = _lib.camera_struct(self.cam)
+        _lib.call("ssr_project_aux", cam, n, self.sh_degree, flat[sl[0][0]:].data_ptr(),
+                  flat[sl[1][0]:].data_ptr(), flat[sl[2][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(),
+                  self.bufs["tiles"].data_ptr(), *[a[x].data_ptr() for x in (
+                      "cam_points", "clamp_mul", "cov2d", "cov3d_cam", "sh_dirs", "sh_radii", "sh_lo", "sh_hi",
+                      "radii")], _lib.stream_ptr())
+        gi = self.gauss_index
+        out = {k2: v[gi] for k2, v in a.items()}
+        out["sh_lo"] = out["sh_lo"].bool()
+        out["sh_hi"] = out["sh_hi"].bool()
+        self._cache["aux"] = out
+        return out
+
+    cam_points = property(lambda s: s._aux()["cam_points"])
+    clamp_mul = property(lambda s: s._aux()["clamp_mul"])
+    cov2d = property(lambda s: s._aux()["cov2d"])
+    cov3d_cam = property(lambda s: s._aux()["cov3d_cam"])
+    sh_dirs = property(lambda s: s._aux()["sh_dirs"])
+    sh_radii = property(lambda s: s._aux()["sh_radii"])
+    sh_lo = property(lambda s: s._aux()["sh_lo"])
+    sh_hi = property(lambda s: s._aux()["sh_hi"])
+    radii = property(lambda s: s._aux()["radii"])
+
+
+def _alloc_splats(n: int, dev) -> dict:
+    e = lambda *s, dt=torch.float32: torch.empty(s, dtype=dt, device=dev)
+    return dict(mean=e(n, 2, dt=torch.float64), conic_opa=e(n, 4), color=e(n, 4),
+                conic_opa64=e(n, 4, dt=torch.float64), color64=e(n, 4, dt=torch.float64),
+                depth=e(n, dt=torch.float64), rect=e(n, 4, dt=torch.int32), tiles=e(n, dt=torch.int32),
+                offset=e(n, dt=torch.int32))
+
+
+def project_field(field, cam: CameraFrame) -> ProjectedSplats:
+    """Project every Gaussian, cull, bin into tiles and depth-sort (projection.py:69-191)."""
+    from ..field import class_slices
+
+    dev = _lib.require_cuda()
+    if not isinstance(cam, CameraFrame):
+        raise InvalidParameter("cam must be a CameraFrame")
+    n, k = len(field), field.n_sh_coeffs
+    tiles_x, tiles_y = tile_grid(cam.width, cam.height)
+    n_tiles = tiles_x * tiles_y
+    st = _lib.stream_ptr()
+    bufs = _alloc_splats(n, dev)
+    sp = ProjectedSplats(n, field.sh_degree, tiles_x, tiles_y, bufs,
+                         torch.empty(0, dtype=torch.int32, device=dev),
+                         torch.zeros(n_tiles, 2, dtype=torch.int32, device=dev), cam, (field.flat, n, k))
+    if n == 0:
+        return sp
+    flat = field.flat
+    sl = class_slices(n, k)
+    cstruct = _lib.camera_struct(cam)
+    s = sp.struct()
+    _lib.call("ssr_preprocess", cstruct, n, field.sh_degree, flat[sl[0][0]:].data_ptr(), flat[sl[1][0]:].data_ptr(),
+              flat[sl[2][0]:].data_ptr(), flat[sl[3][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(), s, st)
+    ws = torch.empty(_lib.query("ssr_scan_workspace", n), dtype=torch.uint8, device=dev)
+    total = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.call("ssr_scan_tiles", n, s, ws.data_ptr(), ws.numel(), total.data_ptr(), st)
+    m = int(total.item())  # host needs M to size the instance buffers
+    if m < 0:
+        raise InvalidParameter("instance count overflow")
+    sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
+    ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
+    _lib.call("ssr_bin_tiles", n, m, tiles_x, tiles_y, s, sp.inst_gauss.data_ptr() if m else None,
+              sp.tile_ranges.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    return sp
