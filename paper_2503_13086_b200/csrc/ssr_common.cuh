@@ -68,7 +68,7 @@ inline Cam to_cam(const ssr_camera& c) {
 
 // ------------------------------------------------------------------ fp64 SH
 // sh.py:36-65
-__device__ __forceinline__ void sh_basis64(int deg, const double d[3], double* out) {
+__device__ __forceinline__ void sh_basis64(const int deg, const double d[3], double* out) {
   const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
                         -1.0925484305920792, 0.5462742152960396};
   const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
@@ -283,14 +283,44 @@ __device__ __forceinline__ void sh_color64(const Cam& cam, int deg, const float*
 }
 
 // ------------------------------------------------------------------ fp32 pair math
-// kernels.py:72-80.  Rounding pinned so forward and backward agree bitwise.
-__device__ __forceinline__ float pair_power(float dx, float dy, float a, float b, float c, float& q1) {
-  const float dxx = __fmul_rn(dx, dx), dyy = __fmul_rn(dy, dy), dxy = __fmul_rn(dx, dy);
-  q1 = __fmaf_rn(c, dyy, __fmul_rn(a, dxx));
-  return __fmaf_rn(-0.5f, q1, -__fmul_rn(b, dxy));
+// kernels.py:72-80 in base 2.  The staged conic is pre-scaled so that
+//   power2 = a2 dx^2 + b2 dx dy + c2 dy^2 = log2(e) * power,
+//   a2 = -0.5 a log2e, b2 = -b log2e, c2 = -0.5 c log2e,
+// and alpha = opacity * ex2(power2) is one MUFU.EX2.  Every rounding step is
+// pinned (__f*_rn, inline ex2.approx) so the forward and both backward
+// kernels compute bit-identical alphas and transmittances.
+constexpr float LOG2E_F = 1.4426950408889634f;
+// pairs with power < -25 (alpha < 1.4e-11 * opacity): no threshold is within
+// reach, the soft term equals S0 to 3e-10 and gradient terms are ~1e-10.
+constexpr float FAR_POWER2 = -25.0f * 1.4426950408889634f;
+
+struct StagedConic {
+  float a2, b2, c2;
+};
+
+__device__ __forceinline__ StagedConic stage_conic(float a, float b, float c) {
+  StagedConic s;
+  s.a2 = __fmul_rn(-0.5f * LOG2E_F, a);
+  s.b2 = __fmul_rn(-LOG2E_F, b);
+  s.c2 = __fmul_rn(-0.5f * LOG2E_F, c);
+  return s;
 }
 
-__device__ __forceinline__ float pair_alpha(float opa, float power) { return __fmul_rn(opa, expf(power)); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Returns power2; qpos = a2 dx^2 + c2 dy^2 (<= 0) is the magnitude reference
+// for the guard band of the power > 0 decision.
+__device__ __forceinline__ float pair_power2(float dxx, float dxy, float dyy, float a2, float b2, float c2,
+                                             float& qpos) {
+  qpos = __fmaf_rn(c2, dyy, __fmul_rn(a2, dxx));
+  return __fmaf_rn(b2, dxy, qpos);
+}
+
+__device__ __forceinline__ float pair_alpha2(float opa, float power2) { return __fmul_rn(opa, ex2_approx(power2)); }
 
 // Soft count of the forward (kernels.py:83) is accumulated as
 //   n_small * S0 + sum(y * p(y)) + sum(sigmoid(alpha) for alpha >= 2.5e-3),
@@ -316,7 +346,7 @@ __device__ __forceinline__ float soft_sigmoid_accurate(float alpha) {
 
 __device__ __forceinline__ float soft_sigmoid(float alpha) {
   // 1 / (1 + exp(-(alpha - 1/255) / 0.01))   (kernels.py:83)
-  const float e = __expf(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f));
+  const float e = ex2_approx(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f * LOG2E_F));
   return __fdividef(1.0f, 1.0f + e);
 }
 

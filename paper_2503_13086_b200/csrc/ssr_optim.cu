@@ -16,35 +16,37 @@ struct AdamConsts {
   float bc1[6], bc2[6];
 };
 
-__device__ __forceinline__ int adam_class(int64_t idx, int64_t n, int K) {
+template <int K>
+__device__ __forceinline__ int adam_class(int64_t idx, int64_t n) {
   if (idx < 3 * n) return 0;
   if (idx < 7 * n) return 1;
   if (idx < 10 * n) return 2;
   if (idx < 11 * n) return 3;
-  return ((idx - 11 * n) % K) == 0 ? 4 : 5;
+  return ((uint64_t)(idx - 11 * n) % (uint64_t)K) == 0 ? 4 : 5;  // K is a compile-time constant
 }
 
 __device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, float lr, float bc1, float bc2) {
-  m = 0.9f * m + 0.1f * g;
-  v = 0.999f * v + 0.001f * g * g;
+  m = __fmaf_rn(0.9f, m, 0.1f * g);
+  v = __fmaf_rn(0.999f, v, 0.001f * g * g);
   const float mh = m / bc1, vh = v / bc2;
   p -= lr * mh / (sqrtf(vh) + 1e-15f);
 }
 
-__global__ void __launch_bounds__(256) k_adam4(int64_t n, int K, int64_t total4, float4* __restrict__ p,
+template <int K>
+__global__ void __launch_bounds__(256) k_adam4(int64_t n, int64_t total4, float4* __restrict__ p,
                                                const float4* __restrict__ g, float4* __restrict__ m,
                                                float4* __restrict__ v, AdamConsts c) {
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total4; q += (int64_t)gridDim.x * blockDim.x) {
     float4 pp = p[q], gg = g[q], mm = m[q], vv = v[q];
     const int64_t i0 = q * 4;
     int cl;
-    cl = adam_class(i0, n, K);
+    cl = adam_class<K>(i0, n);
     adam_one(pp.x, gg.x, mm.x, vv.x, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class(i0 + 1, n, K);
+    cl = adam_class<K>(i0 + 1, n);
     adam_one(pp.y, gg.y, mm.y, vv.y, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class(i0 + 2, n, K);
+    cl = adam_class<K>(i0 + 2, n);
     adam_one(pp.z, gg.z, mm.z, vv.z, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class(i0 + 3, n, K);
+    cl = adam_class<K>(i0 + 3, n);
     adam_one(pp.w, gg.w, mm.w, vv.w, c.lr[cl], c.bc1[cl], c.bc2[cl]);
     p[q] = pp;
     m[q] = mm;
@@ -52,16 +54,42 @@ __global__ void __launch_bounds__(256) k_adam4(int64_t n, int K, int64_t total4,
   }
 }
 
-__global__ void k_adam1(int64_t n, int K, int64_t start, int64_t total, float* p, const float* g, float* m, float* v,
+template <int K>
+__global__ void k_adam1(int64_t n, int64_t start, int64_t total, float* p, const float* g, float* m, float* v,
                         AdamConsts c) {
   const int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
-  const int cl = adam_class(i, n, K);
+  const int cl = adam_class<K>(i, n);
   float pp = p[i], mm = m[i], vv = v[i];
   adam_one(pp, g[i], mm, vv, c.lr[cl], c.bc1[cl], c.bc2[cl]);
   p[i] = pp;
   m[i] = mm;
   v[i] = vv;
+}
+
+template <int K>
+static int launch_adam(int64_t n, float* params, const float* grads, float* m, float* v, const AdamConsts& c,
+                       cudaStream_t st) {
+  const int64_t total = (int64_t)(11 + 3 * K) * n;
+  const bool aligned = ((((uintptr_t)params) | ((uintptr_t)grads) | ((uintptr_t)m) | ((uintptr_t)v)) & 15) == 0;
+  int64_t done = 0;
+  if (aligned) {
+    const int64_t total4 = total / 4;
+    if (total4 > 0) {
+      int64_t blocks = (total4 + 255) / 256;
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      k_adam4<K><<<(unsigned)blocks, 256, 0, st>>>(n, total4, (float4*)params, (const float4*)grads, (float4*)m,
+                                                   (float4*)v, c);
+      SSR_TRY(check_launch("k_adam4"));
+    }
+    done = total4 * 4;
+  }
+  if (done < total) {
+    const int64_t rem = total - done;
+    k_adam1<K><<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(n, done, total, params, grads, m, v, c);
+    SSR_TRY(check_launch("k_adam1"));
+  }
+  return SSR_OK;
 }
 
 // field.py:321-327 masks.  flags: bit0 keep, bit1 clone, bit2 split.
@@ -181,27 +209,13 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
   c.lr[5] = (float)lr_sh_rest;
   c.bc1[5] = (float)bc1[4];
   c.bc2[5] = (float)bc2[4];
-  const int64_t total = (int64_t)(11 + 3 * K) * n;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool aligned = ((((uintptr_t)params) | ((uintptr_t)grads) | ((uintptr_t)m) | ((uintptr_t)v)) & 15) == 0;
-  int64_t done = 0;
-  if (aligned) {
-    const int64_t total4 = total / 4;
-    if (total4 > 0) {
-      int64_t blocks = (total4 + 255) / 256;
-      if (blocks > 148 * 16) blocks = 148 * 16;
-      k_adam4<<<(unsigned)blocks, 256, 0, st>>>(n, K, total4, (float4*)params, (const float4*)grads, (float4*)m,
-                                                (float4*)v, c);
-      SSR_TRY(check_launch("k_adam4"));
-    }
-    done = total4 * 4;
+  switch (K) {
+    case 1: return launch_adam<1>(n, params, grads, m, v, c, st);
+    case 4: return launch_adam<4>(n, params, grads, m, v, c, st);
+    case 9: return launch_adam<9>(n, params, grads, m, v, c, st);
+    default: return launch_adam<16>(n, params, grads, m, v, c, st);
   }
-  if (done < total) {
-    const int64_t rem = total - done;
-    k_adam1<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(n, K, done, total, params, grads, m, v, c);
-    SSR_TRY(check_launch("k_adam1"));
-  }
-  return SSR_OK;
 }
 
 extern "C" int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degree, const float* stats,

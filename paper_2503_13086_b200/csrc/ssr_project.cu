@@ -297,8 +297,10 @@ extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, co
   if (n == 0) return SSR_OK;
   int tx, ty;
   tile_dims(cam, &tx, &ty);
-  k_chain<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      to_cam(*cam), n, sh_degree, tx, ty, positions, rotations, log_scales, sh, splats.tiles, splats.offset,
-      inst_rows, grads, accumulate, stats);
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  cudaStream_t st = (cudaStream_t)stream;
+  const Cam c = to_cam(*cam);
+  k_chain<<<blocks, 128, 0, st>>>(c, n, sh_degree, tx, ty, positions, rotations, log_scales, sh, splats.tiles,
+                                  splats.offset, inst_rows, grads, accumulate, stats);
   return check_launch("k_chain");
 }

@@ -65,9 +65,9 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
   const float band = a.band;
 
-  __shared__ float4 sA[TILE_PX];
-  __shared__ float4 sB[TILE_PX];
-  __shared__ float sC[TILE_PX];
+  __shared__ float4 sA[TILE_PX];  // tile-relative mean x, y; staged conic a2, b2
+  __shared__ float4 sB[TILE_PX];  // opacity, r, g, b
+  __shared__ float sC[TILE_PX];   // staged conic c2
   __shared__ int sMax[8];
 
   float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, sdev = 0.f;
@@ -84,62 +84,71 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
       const double2 m = a.mean[g];
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
-      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), co.x, co.y);
-      sB[tid] = make_float4(co.z, co.w, col.x, col.y);
-      sC[tid] = col.z;
+      const StagedConic q = stage_conic(co.x, co.y, co.z);
+      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), q.a2, q.b2);
+      sB[tid] = make_float4(co.w, col.x, col.y, col.z);
+      sC[tid] = q.c2;
     }
     __syncthreads();
     if (!done) {
       const int n = min(TILE_PX, s1 - base);
       const int k0 = base - s0;
-      for (int j = 0; j < n; j++) {
-        const int k = k0 + j;
-        if ((k & 31) == 0 && k) {
-          ck[(size_t)(k >> 5) * TILE_PX] = make_float4(T, c0, c1, c2);
+      for (int j0 = 0; j0 < n; j0 += BUCKET) {
+        if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
+          ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(T, c0, c1, c2);
           sbig += (double)sdev;
           sdev = 0.f;
         }
-        const float4 A = sA[j];
-        const float4 B = sB[j];
-        const float dx = fpx - A.x, dy = fpy - A.y;
-        float q1;
-        const float power = pair_power(dx, dy, A.z, A.w, B.x, q1);
-        if (power > -1e-6f * q1 && q1 != 0.f) {  // near the power > 0 skip decision
-          flag = true;
-          break;
+        const int jend = min(j0 + BUCKET, n);
+        for (int j = j0; j < jend; j++) {
+          const float4 A = sA[j];
+          const float dx = fpx - A.x, dy = fpy - A.y;
+          const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+          float qpos;
+          const float p2 = pair_power2(dxx, dxy, dyy, A.z, A.w, sC[j], qpos);
+          if (p2 < FAR_POWER2) {
+            scnt++;
+            continue;
+          }
+          if (p2 > 1e-6f * qpos && qpos != 0.f) {  // near the power > 0 skip decision
+            flag = true;
+            goto walk_done;
+          }
+          if (p2 > 0.f) continue;
+          const float4 B = sB[j];
+          float alpha = pair_alpha2(B.x, p2);
+          if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
+            flag = true;
+            goto walk_done;
+          }
+          alpha = fminf(alpha, ALPHA_CAP_F);
+          const float y = __fmul_rn(alpha, 100.f);
+          if (y < SOFT_Y0) {
+            scnt++;
+            sdev += soft_dev_poly(y);
+          } else {
+            sbig += (double)soft_sigmoid_accurate(alpha);
+          }
+          if (alpha < ALPHA_MIN_F) continue;
+          const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
+          if (fabsf(test - T_EPS_F) < T_EPS_F * 2.f * band) {
+            flag = true;
+            goto walk_done;
+          }
+          if (test < T_EPS_F) {
+            term = true;
+            nwk = k0 + j + 1;
+            goto walk_done;
+          }
+          const float w = __fmul_rn(alpha, T);
+          c0 = __fmaf_rn(B.y, w, c0);
+          c1 = __fmaf_rn(B.z, w, c1);
+          c2 = __fmaf_rn(B.w, w, c2);
+          hard++;
+          T = test;
         }
-        if (power > 0.f) continue;
-        float alpha = pair_alpha(B.y, power);
-        if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
-          flag = true;
-          break;
-        }
-        alpha = fminf(alpha, ALPHA_CAP_F);
-        const float y = __fmul_rn(alpha, 100.f);
-        if (y < SOFT_Y0) {
-          scnt++;
-          sdev += soft_dev_poly(y);
-        } else {
-          sbig += (double)soft_sigmoid_accurate(alpha);
-        }
-        if (alpha < ALPHA_MIN_F) continue;
-        const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
-        if (fabsf(test - T_EPS_F) < T_EPS_F * 2.f * band) {
-          flag = true;
-          break;
-        }
-        if (test < T_EPS_F) {
-          term = true;
-          nwk = k + 1;
-          break;
-        }
-        const float w = __fmul_rn(alpha, T);
-        c0 = __fmaf_rn(B.z, w, c0);
-        c1 = __fmaf_rn(B.w, w, c1);
-        c2 = __fmaf_rn(sC[j], w, c2);
-        hard++;
-        T = test;
       }
+    walk_done:
       if (flag || term) done = true;
     }
   }
@@ -297,9 +306,9 @@ __global__ void __launch_bounds__(32) k_forward_fixup(RasterArgs a) {
 
 // ------------------------------------------------------------------ backward, splat-parallel (fp32)
 // Taming-style: one warp per (tile, 32-splat bucket); lane l owns slot
-// 32b+l and accumulates its 9 gradient terms in registers while the 256
-// pixels stream through the warp as a systolic pipeline: at step i lane l
-// handles pixel i-l and receives that pixel's running (T, H = w.C_front)
+// 32b+l and accumulates its 9 gradient terms in registers while the bucket's
+// live pixels stream through the warp as a systolic pipeline: at step i lane
+// l handles live pixel i-l and receives that pixel's running (T, H = w.C_front)
 // from lane l-1 by shuffle.  Lane 0 seeds each pixel from the forward's
 // bucket checkpoint.  No atomics; each instance row is written once.
 __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
@@ -313,10 +322,10 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
 
-  __shared__ float4 sW[TILE_PX];  // (dL/dr, dL/dg, dL/db, dL/dsoft)
-  __shared__ float sWimg[TILE_PX];  // w . image
-  __shared__ int sNW[TILE_PX];  // n_walk << 1 | terminated  (0 = skip pixel)
-  __shared__ float4 sCk[8][TILE_PX];
+  __shared__ float4 sPA[TILE_PX];  // dL/dr, dL/dg, dL/db, dL/dsoft
+  __shared__ float4 sPB[TILE_PX];  // pixel x, y (tile-relative), w . image, n_walk << 1 | terminated
+  __shared__ float2 sSeed[8][TILE_PX];  // per warp: (T, H) entering the bucket, i-th live pixel
+  __shared__ uint8_t sList[8][TILE_PX];  // per warp: live pixels of the current bucket
   {
     const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
     int nwt = 0;
@@ -328,22 +337,42 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
       w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
       wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
     }
-    sW[tid] = w;
-    sWimg[tid] = wimg;
-    sNW[tid] = nwt;
+    sPA[tid] = w;
+    sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(nwt));
   }
   __syncthreads();
 
   const int nb = (maxw + 31) >> 5;
   const float4* ckt = a.ckpt + ckpt_base(s0, t);
+  const unsigned lt_mask = (1u << lane) - 1u;
   for (int b = warp; b < nb; b += 8) {
-    if (b > 0) {
-      for (int p = lane; p < TILE_PX; p += 32) sCk[warp][p] = ckt[(size_t)b * TILE_PX + p];
+    const int kb = b * 32;
+    // live pixels of this bucket: the walk reaches slot kb (compacted, pixel order)
+    int n_live = 0;
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      const int p = c * 32 + lane;
+      const bool lv = (__float_as_int(sPB[p].w) >> 1) > kb;
+      const unsigned msk = __ballot_sync(FULL, lv);
+      if (lv) sList[warp][n_live + __popc(msk & lt_mask)] = (uint8_t)p;
+      n_live += __popc(msk);
     }
     __syncwarp();
-    const int k = b * 32 + lane;
+    for (int j = lane; j < n_live; j += 32) {
+      const int p = sList[warp][j];
+      float2 sd = make_float2(1.f, 0.f);
+      if (b > 0) {
+        const float4 c = ckt[(size_t)b * TILE_PX + p];
+        const float4 w = sPA[p];
+        sd = make_float2(c.x, w.x * c.y + w.y * c.z + w.z * c.w);
+      }
+      sSeed[warp][j] = sd;
+    }
+    __syncwarp();
+    const int k = kb + lane;
     const bool live = k < maxw;
     float mrx = 0.f, mry = 0.f, ca = 0.f, cb = 0.f, cc = 0.f, opa = 0.f, cr = 0.f, cg = 0.f, cbl = 0.f;
+    StagedConic q = {0.f, 0.f, 0.f};
     uint32_t orow = 0;
     if (live) {
       const uint32_t g = a.inst[s0 + k];
@@ -356,6 +385,7 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
       cb = co.y;
       cc = co.z;
       opa = co.w;
+      q = stage_conic(ca, cb, cc);
       cr = col.x;
       cg = col.y;
       cbl = col.z;
@@ -363,60 +393,58 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
     }
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
     float T = 1.f, H = 0.f;
-    for (int i = 0; i < TILE_PX + 31; i++) {
+    const int n_steps = n_live + 31;
+    for (int i = 0; i < n_steps; i++) {
       float Tin = __shfl_up_sync(FULL, T, 1);
       float Hin = __shfl_up_sync(FULL, H, 1);
-      if (lane == 0 && i < TILE_PX) {
-        if (b == 0) {
-          Tin = 1.f;
-          Hin = 0.f;
-        } else {
-          const float4 c = sCk[warp][i];
-          const float4 w = sW[i];
-          Tin = c.x;
-          Hin = w.x * c.y + w.y * c.z + w.z * c.w;
-        }
+      if (lane == 0 && i < n_live) {
+        const float2 sd = sSeed[warp][i];
+        Tin = sd.x;
+        Hin = sd.y;
       }
       T = Tin;
       H = Hin;
-      const int p = i - lane;
-      if (!live || p < 0 || p >= TILE_PX) continue;
-      const int nwt = sNW[p];
+      const int j = i - lane;
+      if (!live || (unsigned)j >= (unsigned)n_live) continue;
+      const int p = sList[warp][j];
+      const float4 PB = sPB[p];
+      const int nwt = __float_as_int(PB.w);
       const int nw = nwt >> 1;
       if (k >= nw) continue;
-      const float dx = (float)(p & 15) - mrx, dy = (float)(p >> 4) - mry;
-      float q1;
-      const float power = pair_power(dx, dy, ca, cb, cc, q1);
-      if (power > 0.f) continue;
-      const float araw = pair_alpha(opa, power);
+      const float dx = PB.x - mrx, dy = PB.y - mry;
+      const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+      float qpos;
+      const float p2 = pair_power2(dxx, dxy, dyy, q.a2, q.b2, q.c2, qpos);
+      if (p2 > 0.f || p2 < FAR_POWER2) continue;  // far pairs: |contribution| < 1e-9 relative
+      const float araw = pair_alpha2(opa, p2);
       const bool capped = araw > ALPHA_CAP_F;
       const float alpha = capped ? ALPHA_CAP_F : araw;
       const bool blended = alpha >= ALPHA_MIN_F && !((nwt & 1) && k == nw - 1);
-      const float4 w = sW[p];
+      const float4 w = sPA[p];
       float dlda = 0.f;
       if (blended) {
         const float wc = w.x * cr + w.y * cg + w.z * cbl;
         const float aT = alpha * T;
-        g0 += aT * w.x;
-        g1 += aT * w.y;
-        g2 += aT * w.z;
+        g0 = fmaf(aT, w.x, g0);
+        g1 = fmaf(aT, w.y, g1);
+        g2 = fmaf(aT, w.z, g2);
         const float one_m = __fsub_rn(1.f, alpha);
-        const float sdot = sWimg[p] - H - aT * wc;  // w . (colour behind this splat)
+        const float awc = aT * wc;
+        const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
         dlda = T * wc - __fdividef(sdot, one_m);
-        H += aT * wc;
+        H += awc;
         T = __fmul_rn(T, one_m);
       }
       if (!capped) {
         const float sv = soft_sigmoid(alpha);
-        const float gsoft = w.w * sv * (1.f - sv) * 100.f;
-        g3 += (dlda + gsoft) * alpha * (1.f - opa);
+        g3 = fmaf(dlda + w.w * sv * (1.f - sv) * 100.f, alpha, g3);
         if (blended) {
           const float gp = dlda * alpha;
-          g4 += gp * (ca * dx + cb * dy);
-          g5 += gp * (cb * dx + cc * dy);
-          g6 += gp * (-0.5f * dx * dx);
-          g7 += gp * (-dx * dy);
-          g8 += gp * (-0.5f * dy * dy);
+          g4 = fmaf(gp, ca * dx + cb * dy, g4);
+          g5 = fmaf(gp, cb * dx + cc * dy, g5);
+          g6 = fmaf(gp, dxx, g6);
+          g7 = fmaf(gp, dxy, g7);
+          g8 = fmaf(gp, dyy, g8);
         }
       }
     }
@@ -425,13 +453,14 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
       r[0] = g0;
       r[1] = g1;
       r[2] = g2;
-      r[3] = g3;
+      r[3] = g3 * (1.f - opa);
       r[4] = g4;
       r[5] = g5;
-      r[6] = g6;
-      r[7] = g7;
-      r[8] = g8;
+      r[6] = -0.5f * g6;
+      r[7] = -g7;
+      r[8] = -0.5f * g8;
     }
+    __syncwarp();
   }
   // rows of slots no pixel walked
   for (int k = maxw + tid; k < len; k += blockDim.x) {
@@ -456,7 +485,7 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
   __shared__ float4 sA[32], sB[32];
-  __shared__ float sC[32];
+  __shared__ float4 sQ[32];
   __shared__ uint32_t sRow[32];
   __shared__ float part[8][32][9];
 
@@ -481,9 +510,10 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
       const double2 m = a.mean[g];
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
+      const StagedConic q = stage_conic(co.x, co.y, co.z);
       sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), co.x, co.y);
       sB[tid] = make_float4(co.z, co.w, col.x, col.y);
-      sC[tid] = col.z;
+      sQ[tid] = make_float4(q.a2, q.b2, q.c2, col.z);
       sRow[tid] = inst_row(a, g, tx, ty);
     }
     __syncthreads();
@@ -492,18 +522,19 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
       const int k = kb + j;
       float c[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (k < nw) {
-        const float4 A = sA[j], B = sB[j];
+        const float4 A = sA[j], B = sB[j], Q = sQ[j];
         const float dx = fpx - A.x, dy = fpy - A.y;
-        float q1;
-        const float power = pair_power(dx, dy, A.z, A.w, B.x, q1);
-        if (power <= 0.f) {
-          const float araw = pair_alpha(B.y, power);
+        const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+        float qpos;
+        const float p2 = pair_power2(dxx, dxy, dyy, Q.x, Q.y, Q.z, qpos);
+        if (p2 <= 0.f && p2 >= FAR_POWER2) {
+          const float araw = pair_alpha2(B.y, p2);
           const bool capped = araw > ALPHA_CAP_F;
           const float alpha = capped ? ALPHA_CAP_F : araw;
           const bool blended = alpha >= ALPHA_MIN_F && !(term && k == nw - 1);
           float dlda = 0.f;
           if (blended) {
-            const float wc = w.x * B.z + w.y * B.w + w.z * sC[j];
+            const float wc = w.x * B.z + w.y * B.w + w.z * Q.w;
             const float aT = alpha * T;
             c[0] = aT * w.x;
             c[1] = aT * w.y;
@@ -520,9 +551,9 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
               const float gp = dlda * alpha;
               c[4] = gp * (A.z * dx + A.w * dy);
               c[5] = gp * (A.w * dx + B.x * dy);
-              c[6] = gp * (-0.5f * dx * dx);
-              c[7] = gp * (-dx * dy);
-              c[8] = gp * (-0.5f * dy * dy);
+              c[6] = gp * (-0.5f * dxx);
+              c[7] = gp * (-dxy);
+              c[8] = gp * (-0.5f * dyy);
             }
           }
         }
