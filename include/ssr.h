@@ -61,7 +61,7 @@ typedef struct ssr_splats {
   double* depth;       /* N      camera-space z, fp64 */
   int32_t* rect;       /* N x 4  tile rect (tx0, ty0, tx1, ty1), exclusive upper */
   uint32_t* tiles;     /* N      tiles touched (0 = culled) */
-  uint32_t* offset;    /* N      exclusive scan of tiles = first instance id */
+  uint32_t* offset;    /* N      first instance id: tiles scanned in (fp64 depth, row) order */
 } ssr_splats;
 
 /* Render-time per-pixel / per-tile state retained for the backward. */
@@ -100,14 +100,16 @@ int ssr_project_aux(const ssr_camera* cam, int64_t n, int32_t sh_degree, const f
                     uint8_t* sh_hi, double* radii, void* stream);
 
 /* ---------------------------------------------------------- stage 2 */
-/* Exclusive scan of splats.tiles into splats.offset; *total_dev (device) gets M. */
+/* Depth pre-sort of the N rows by fp32(depth) with an fp64 tie-fix, then the
+ * exclusive scan of splats.tiles in that order into splats.offset (so each
+ * row's instances are emitted at depth-ordered positions); *total_dev gets M. */
 int ssr_scan_workspace(int64_t n, int64_t* bytes);
 int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int64_t workspace_bytes,
                    uint32_t* total_dev, void* stream);
 
-/* projection.py:165-191: duplicate each visible splat per overlapped tile,
- * 64-bit (tile << 32 | fp32 depth bits) stable radix sort, tie-fix of equal
- * keys by (fp64 depth, index), searchsorted tile ranges.  Outputs:
+/* projection.py:165-191: duplicate each visible splat per overlapped tile at
+ * its depth-ordered offset, stable radix sort by tile id (ceil(log2 n_tiles)
+ * bits) -> (tile, fp64 depth, row) order, searchsorted tile ranges.  Outputs:
  *   inst_gauss[M]   field row of each sorted instance
  *   tile_ranges[2*n_tiles]  (start, end) per tile, searchsorted semantics */
 int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes);
@@ -139,7 +141,8 @@ int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* i
  * order) and chain through projection/SH in fp64.  grads is the flat
  * FieldGrads buffer [pos 3N | rot 4N | logscale 3N | logit N | sh 3KN |
  * screen_norm N | visible N].  accumulate!=0 adds into it (view batches);
- * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible. */
+ * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible.
+ * inst_rows is consumed (used as scratch between the two chain kernels). */
 int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
               const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
               const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream);
@@ -148,7 +151,7 @@ int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* 
 /* optim.py:29-47,113-130: dense bias-corrected Adam over the flat parameter
  * buffer [pos | rot | logscale | logit | sh] (n rows, K sh coeffs).
  * lr[5] = (pos, rot, scale, opacity, sh_dc), sh rest lr = lr_sh_rest;
- * bc1/bc2[5] = 1 - beta^step per class. */
+ * bc1/bc2[5] = 1 - beta^step per class.  lr, bc1, bc2 are HOST arrays. */
 int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, float* m, float* v,
              const double* lr, double lr_sh_rest, const double* bc1, const double* bc2, void* stream);
 

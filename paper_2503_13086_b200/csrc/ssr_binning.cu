@@ -1,11 +1,16 @@
-// Stage 2: tile-key duplication, prefix scan, 64-bit (tile, depth) radix
-// sort, tie-fix and searchsorted tile ranges (rasterize/projection.py:165-191).
+// Stage 2: tile-key duplication, prefix scan and the (tile, depth) sort
+// (rasterize/projection.py:165-191), as a depth pre-sort + stable tile sort:
 //
-// Key = (tile << 32) | float_bits(fp32(depth64)).  fp64 -> fp32 rounding is
-// monotone, so the fp32 key never inverts the reference's fp64 order; it can
-// only create ties, which the tie-fix pass re-orders by (fp64 depth, field
-// row).  The radix sort is stable and instances are emitted in field-row
-// order, which is exactly the reference's np.lexsort tie-break.
+//  1. the N Gaussians are radix-sorted by fp32(depth64) bits (culled rows
+//     keyed last); runs of equal fp32 keys are re-ordered by (fp64 depth,
+//     field row).  fp64 -> fp32 rounding is monotone, so this is exactly the
+//     reference's fp64 depth order with row-index tie-break;
+//  2. tiles-touched counts are scanned in that order, so every Gaussian's
+//     instances are emitted at depth-ordered positions (splats.offset);
+//  3. one stable LSD radix sort over the tile id alone (ceil(log2 n_tiles)
+//     bits) turns the depth-ordered instance list into (tile, depth, row)
+//     order -- np.lexsort((depth, tile)) over splat-major instances;
+//  4. searchsorted tile ranges from the sorted tile ids.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -15,46 +20,89 @@ namespace ssr {
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-__global__ void k_scan_total(int64_t n, const uint32_t* tiles, const uint32_t* offset, uint32_t* total) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *total = n ? offset[n - 1] + tiles[n - 1] : 0u;
+__global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const uint32_t* __restrict__ tiles,
+                                                    const double* __restrict__ depth, uint32_t* __restrict__ keys,
+                                                    uint32_t* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // depth > ZNEAR > 0 for kept rows, so the float bit pattern is monotone
+  keys[i] = tiles[i] ? __float_as_uint(__double2float_rn(depth[i])) : 0xffffffffu;
+  vals[i] = (uint32_t)i;
 }
 
-// One thread per field row writes its tiles.  Emission order inside a row is
-// ty-outer / tx-inner (projection.py:175-182).
+// Runs of equal fp32 depth keys: insertion sort by fp64 depth (stable, so
+// equal fp64 depths keep field-row order).  Also gathers tiles in depth order.
+__global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t* __restrict__ keys,
+                                                      uint32_t* __restrict__ order, const double* __restrict__ depth) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t key = keys[s];
+  if (key == 0xffffffffu) return;
+  const bool head = (s == 0) || (keys[s - 1] != key);
+  if (!head || s + 1 >= n || keys[s + 1] != key) return;
+  int64_t e = s + 1;
+  while (e < n && keys[e] == key) e++;
+  for (int64_t a = s + 1; a < e; a++) {
+    const uint32_t v = order[a];
+    const double d = depth[v];
+    int64_t b = a - 1;
+    while (b >= s && depth[order[b]] > d) {
+      order[b + 1] = order[b];
+      b--;
+    }
+    order[b + 1] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gather_counts(int64_t n, const uint32_t* __restrict__ order,
+                                                       const uint32_t* __restrict__ tiles,
+                                                       uint32_t* __restrict__ cnt) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) cnt[r] = tiles[order[r]];
+}
+
+__global__ void __launch_bounds__(256) k_scatter_offsets(int64_t n, const uint32_t* __restrict__ order,
+                                                         const uint32_t* __restrict__ cnt,
+                                                         const uint32_t* __restrict__ off_sorted,
+                                                         uint32_t* __restrict__ offset, uint32_t* __restrict__ total) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  offset[order[r]] = off_sorted[r];
+  if (r == n - 1) *total = off_sorted[r] + cnt[r];
+}
+
+__global__ void k_zero_total(uint32_t* total) {
+  if (threadIdx.x == 0) *total = 0u;
+}
+
+// One thread per field row writes its tiles at its depth-ordered offset;
+// emission order inside a row is ty-outer / tx-inner (projection.py:175-182).
 __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const uint32_t* __restrict__ tiles,
-                                                   const uint32_t* __restrict__ offset,
-                                                   const int4* __restrict__ rect, const double* __restrict__ depth,
-                                                   unsigned long long* __restrict__ keys,
-                                                   uint32_t* __restrict__ vals) {
+                                                   const uint32_t* __restrict__ offset, const int4* __restrict__ rect,
+                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t nt = tiles[i];
   if (nt == 0) return;
   const int4 r = rect[i];
-  const unsigned long long dbits = (unsigned long long)__float_as_uint(__double2float_rn(depth[i]));
   uint32_t o = offset[i];
   for (int ty = r.y; ty < r.w; ty++) {
-    const unsigned long long row = (unsigned long long)ty * tiles_x;
+    const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
     for (int tx = r.x; tx < r.z; tx++) {
-      keys[o] = ((row + tx) << 32) | dbits;
+      keys[o] = row + (uint32_t)tx;
       vals[o] = (uint32_t)i;
       o++;
     }
   }
 }
 
-// Tie-fix + searchsorted ranges, one thread per sorted instance.
-__global__ void __launch_bounds__(256) k_tiefix_ranges(int64_t m, int n_tiles,
-                                                       const unsigned long long* __restrict__ keys,
-                                                       uint32_t* __restrict__ vals, const double* __restrict__ depth,
-                                                       int32_t* __restrict__ ranges) {
+// searchsorted(left/right) for every tile id from the sorted tile keys.
+__global__ void __launch_bounds__(256) k_ranges(int64_t m, int n_tiles, const uint32_t* __restrict__ keys,
+                                                int32_t* __restrict__ ranges) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= m) return;
-  const unsigned long long key = keys[s];
-  const int tile = (int)(key >> 32);
-  const int prev = s > 0 ? (int)(keys[s - 1] >> 32) : -1;
-  // searchsorted(left) start of every tile in (prev, tile]; searchsorted(right)
-  // end of every tile in [prev, tile)
+  const int tile = (int)keys[s];
+  const int prev = s > 0 ? (int)keys[s - 1] : -1;
   if (tile != prev) {
     for (int t = prev + 1; t <= tile; t++) ranges[2 * t] = (int32_t)s;
     for (int t = prev < 0 ? 0 : prev; t < tile; t++) ranges[2 * t + 1] = (int32_t)s;
@@ -63,37 +111,26 @@ __global__ void __launch_bounds__(256) k_tiefix_ranges(int64_t m, int n_tiles,
     for (int t = tile + 1; t < n_tiles; t++) ranges[2 * t] = (int32_t)m;
     for (int t = tile; t < n_tiles; t++) ranges[2 * t + 1] = (int32_t)m;
   }
-  // tie-fix: the head of a run of equal keys insertion-sorts it by fp64 depth
-  // (stable, so equal fp64 depths stay in field-row order)
-  const bool head = (s == 0) || (keys[s - 1] != key);
-  if (head && s + 1 < m && keys[s + 1] == key) {
-    int64_t e = s + 1;
-    while (e < m && keys[e] == key) e++;
-    for (int64_t a = s + 1; a < e; a++) {
-      const uint32_t v = vals[a];
-      const double d = depth[v];
-      int64_t b = a - 1;
-      while (b >= s && depth[vals[b]] > d) {
-        vals[b + 1] = vals[b];
-        b--;
-      }
-      vals[b + 1] = v;
-    }
-  }
 }
 
 static int tile_bits(int n_tiles) {
-  int b = 0;
+  int b = 1;
   while ((1LL << b) < (long long)n_tiles) b++;
   return b;
 }
 
-static size_t sort_temp_bytes(int64_t m, int n_tiles) {
+static size_t sort32_temp_bytes(int64_t m, int end_bit) {
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs((void*)nullptr, bytes, (const unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (int)(m > 0 ? m : 1), 0, 32 + tile_bits(n_tiles));
+  cub::DeviceRadixSort::SortPairs((void*)nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(m > 0 ? m : 1), 0, end_bit);
   return bytes;
+}
+
+static size_t scan_temp_bytes(int64_t n) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)(n > 0 ? n : 1));
+  return b;
 }
 
 }  // namespace ssr
@@ -101,10 +138,8 @@ static size_t sort_temp_bytes(int64_t m, int n_tiles) {
 using namespace ssr;
 
 extern "C" int ssr_scan_workspace(int64_t n, int64_t* bytes) {
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                (int)(n > 0 ? n : 1));
-  *bytes = (int64_t)b;
+  const int64_t a = align_up(4 * (n > 0 ? n : 1), 256);
+  *bytes = 6 * a + align_up((int64_t)sort32_temp_bytes(n, 32), 256) + align_up((int64_t)scan_temp_bytes(n), 256);
   return SSR_OK;
 }
 
@@ -115,22 +150,45 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
     set_error("ssr_scan_tiles: n out of range");
     return SSR_ERR_INVALID;
   }
-  if (n > 0) {
-    size_t b = (size_t)workspace_bytes;
-    SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum(workspace, b, splats.tiles, splats.offset, (int)n, st),
-                       "scan tiles"));
+  int64_t need = 0;
+  ssr_scan_workspace(n, &need);
+  if (workspace_bytes < need) {
+    set_error("ssr_scan_tiles: workspace too small");
+    return SSR_ERR_INVALID;
   }
-  k_scan_total<<<1, 32, 0, st>>>(n, splats.tiles, splats.offset, total_dev);
-  return check_launch("k_scan_total");
+  if (n == 0) {
+    k_zero_total<<<1, 32, 0, st>>>(total_dev);
+    return check_launch("k_zero_total");
+  }
+  const int64_t a = align_up(4 * n, 256);
+  char* w = (char*)workspace;
+  uint32_t* keys_in = (uint32_t*)w;
+  uint32_t* keys_out = (uint32_t*)(w + a);
+  uint32_t* vals_in = (uint32_t*)(w + 2 * a);
+  uint32_t* order = (uint32_t*)(w + 3 * a);
+  uint32_t* cnt = (uint32_t*)(w + 4 * a);
+  uint32_t* off_sorted = (uint32_t*)(w + 5 * a);
+  char* temp = w + 6 * a;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  k_depth_keys<<<blocks, 256, 0, st>>>(n, splats.tiles, splats.depth, keys_in, vals_in);
+  SSR_TRY(check_launch("k_depth_keys"));
+  size_t tb = sort32_temp_bytes(n, 32);
+  SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)temp, tb, keys_in, keys_out, vals_in, order, (int)n, 0, 32,
+                                                     st),
+                     "depth sort"));
+  k_depth_tiefix<<<blocks, 256, 0, st>>>(n, keys_out, order, splats.depth);
+  SSR_TRY(check_launch("k_depth_tiefix"));
+  k_gather_counts<<<blocks, 256, 0, st>>>(n, order, splats.tiles, cnt);
+  SSR_TRY(check_launch("k_gather_counts"));
+  size_t sb = scan_temp_bytes(n);
+  SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb, cnt, off_sorted, (int)n, st), "scan tiles"));
+  k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev);
+  return check_launch("k_scatter_offsets");
 }
 
 extern "C" int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes) {
-  int64_t b = 0;
-  b += align_up(8 * (m > 0 ? m : 1), 256);  // keys in
-  b += align_up(8 * (m > 0 ? m : 1), 256);  // keys out
-  b += align_up(4 * (m > 0 ? m : 1), 256);  // vals in
-  b += align_up((int64_t)sort_temp_bytes(m, n_tiles), 256);
-  *bytes = b;
+  const int64_t a = align_up(4 * (m > 0 ? m : 1), 256);
+  *bytes = 3 * a + align_up((int64_t)sort32_temp_bytes(m, tile_bits(n_tiles > 0 ? n_tiles : 1)), 256);
   return SSR_OK;
 }
 
@@ -152,24 +210,21 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   if (m == 0) {
     return check_cuda(cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * n_tiles, st), "ranges memset");
   }
+  const int64_t a = align_up(4 * m, 256);
   char* w = (char*)workspace;
-  unsigned long long* keys_in = (unsigned long long*)w;
-  w += align_up(8 * m, 256);
-  unsigned long long* keys_out = (unsigned long long*)w;
-  w += align_up(8 * m, 256);
-  uint32_t* vals_in = (uint32_t*)w;
-  w += align_up(4 * m, 256);
-  size_t temp = sort_temp_bytes(m, n_tiles);
-
+  uint32_t* keys_in = (uint32_t*)w;
+  uint32_t* keys_out = (uint32_t*)(w + a);
+  uint32_t* vals_in = (uint32_t*)(w + 2 * a);
+  const int bits = tile_bits(n_tiles);
+  size_t temp = sort32_temp_bytes(m, bits);
   k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, tiles_x, splats.tiles, splats.offset,
-                                                           (const int4*)splats.rect, splats.depth, keys_in, vals_in);
+                                                           (const int4*)splats.rect, keys_in, vals_in);
   SSR_TRY(check_launch("k_duplicate"));
-  SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)w, temp, keys_in, keys_out, vals_in, inst_gauss, (int)m,
-                                                     0, 32 + tile_bits(n_tiles), st),
-                     "radix sort"));
-  k_tiefix_ranges<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, n_tiles, keys_out, inst_gauss, splats.depth,
-                                                               tile_ranges);
-  return check_launch("k_tiefix_ranges");
+  SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)(w + 3 * a), temp, keys_in, keys_out, vals_in, inst_gauss,
+                                                     (int)m, 0, bits, st),
+                     "tile sort"));
+  k_ranges<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, n_tiles, keys_out, tile_ranges);
+  return check_launch("k_ranges");
 }
 
 extern "C" int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles) {

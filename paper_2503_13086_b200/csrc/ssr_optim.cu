@@ -11,85 +11,77 @@
 
 namespace ssr {
 
-struct AdamConsts {
-  float lr[6];  // pos, rot, scale, opacity, sh dc, sh rest
-  float bc1[6], bc2[6];
+// One launch; blocks are assigned to class regions so every block has a
+// uniform learning rate and bias correction (no per-element class lookup).
+struct AdamRegion {
+  int64_t start, count;  // element range in the flat buffer
+  int64_t block0;        // first block of this region
+  float lr, lr_rest;     // sh region: lr = DC rate, lr_rest = rest rate
+  float inv_bc1, inv_bc2;
+  int is_sh;
+};
+struct AdamPlan {
+  AdamRegion r[5];
 };
 
-template <int K>
-__device__ __forceinline__ int adam_class(int64_t idx, int64_t n) {
-  if (idx < 3 * n) return 0;
-  if (idx < 7 * n) return 1;
-  if (idx < 10 * n) return 2;
-  if (idx < 11 * n) return 3;
-  return ((uint64_t)(idx - 11 * n) % (uint64_t)K) == 0 ? 4 : 5;  // K is a compile-time constant
-}
+constexpr int ADAM_THREADS = 256;
+constexpr int ADAM_PER_THREAD = 8;  // two float4 per thread
+constexpr int64_t ADAM_PER_BLOCK = (int64_t)ADAM_THREADS * ADAM_PER_THREAD;
 
-__device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, float lr, float bc1, float bc2) {
+__device__ __forceinline__ float adam_one(float p, float g, float& m, float& v, float lr, float ib1, float ib2) {
   m = __fmaf_rn(0.9f, m, 0.1f * g);
   v = __fmaf_rn(0.999f, v, 0.001f * g * g);
-  const float mh = m / bc1, vh = v / bc2;
-  p -= lr * mh / (sqrtf(vh) + 1e-15f);
+  return p - __fdividef(lr * (m * ib1), sqrtf(v * ib2) + 1e-15f);
 }
 
 template <int K>
-__global__ void __launch_bounds__(256) k_adam4(int64_t n, int64_t total4, float4* __restrict__ p,
-                                               const float4* __restrict__ g, float4* __restrict__ m,
-                                               float4* __restrict__ v, AdamConsts c) {
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total4; q += (int64_t)gridDim.x * blockDim.x) {
-    float4 pp = p[q], gg = g[q], mm = m[q], vv = v[q];
-    const int64_t i0 = q * 4;
-    int cl;
-    cl = adam_class<K>(i0, n);
-    adam_one(pp.x, gg.x, mm.x, vv.x, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class<K>(i0 + 1, n);
-    adam_one(pp.y, gg.y, mm.y, vv.y, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class<K>(i0 + 2, n);
-    adam_one(pp.z, gg.z, mm.z, vv.z, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    cl = adam_class<K>(i0 + 3, n);
-    adam_one(pp.w, gg.w, mm.w, vv.w, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-    p[q] = pp;
-    m[q] = mm;
-    v[q] = vv;
-  }
-}
-
-template <int K>
-__global__ void k_adam1(int64_t n, int64_t start, int64_t total, float* p, const float* g, float* m, float* v,
-                        AdamConsts c) {
-  const int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int cl = adam_class<K>(i, n);
-  float pp = p[i], mm = m[i], vv = v[i];
-  adam_one(pp, g[i], mm, vv, c.lr[cl], c.bc1[cl], c.bc2[cl]);
-  p[i] = pp;
-  m[i] = mm;
-  v[i] = vv;
-}
-
-template <int K>
-static int launch_adam(int64_t n, float* params, const float* grads, float* m, float* v, const AdamConsts& c,
-                       cudaStream_t st) {
-  const int64_t total = (int64_t)(11 + 3 * K) * n;
-  const bool aligned = ((((uintptr_t)params) | ((uintptr_t)grads) | ((uintptr_t)m) | ((uintptr_t)v)) & 15) == 0;
-  int64_t done = 0;
-  if (aligned) {
-    const int64_t total4 = total / 4;
-    if (total4 > 0) {
-      int64_t blocks = (total4 + 255) / 256;
-      if (blocks > 148 * 8) blocks = 148 * 8;
-      k_adam4<K><<<(unsigned)blocks, 256, 0, st>>>(n, total4, (float4*)params, (const float4*)grads, (float4*)m,
-                                                   (float4*)v, c);
-      SSR_TRY(check_launch("k_adam4"));
+__global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __restrict__ p,
+                                                       const float* __restrict__ g, float* __restrict__ m,
+                                                       float* __restrict__ v) {
+  const int64_t bid = blockIdx.x;
+  int ri = 0;
+#pragma unroll
+  for (int i = 1; i < 5; i++)
+    if (bid >= plan.r[i].block0) ri = i;
+  const AdamRegion R = plan.r[ri];
+  const int64_t e0 = R.start + (bid - R.block0) * ADAM_PER_BLOCK;
+  const int64_t e_end = R.start + R.count;
+  const bool vec = ((R.start & 3) == 0);
+  if (vec && e0 + ADAM_PER_BLOCK <= e_end) {
+#pragma unroll
+    for (int u = 0; u < ADAM_PER_THREAD / 4; u++) {
+      const int64_t e = e0 + (int64_t)(u * ADAM_THREADS + threadIdx.x) * 4;
+      float4 pp = *reinterpret_cast<float4*>(p + e);
+      const float4 gg = *reinterpret_cast<const float4*>(g + e);
+      float4 mm = *reinterpret_cast<float4*>(m + e);
+      float4 vv = *reinterpret_cast<float4*>(v + e);
+      float lr0 = R.lr, lr1 = R.lr, lr2 = R.lr, lr3 = R.lr;
+      if (R.is_sh) {
+        const int64_t j = e - R.start;
+        lr0 = ((j + 0) % K) == 0 ? R.lr : R.lr_rest;
+        lr1 = ((j + 1) % K) == 0 ? R.lr : R.lr_rest;
+        lr2 = ((j + 2) % K) == 0 ? R.lr : R.lr_rest;
+        lr3 = ((j + 3) % K) == 0 ? R.lr : R.lr_rest;
+      }
+      pp.x = adam_one(pp.x, gg.x, mm.x, vv.x, lr0, R.inv_bc1, R.inv_bc2);
+      pp.y = adam_one(pp.y, gg.y, mm.y, vv.y, lr1, R.inv_bc1, R.inv_bc2);
+      pp.z = adam_one(pp.z, gg.z, mm.z, vv.z, lr2, R.inv_bc1, R.inv_bc2);
+      pp.w = adam_one(pp.w, gg.w, mm.w, vv.w, lr3, R.inv_bc1, R.inv_bc2);
+      *reinterpret_cast<float4*>(p + e) = pp;
+      *reinterpret_cast<float4*>(m + e) = mm;
+      *reinterpret_cast<float4*>(v + e) = vv;
     }
-    done = total4 * 4;
+  } else {
+    for (int u = 0; u < ADAM_PER_THREAD; u++) {
+      const int64_t e = e0 + (int64_t)u * ADAM_THREADS + threadIdx.x;
+      if (e >= e_end) break;
+      const float lr = (R.is_sh && ((e - R.start) % K) != 0) ? R.lr_rest : R.lr;
+      float mm = m[e], vv = v[e];
+      p[e] = adam_one(p[e], g[e], mm, vv, lr, R.inv_bc1, R.inv_bc2);
+      m[e] = mm;
+      v[e] = vv;
+    }
   }
-  if (done < total) {
-    const int64_t rem = total - done;
-    k_adam1<K><<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(n, done, total, params, grads, m, v, c);
-    SSR_TRY(check_launch("k_adam1"));
-  }
-  return SSR_OK;
 }
 
 // field.py:321-327 masks.  flags: bit0 keep, bit1 clone, bit2 split.
@@ -200,22 +192,30 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
   }
   if (n == 0) return SSR_OK;
   const int K = (sh_degree + 1) * (sh_degree + 1);
-  AdamConsts c;
-  for (int i = 0; i < 5; i++) {
-    c.lr[i] = (float)lr[i];
-    c.bc1[i] = (float)bc1[i];
-    c.bc2[i] = (float)bc2[i];
+  const int64_t widths[5] = {3, 4, 3, 1, 3 * (int64_t)K};
+  AdamPlan plan;
+  int64_t start = 0, blocks = 0;
+  for (int c = 0; c < 5; c++) {
+    AdamRegion& R = plan.r[c];
+    R.start = start;
+    R.count = widths[c] * n;
+    R.block0 = blocks;
+    R.lr = (float)lr[c];
+    R.lr_rest = (float)lr_sh_rest;
+    R.inv_bc1 = (float)(1.0 / bc1[c]);
+    R.inv_bc2 = (float)(1.0 / bc2[c]);
+    R.is_sh = c == 4;
+    start += R.count;
+    blocks += (R.count + ADAM_PER_BLOCK - 1) / ADAM_PER_BLOCK;
   }
-  c.lr[5] = (float)lr_sh_rest;
-  c.bc1[5] = (float)bc1[4];
-  c.bc2[5] = (float)bc2[4];
   cudaStream_t st = (cudaStream_t)stream;
   switch (K) {
-    case 1: return launch_adam<1>(n, params, grads, m, v, c, st);
-    case 4: return launch_adam<4>(n, params, grads, m, v, c, st);
-    case 9: return launch_adam<9>(n, params, grads, m, v, c, st);
-    default: return launch_adam<16>(n, params, grads, m, v, c, st);
+    case 1: k_adam<1><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
+    case 4: k_adam<4><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
+    case 9: k_adam<9><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
+    default: k_adam<16><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
   }
+  return check_launch("k_adam");
 }
 
 extern "C" int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degree, const float* stats,

@@ -68,25 +68,25 @@ __global__ void k_project_aux(Cam cam, int64_t n, int deg, int tiles_x, int tile
   radii[i] = P.radius;
 }
 
-// backward.py:110-259 + sh.py:135-152 -- one thread per field row: merge the
+// backward.py:110-206 (geometry half) -- one thread per field row: merge the
 // row's instance rows in splat-major (= ascending tile, bincount) order, then
-// chain screen-space gradients to the parameters in float64.
-__global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int tiles_x, int tiles_y,
-                                               const float* __restrict__ pos, const float* __restrict__ rot,
-                                               const float* __restrict__ ls, const float* __restrict__ sh,
-                                               const uint32_t* __restrict__ tiles,
-                                               const uint32_t* __restrict__ offset,
-                                               const float* __restrict__ rows, float* __restrict__ grads,
-                                               int accumulate, float* __restrict__ stats) {
+// chain d_mu / d_conic through the projection to position, rotation and
+// log-scale in float64.  The merged colour gradient is handed to k_chain_sh
+// in the first three floats of the Gaussian's own first instance row.
+__global__ void __launch_bounds__(128) k_chain_geo(Cam cam, int64_t n, int K, int tiles_x, int tiles_y,
+                                                   const float* __restrict__ pos, const float* __restrict__ rot,
+                                                   const float* __restrict__ ls,
+                                                   const uint32_t* __restrict__ tiles,
+                                                   const uint32_t* __restrict__ offset, float* __restrict__ rows,
+                                                   float* __restrict__ grads, int accumulate,
+                                                   float* __restrict__ stats) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int K = (deg + 1) * (deg + 1);
   const int S = 11 + 3 * K;
   float* g_pos = grads;
   float* g_rot = grads + 3 * n;
   float* g_ls = grads + 7 * n;
   float* g_logit = grads + 10 * n;
-  float* g_sh = grads + 11 * n;
   float* g_screen = grads + (int64_t)S * n;
   float* g_vis = grads + (int64_t)(S + 1) * n;
   const uint32_t nt = tiles[i];
@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int 
       for (int j = 0; j < 4; j++) g_rot[i * 4 + j] = 0.f;
       for (int j = 0; j < 3; j++) g_ls[i * 3 + j] = 0.f;
       g_logit[i] = 0.f;
-      for (int j = 0; j < 3 * K; j++) g_sh[i * 3 * K + j] = 0.f;
       g_screen[i] = 0.f;
       g_vis[i] = 0.f;
     }
@@ -104,33 +103,15 @@ __global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int 
   }
   // bincount merge (backward.py:110-118): ascending tile order
   double pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const float* rw = rows + (int64_t)offset[i] * 9;
+  float* rw = rows + (int64_t)offset[i] * 9;
   for (uint32_t j = 0; j < nt; j++)
     for (int c = 0; c < 9; c++) pr[c] += (double)rw[j * 9 + c];
+  rw[0] = (float)pr[0];
+  rw[1] = (float)pr[1];
+  rw[2] = (float)pr[2];
 
   Proj64 P;
   project64(cam, pos + i * 3, rot + i * 4, ls + i * 3, tiles_x, tiles_y, P);
-  double dir[3], rs, basis[16], col[3];
-  bool lo[3], hi[3];
-  const float* shrow = sh + i * 3 * K;
-  sh_color64(cam, deg, pos + i * 3, shrow, dir, &rs, basis, col, lo, hi);
-
-  // sh.py:135-152
-  double dcol[3];
-  for (int c = 0; c < 3; c++) dcol[c] = (lo[c] || hi[c]) ? 0.0 : pr[c];
-  double gb[48];
-  sh_basis_grad64(deg, dir, gb);
-  double ddir[3];
-  for (int d = 0; d < 3; d++) {
-    double acc = 0.0;
-    for (int c = 0; c < 3; c++)
-      for (int k = 0; k < K; k++) acc += dcol[c] * (double)shrow[c * K + k] * gb[k * 3 + d];
-    ddir[d] = acc;
-  }
-  const double radial = ddir[0] * dir[0] + ddir[1] * dir[1] + ddir[2] * dir[2];
-  double dpos_sh[3];
-  for (int d = 0; d < 3; d++) dpos_sh[d] = (ddir[d] - radial * dir[d]) / rs;
-
   // conic -> V2: g_v2 = -Q G Q  (backward.py:502-515)
   const double q[4] = {P.qa, P.qb, P.qb, P.qc};
   const double gq[4] = {pr[6], 0.5 * pr[7], 0.5 * pr[7], pr[8]};
@@ -181,8 +162,7 @@ __global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int 
   dcam[1] += pr[5] * fy / z;
   dcam[2] += -pr[4] * fx * x / z2 - pr[5] * fy * y / z2;
   double dpos[3];
-  for (int d = 0; d < 3; d++)
-    dpos[d] = dcam[0] * R[0 * 3 + d] + dcam[1] * R[1 * 3 + d] + dcam[2] * R[2 * 3 + d] + dpos_sh[d];
+  for (int d = 0; d < 3; d++) dpos[d] = dcam[0] * R[0 * 3 + d] + dcam[1] * R[1 * 3 + d] + dcam[2] * R[2 * 3 + d];
 
   // _cov_to_rotation_scale (backward.py:562-612)
   double m[9], gs[9], dm[9], drot[9], dls[3];
@@ -217,14 +197,11 @@ __global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int 
   const double rad = dqn[0] * P.qn[0] + dqn[1] * P.qn[1] + dqn[2] * P.qn[2] + dqn[3] * P.qn[3];
   const double screen =
       sqrt(pr[4] * pr[4] + pr[5] * pr[5]) * (0.5 * (double)(cam.width > cam.height ? cam.width : cam.height));
-
   if (accumulate) {
     for (int j = 0; j < 3; j++) g_pos[i * 3 + j] += (float)dpos[j];
     for (int j = 0; j < 4; j++) g_rot[i * 4 + j] += (float)((dqn[j] - rad * P.qn[j]) / P.qnorm);
     for (int j = 0; j < 3; j++) g_ls[i * 3 + j] += (float)dls[j];
     g_logit[i] += (float)pr[3];
-    for (int c = 0; c < 3; c++)
-      for (int k = 0; k < K; k++) g_sh[(i * 3 + c) * K + k] += (float)(dcol[c] * basis[k]);
     g_screen[i] += (float)screen;
     g_vis[i] += 1.f;
   } else {
@@ -232,14 +209,71 @@ __global__ void __launch_bounds__(128) k_chain(Cam cam, int64_t n, int deg, int 
     for (int j = 0; j < 4; j++) g_rot[i * 4 + j] = (float)((dqn[j] - rad * P.qn[j]) / P.qnorm);
     for (int j = 0; j < 3; j++) g_ls[i * 3 + j] = (float)dls[j];
     g_logit[i] = (float)pr[3];
-    for (int c = 0; c < 3; c++)
-      for (int k = 0; k < K; k++) g_sh[(i * 3 + c) * K + k] = (float)(dcol[c] * basis[k]);
     g_screen[i] = (float)screen;
     g_vis[i] = 1.f;
   }
   if (stats) {
     stats[i] += (float)screen;
     stats[n + i] += 1.f;
+  }
+}
+
+// sh.py:135-152 (+ backward.py:200) -- SH coefficients and the view-direction
+// path into positions.  128 rows per block; the block's coefficient rows and
+// their gradients move through shared memory so global traffic is coalesced.
+constexpr int CHAIN_SH_ROWS = 128;
+__global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, int deg,
+                                                            const float* __restrict__ pos,
+                                                            const float* __restrict__ sh,
+                                                            const uint32_t* __restrict__ tiles,
+                                                            const uint32_t* __restrict__ offset,
+                                                            const float* __restrict__ rows,
+                                                            float* __restrict__ grads, int accumulate) {
+  extern __shared__ float s_sh[];  // [CHAIN_SH_ROWS * 3K] coefficients, then gradients in place
+  const int K = (deg + 1) * (deg + 1);
+  const int W = 3 * K;
+  const int64_t i0 = (int64_t)blockIdx.x * CHAIN_SH_ROWS;
+  const int rows_here = (int)min((int64_t)CHAIN_SH_ROWS, n - i0);
+  const int64_t base = i0 * W;
+  const int tot = rows_here * W;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) s_sh[e] = sh[base + e];
+  __syncthreads();
+  const int64_t i = i0 + threadIdx.x;
+  float* my = s_sh + threadIdx.x * W;
+  if (threadIdx.x < rows_here) {
+    const uint32_t nt = tiles[i];
+    if (nt == 0) {
+      for (int e = 0; e < W; e++) my[e] = 0.f;
+    } else {
+      const float* rw = rows + (int64_t)offset[i] * 9;
+      double dir[3], rs, basis[16], col[3];
+      bool lo[3], hi[3];
+      sh_color64(cam, deg, pos + i * 3, my, dir, &rs, basis, col, lo, hi);
+      double dcol[3];
+      for (int c = 0; c < 3; c++) dcol[c] = (lo[c] || hi[c]) ? 0.0 : (double)rw[c];
+      // d_dir = sum_c sum_k dcol_c coeff_ck dY_k/ddir  (sh.py:147-148)
+      double gb[48];
+      sh_basis_grad64(deg, dir, gb);
+      double ddir[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < K; k++) {
+        const double vk = dcol[0] * (double)my[k] + dcol[1] * (double)my[K + k] + dcol[2] * (double)my[2 * K + k];
+        ddir[0] += vk * gb[k * 3 + 0];
+        ddir[1] += vk * gb[k * 3 + 1];
+        ddir[2] += vk * gb[k * 3 + 2];
+      }
+      const double radial = ddir[0] * dir[0] + ddir[1] * dir[1] + ddir[2] * dir[2];
+      float* g_pos = grads + i * 3;
+      for (int d = 0; d < 3; d++) g_pos[d] += (float)((ddir[d] - radial * dir[d]) / rs);
+      for (int c = 0; c < 3; c++)
+        for (int k = 0; k < K; k++) my[c * K + k] = (float)(dcol[c] * basis[k]);
+    }
+  }
+  __syncthreads();
+  float* g_sh = grads + 11 * n + base;
+  if (accumulate) {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] += s_sh[e];
+  } else {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] = s_sh[e];
   }
 }
 
@@ -297,10 +331,18 @@ extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, co
   if (n == 0) return SSR_OK;
   int tx, ty;
   tile_dims(cam, &tx, &ty);
-  const unsigned blocks = (unsigned)((n + 127) / 128);
   cudaStream_t st = (cudaStream_t)stream;
   const Cam c = to_cam(*cam);
-  k_chain<<<blocks, 128, 0, st>>>(c, n, sh_degree, tx, ty, positions, rotations, log_scales, sh, splats.tiles,
-                                  splats.offset, inst_rows, grads, accumulate, stats);
-  return check_launch("k_chain");
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  // inst_rows is scratch from here on: the geometry pass parks each Gaussian's
+  // merged colour gradient in its own first row for the SH pass
+  float* rows = const_cast<float*>(inst_rows);
+  k_chain_geo<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(c, n, K, tx, ty, positions, rotations, log_scales,
+                                                           splats.tiles, splats.offset, rows, grads, accumulate,
+                                                           stats);
+  SSR_TRY(check_launch("k_chain_geo"));
+  const size_t smem = (size_t)CHAIN_SH_ROWS * 3 * K * sizeof(float);
+  k_chain_sh<<<(unsigned)((n + CHAIN_SH_ROWS - 1) / CHAIN_SH_ROWS), CHAIN_SH_ROWS, smem, st>>>(
+      c, n, sh_degree, positions, sh, splats.tiles, splats.offset, rows, grads, accumulate);
+  return check_launch("k_chain_sh");
 }
