@@ -122,10 +122,12 @@ int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles);
 
 /* ---------------------------------------------------------- stage 3 */
 /* kernels.py:31-103: 16x16-tile front-to-back blend (fp32) with an fp64
- * guard-band re-walk of pixels whose discrete decisions sit within `band`
- * (relative) of a threshold. */
+ * guard-band re-walk of pixels whose discrete decisions sit within a relative
+ * band of a threshold: band_alpha around the alpha >= 1/255
+ * gate and the 0.99 cap, band_t around the T(1 - alpha) < 1e-4 termination. */
 int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
-                const int32_t* tile_ranges, ssr_frame frame, float band, void* stream);
+                const int32_t* tile_ranges, ssr_frame frame, float band_alpha, float band_t,
+                void* stream);
 
 /* ---------------------------------------------------------- stage 4 */
 /* kernels.py:106-353: per-instance rows [dcolor rgb, dlogit, dmu xy,

@@ -55,7 +55,7 @@ _SIGS = {
     "ssr_bin_tiles": [c_int64, c_int64, c_int32, c_int32, SsrSplats, c_void_p, c_void_p, c_void_p, c_int64,
                       c_void_p],
     "ssr_ckpt_floats": [c_int64, c_int32],
-    "ssr_forward": [c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_float, c_void_p],
+    "ssr_forward": [c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_float, c_float, c_void_p],
     "ssr_backward": [c_int32, c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_void_p, c_void_p, c_void_p,
                      c_void_p],
     "ssr_chain": [ctypes.POINTER(SsrCamera), c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -294,6 +294,26 @@ constexpr float LOG2E_F = 1.4426950408889634f;
 // reach, the soft term equals S0 to 3e-10 and gradient terms are ~1e-10.
 constexpr float FAR_POWER2 = -25.0f * 1.4426950408889634f;
 
+// Tile-relative mean split into an exact integer part and a float fraction:
+// dx = (px - mi) - mf, where px - mi is exact, so dx carries only one rounding
+// (6e-8 relative) instead of the rounding of a float mean near 32 (2e-6 px).
+struct StagedMean {
+  float xi, xf, yi, yf;
+};
+
+__device__ __forceinline__ StagedMean stage_mean(double mx, double my, int x00, int y00) {
+  StagedMean s;
+  const double rx = mx - (double)x00, ry = my - (double)y00;
+  const double ix = rint(rx), iy = rint(ry);
+  s.xi = (float)ix;
+  s.xf = (float)(rx - ix);
+  s.yi = (float)iy;
+  s.yf = (float)(ry - iy);
+  return s;
+}
+
+__device__ __forceinline__ float pair_d(float fp, float mi, float mf) { return __fsub_rn(__fsub_rn(fp, mi), mf); }
+
 struct StagedConic {
   float a2, b2, c2;
 };
@@ -341,7 +361,9 @@ __device__ __forceinline__ float soft_dev_poly(float y) {
 }
 
 __device__ __forceinline__ float soft_sigmoid_accurate(float alpha) {
-  return 1.0f / (1.0f + expf(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f)));
+  // ex2.approx (2^-22 rel) + rcp.approx: ~1e-7 abs on a value in [0.5, 1]
+  const float e = ex2_approx(__fmul_rn(__fsub_rn(ALPHA_MIN_F, alpha), 100.0f * LOG2E_F));
+  return __fdividef(1.0f, 1.0f + e);
 }
 
 __device__ __forceinline__ float soft_sigmoid(float alpha) {

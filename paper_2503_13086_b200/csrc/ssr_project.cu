@@ -24,8 +24,12 @@ __global__ void __launch_bounds__(256) k_preprocess(Cam cam, int64_t n, int deg,
   sh_color64(cam, deg, pos + i * 3, sh + i * 3 * K, dir, &rs, basis, col, lo, hi);
   const double opa = 1.0 / (1.0 + exp(-(double)logit[i]));
   reinterpret_cast<double2*>(o.mean)[i] = make_double2(P.u, P.v);
+  // near-singular conics (1 - |b|/sqrt(ac) < 1e-3) are the only ones whose fp32
+  // power can round across 0; they carry a negative fp32 opacity so the
+  // forward can test the power > 0 guard band with a warp-uniform branch
+  const bool fragile = 1.0 - fabs(P.qb) / sqrt(P.qa * P.qc) < 1e-3;
   reinterpret_cast<float4*>(o.conic_opa)[i] =
-      make_float4((float)P.qa, (float)P.qb, (float)P.qc, (float)opa);
+      make_float4((float)P.qa, (float)P.qb, (float)P.qc, fragile ? -(float)opa : (float)opa);
   reinterpret_cast<float4*>(o.color)[i] = make_float4((float)col[0], (float)col[1], (float)col[2], 0.f);
   double2* c64 = reinterpret_cast<double2*>(o.conic_opa64) + 2 * i;
   c64[0] = make_double2(P.qa, P.qb);

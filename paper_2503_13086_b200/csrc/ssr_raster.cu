@@ -23,7 +23,7 @@ struct RasterArgs {
   int width, height, tiles_x, tiles_y;
   float bg[3];
   double bg64[3];
-  float band;
+  float band, band_t;
   const double2* mean;
   const float4* conic_opa;
   const float4* color;
@@ -62,12 +62,12 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const bool inside = px < a.width && py < a.height;
   const int2 rg = a.ranges[t];
   const int s0 = rg.x, s1 = rg.y;
-  const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
-  const float band = a.band;
+  float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
+  const float band = a.band, band_t = a.band_t;
 
-  __shared__ float4 sA[TILE_PX];  // tile-relative mean x, y; staged conic a2, b2
-  __shared__ float4 sB[TILE_PX];  // opacity, r, g, b
-  __shared__ float sC[TILE_PX];   // staged conic c2
+  __shared__ float4 sM[TILE_PX];  // staged mean (x int, x frac, y int, y frac)
+  __shared__ float4 sA[TILE_PX];  // staged conic a2, b2, c2; opacity
+  __shared__ float4 sB[TILE_PX];  // r, g, b
   __shared__ int sMax[8];
 
   float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, sdev = 0.f;
@@ -85,9 +85,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
       const StagedConic q = stage_conic(co.x, co.y, co.z);
-      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), q.a2, q.b2);
-      sB[tid] = make_float4(co.w, col.x, col.y, col.z);
-      sC[tid] = q.c2;
+      const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
+      sM[tid] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
+      sA[tid] = make_float4(q.a2, q.b2, q.c2, co.w);  // opacity < 0 marks a fragile conic
+      sB[tid] = col;
     }
     __syncthreads();
     if (!done) {
@@ -101,22 +102,23 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         }
         const int jend = min(j0 + BUCKET, n);
         for (int j = j0; j < jend; j++) {
+          const float4 M = sM[j];
           const float4 A = sA[j];
-          const float dx = fpx - A.x, dy = fpy - A.y;
+          asm volatile("" : "+f"(fpx), "+f"(fpy));  // keep the pixel coordinates in registers
+          const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
           const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
           float qpos;
-          const float p2 = pair_power2(dxx, dxy, dyy, A.z, A.w, sC[j], qpos);
+          const float p2 = pair_power2(dxx, dxy, dyy, A.x, A.y, A.z, qpos);
           if (p2 < FAR_POWER2) {
             scnt++;
             continue;
           }
-          if (p2 > 1e-6f * qpos && qpos != 0.f) {  // near the power > 0 skip decision
+          if (A.w < 0.f && p2 > 1e-6f * qpos && qpos != 0.f) {  // fragile conic near power > 0
             flag = true;
             goto walk_done;
           }
           if (p2 > 0.f) continue;
-          const float4 B = sB[j];
-          float alpha = pair_alpha2(B.x, p2);
+          float alpha = pair_alpha2(fabsf(A.w), p2);
           if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
             flag = true;
             goto walk_done;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           }
           if (alpha < ALPHA_MIN_F) continue;
           const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
-          if (fabsf(test - T_EPS_F) < T_EPS_F * 2.f * band) {
+          if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
             flag = true;
             goto walk_done;
           }
@@ -141,9 +143,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
             goto walk_done;
           }
           const float w = __fmul_rn(alpha, T);
-          c0 = __fmaf_rn(B.y, w, c0);
-          c1 = __fmaf_rn(B.z, w, c1);
-          c2 = __fmaf_rn(B.w, w, c2);
+          const float4 B = sB[j];
+          c0 = __fmaf_rn(B.x, w, c0);
+          c1 = __fmaf_rn(B.y, w, c1);
+          c2 = __fmaf_rn(B.z, w, c2);
           hard++;
           T = test;
         }
@@ -229,11 +232,16 @@ struct Pix64 {
 };
 
 // Front-to-back walk of one pixel by one warp (lanes = 32 consecutive slots).
-__device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, double yy, Pix64& r) {
+// When ck != nullptr the fp32 bucket checkpoint (T, C_front) of every chunk
+// boundary is written for the backward fix-up (chunks coincide with buckets).
+__device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, double yy, Pix64& r,
+                             float4* ck = nullptr) {
   const int lane = threadIdx.x & 31;
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, soft = 0.0;
   int hard = 0, nw = s1 - s0, term = 0;
   for (int cb = s0; cb < s1; cb += 32) {
+    if (ck && cb > s0 && lane == 0)
+      ck[(size_t)((cb - s0) >> 5) * TILE_PX] = make_float4((float)T, (float)C0, (float)C1, (float)C2);
     Slot64 q;
     slot64(a, cb + lane, s1, xx, yy, q);
     const double f = q.cand ? (1.0 - q.alpha) : 1.0;
@@ -273,22 +281,45 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
   r.term = term;
 }
 
-// Forward fix-up: one warp per tile, flagged pixels re-walked in float64.
-__global__ void __launch_bounds__(32) k_forward_fixup(RasterArgs a) {
+// Block-wide list of a tile's flagged pixels, in pixel order.
+__device__ __forceinline__ int flagged_list(const RasterArgs& a, int tx, int ty, int* list, int* wcount) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int px = tx * TILE + (tid & 15), py = ty * TILE + (tid >> 4);
+  const bool f = px < a.width && py < a.height && a.flagged[(size_t)py * a.width + px];
+  const unsigned m = __ballot_sync(FULL, f);
+  if (lane == 0) wcount[warp] = __popc(m);
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < 8; w++) {
+    if (w < warp) base += wcount[w];
+    total += wcount[w];
+  }
+  if (f) list[base + __popc(m & ((1u << lane) - 1u))] = tid;
+  __syncthreads();
+  return total;
+}
+
+// Forward fix-up: one CTA (8 warps) per tile with flagged pixels; each warp
+// re-walks flagged pixels in float64 (pixels are independent).
+__global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
   const int t = blockIdx.x;
   const int2 info = a.tile_info[t];
   if (info.y == 0) return;
-  const int lane = threadIdx.x;
+  __shared__ int list[TILE_PX];
+  __shared__ int wcount[8];
+  __shared__ int smax;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int nflag = flagged_list(a, tx, ty, list, wcount);
+  if (threadIdx.x == 0) smax = info.x;
+  __syncthreads();
   const int2 rg = a.ranges[t];
-  int maxw = info.x;
-  for (int p = 0; p < TILE_PX; p++) {
+  for (int f = warp; f < nflag; f += 8) {
+    const int p = list[f];
     const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
-    if (px >= a.width || py >= a.height) continue;
     const size_t pix = (size_t)py * a.width + px;
-    if (!a.flagged[pix]) continue;
     Pix64 r;
-    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r);
+    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt + ckpt_base(rg.x, t) + p);
     if (lane == 0) {
       a.image[pix * 3 + 0] = (float)(r.C[0] + a.bg64[0] * r.T);
       a.image[pix * 3 + 1] = (float)(r.C[1] + a.bg64[1] * r.T);
@@ -298,10 +329,11 @@ __global__ void __launch_bounds__(32) k_forward_fixup(RasterArgs a) {
       a.term[pix] = (uint8_t)r.term;
       a.hard[pix] = r.hard;
       a.soft[pix] = r.soft;
+      atomicMax(&smax, r.nw);
     }
-    maxw = max(maxw, r.nw);
   }
-  if (lane == 0) a.tile_info[t].x = maxw;
+  __syncthreads();
+  if (threadIdx.x == 0) a.tile_info[t].x = smax;
 }
 
 // ------------------------------------------------------------------ backward, splat-parallel (fp32)
@@ -342,9 +374,15 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
   }
   __syncthreads();
 
+  // does any pixel of the tile carry a soft-count gradient?  If not, pairs
+  // with alpha < 1/255 contribute exactly nothing and are skipped (uniform).
+  const bool use_soft = __syncthreads_or(sPA[tid].w != 0.f);
+
   const int nb = (maxw + 31) >> 5;
   const float4* ckt = a.ckpt + ckpt_base(s0, t);
   const unsigned lt_mask = (1u << lane) - 1u;
+  uint8_t* const myList = sList[warp];
+  float2* const mySeed = sSeed[warp];
   for (int b = warp; b < nb; b += 8) {
     const int kb = b * 32;
     // live pixels of this bucket: the walk reaches slot kb (compacted, pixel order)
@@ -354,97 +392,106 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
       const int p = c * 32 + lane;
       const bool lv = (__float_as_int(sPB[p].w) >> 1) > kb;
       const unsigned msk = __ballot_sync(FULL, lv);
-      if (lv) sList[warp][n_live + __popc(msk & lt_mask)] = (uint8_t)p;
+      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint8_t)p;
       n_live += __popc(msk);
     }
     __syncwarp();
     for (int j = lane; j < n_live; j += 32) {
-      const int p = sList[warp][j];
+      const int p = myList[j];
       float2 sd = make_float2(1.f, 0.f);
       if (b > 0) {
         const float4 c = ckt[(size_t)b * TILE_PX + p];
         const float4 w = sPA[p];
         sd = make_float2(c.x, w.x * c.y + w.y * c.z + w.z * c.w);
       }
-      sSeed[warp][j] = sd;
+      mySeed[j] = sd;
     }
     __syncwarp();
     const int k = kb + lane;
     const bool live = k < maxw;
-    float mrx = 0.f, mry = 0.f, ca = 0.f, cb = 0.f, cc = 0.f, opa = 0.f, cr = 0.f, cg = 0.f, cbl = 0.f;
+    float ca = 0.f, cb = 0.f, cc = 0.f, opa = 0.f, cr = 0.f, cg = 0.f, cbl = 0.f;
     StagedConic q = {0.f, 0.f, 0.f};
+    StagedMean sm = {0.f, 0.f, 0.f, 0.f};
+    float p2_min = FAR_POWER2;  // pairs below this contribute nothing
     uint32_t orow = 0;
     if (live) {
       const uint32_t g = a.inst[s0 + k];
       const double2 m = a.mean[g];
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
-      mrx = (float)(m.x - (double)x00);
-      mry = (float)(m.y - (double)y00);
+      sm = stage_mean(m.x, m.y, x00, y00);
       ca = co.x;
       cb = co.y;
       cc = co.z;
-      opa = co.w;
+      opa = fabsf(co.w);
       q = stage_conic(ca, cb, cc);
       cr = col.x;
       cg = col.y;
       cbl = col.z;
       orow = inst_row(a, g, tx, ty);
+      // without soft gradients only alpha >= 1/255 matters: alpha < 0.999/255
+      // is certain below log2(0.999 / (255 opacity))
+      if (!use_soft) p2_min = fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / opa));
     }
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
     float T = 1.f, H = 0.f;
     const int n_steps = n_live + 31;
+    const int last = n_live - 1;
     for (int i = 0; i < n_steps; i++) {
       float Tin = __shfl_up_sync(FULL, T, 1);
       float Hin = __shfl_up_sync(FULL, H, 1);
-      if (lane == 0 && i < n_live) {
-        const float2 sd = sSeed[warp][i];
+      const float2 sd = mySeed[min(i, last)];  // broadcast read
+      if (lane == 0) {
         Tin = sd.x;
         Hin = sd.y;
       }
       T = Tin;
       H = Hin;
       const int j = i - lane;
-      if (!live || (unsigned)j >= (unsigned)n_live) continue;
-      const int p = sList[warp][j];
+      const bool inr = live && (unsigned)j < (unsigned)n_live;
+      const int p = myList[inr ? j : 0];
       const float4 PB = sPB[p];
       const int nwt = __float_as_int(PB.w);
       const int nw = nwt >> 1;
-      if (k >= nw) continue;
-      const float dx = PB.x - mrx, dy = PB.y - mry;
+      const float dx = pair_d(PB.x, sm.xi, sm.xf), dy = pair_d(PB.y, sm.yi, sm.yf);
       const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
       float qpos;
       const float p2 = pair_power2(dxx, dxy, dyy, q.a2, q.b2, q.c2, qpos);
-      if (p2 > 0.f || p2 < FAR_POWER2) continue;  // far pairs: |contribution| < 1e-9 relative
-      const float araw = pair_alpha2(opa, p2);
-      const bool capped = araw > ALPHA_CAP_F;
-      const float alpha = capped ? ALPHA_CAP_F : araw;
-      const bool blended = alpha >= ALPHA_MIN_F && !((nwt & 1) && k == nw - 1);
-      const float4 w = sPA[p];
-      float dlda = 0.f;
-      if (blended) {
-        const float wc = w.x * cr + w.y * cg + w.z * cbl;
-        const float aT = alpha * T;
-        g0 = fmaf(aT, w.x, g0);
-        g1 = fmaf(aT, w.y, g1);
-        g2 = fmaf(aT, w.z, g2);
-        const float one_m = __fsub_rn(1.f, alpha);
-        const float awc = aT * wc;
-        const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
-        dlda = T * wc - __fdividef(sdot, one_m);
-        H += awc;
-        T = __fmul_rn(T, one_m);
-      }
-      if (!capped) {
-        const float sv = soft_sigmoid(alpha);
-        g3 = fmaf(dlda + w.w * sv * (1.f - sv) * 100.f, alpha, g3);
+      if (inr && k < nw && p2 <= 0.f && p2 >= p2_min) {
+        const float araw = pair_alpha2(opa, p2);
+        const bool capped = araw > ALPHA_CAP_F;
+        const float alpha = capped ? ALPHA_CAP_F : araw;
+        const bool blended = alpha >= ALPHA_MIN_F && !((nwt & 1) && k == nw - 1);
+        const float4 w = sPA[p];
+        float dlda = 0.f;
         if (blended) {
-          const float gp = dlda * alpha;
-          g4 = fmaf(gp, ca * dx + cb * dy, g4);
-          g5 = fmaf(gp, cb * dx + cc * dy, g5);
-          g6 = fmaf(gp, dxx, g6);
-          g7 = fmaf(gp, dxy, g7);
-          g8 = fmaf(gp, dyy, g8);
+          const float wc = w.x * cr + w.y * cg + w.z * cbl;
+          const float aT = alpha * T;
+          g0 = fmaf(aT, w.x, g0);
+          g1 = fmaf(aT, w.y, g1);
+          g2 = fmaf(aT, w.z, g2);
+          const float one_m = __fsub_rn(1.f, alpha);
+          const float awc = aT * wc;
+          const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
+          dlda = T * wc - __fdividef(sdot, one_m);
+          H += awc;
+          T = __fmul_rn(T, one_m);
+        }
+        if (!capped) {
+          float gs = dlda;
+          if (use_soft) {
+            const float sv = soft_sigmoid(alpha);
+            gs = fmaf(w.w * sv * (1.f - sv), 100.f, gs);
+          }
+          g3 = fmaf(gs, alpha, g3);
+          if (blended) {
+            const float gp = dlda * alpha;
+            g4 = fmaf(gp, ca * dx + cb * dy, g4);
+            g5 = fmaf(gp, cb * dx + cc * dy, g5);
+            g6 = fmaf(gp, dxx, g6);
+            g7 = fmaf(gp, dxy, g7);
+            g8 = fmaf(gp, dyy, g8);
+          }
         }
       }
     }
@@ -485,7 +532,7 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
   __shared__ float4 sA[32], sB[32];
-  __shared__ float4 sQ[32];
+  __shared__ float4 sQ[32], sM[32];
   __shared__ uint32_t sRow[32];
   __shared__ float part[8][32][9];
 
@@ -511,8 +558,10 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
       const StagedConic q = stage_conic(co.x, co.y, co.z);
-      sA[tid] = make_float4((float)(m.x - (double)x00), (float)(m.y - (double)y00), co.x, co.y);
-      sB[tid] = make_float4(co.z, co.w, col.x, col.y);
+      const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
+      sM[tid] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
+      sA[tid] = make_float4(0.f, 0.f, co.x, co.y);
+      sB[tid] = make_float4(co.z, fabsf(co.w), col.x, col.y);
       sQ[tid] = make_float4(q.a2, q.b2, q.c2, col.z);
       sRow[tid] = inst_row(a, g, tx, ty);
     }
@@ -522,8 +571,8 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
       const int k = kb + j;
       float c[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (k < nw) {
-        const float4 A = sA[j], B = sB[j], Q = sQ[j];
-        const float dx = fpx - A.x, dy = fpy - A.y;
+        const float4 A = sA[j], B = sB[j], Q = sQ[j], M = sM[j];
+        const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
         const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
         float qpos;
         const float p2 = pair_power2(dxx, dxy, dyy, Q.x, Q.y, Q.z, qpos);
@@ -584,40 +633,56 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
 }
 
 // ------------------------------------------------------------------ backward fix-up (fp64)
-// One warp per tile with flagged pixels; pixels in order, lanes over slots.
-// Adds the float64 pixel-walk gradient terms (kernels.py:149-193 semantics,
-// front-to-back) into the rows the fp32 kernel wrote.  Sequential over pixels
-// and lane-disjoint within a pixel, so no atomics and deterministic.
-__global__ void __launch_bounds__(32) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
-                                                       const float* __restrict__ d_soft, float* __restrict__ rows) {
+// Adds the float64 pixel-walk gradient terms of guard-band pixels
+// (kernels.py:149-193 semantics, front to back) into the rows the fp32 kernel
+// wrote.  One warp per (tile, 32-slot bucket): it seeds each flagged pixel of
+// the tile from the bucket checkpoint the forward fix-up wrote, evaluates the
+// bucket's slots in float64 (lanes = slots), and accumulates the pixels'
+// terms in a fixed (pixel) order before one add per slot -- deterministic
+// without atomics, and parallel over buckets.  Backward decisions do not
+// depend on T (termination comes from n_walk / terminated), so fp32 seeds only
+// perturb gradient values, never which slots blend.
+constexpr int FIXUP_YBLOCKS = 8;  // gridDim.y; warp w of block y takes buckets y*8+w, +64, ...
+__global__ void __launch_bounds__(256) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
+                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
   const int t = blockIdx.x;
-  if (a.tile_info[t].y == 0) return;
-  const int lane = threadIdx.x;
+  const int2 info = a.tile_info[t];
+  if (info.y == 0) return;
+  const int nb = (info.x + 31) >> 5;
+  if ((int)blockIdx.y * 8 >= nb) return;
+  __shared__ int list[TILE_PX];
+  __shared__ int wcount[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int nflag = flagged_list(a, tx, ty, list, wcount);
   const int2 rg = a.ranges[t];
   const int s0 = rg.x, s1 = rg.y;
-  for (int p = 0; p < TILE_PX; p++) {
-    const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
-    if (px >= a.width || py >= a.height) continue;
-    const size_t pix = (size_t)py * a.width + px;
-    if (!a.flagged[pix]) continue;
-    Pix64 r;
-    const double xx = (double)px, yy = (double)py;
-    walk_pixel64(a, s0, s1, xx, yy, r);
-    const double w0 = d_image[pix * 3], w1 = d_image[pix * 3 + 1], w2 = d_image[pix * 3 + 2];
-    const double ws = d_soft ? (double)d_soft[pix] : 0.0;
-    const double wimg = w0 * (r.C[0] + a.bg64[0] * r.T) + w1 * (r.C[1] + a.bg64[1] * r.T) +
-                        w2 * (r.C[2] + a.bg64[2] * r.T);
-    double T = 1.0, H = 0.0;
-    const int send = s0 + r.nw;
-    for (int cb = s0; cb < send; cb += 32) {
+  const float4* ckt = a.ckpt + ckpt_base(s0, t);
+  for (int b = blockIdx.y * 8 + warp; b < nb; b += FIXUP_YBLOCKS * 8) {
+    const int kb = b * 32, k = kb + lane;
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int f = 0; f < nflag; f++) {
+      const int p = list[f];
+      const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
+      const size_t pix = (size_t)py * a.width + px;
+      const int nw = a.n_walk[pix];
+      if (nw <= kb) continue;  // warp-uniform
+      const int term = a.term[pix];
+      const double w0 = d_image[pix * 3], w1 = d_image[pix * 3 + 1], w2 = d_image[pix * 3 + 2];
+      const double ws = d_soft ? (double)d_soft[pix] : 0.0;
+      const double wimg =
+          w0 * (double)a.image[pix * 3] + w1 * (double)a.image[pix * 3 + 1] + w2 * (double)a.image[pix * 3 + 2];
+      double T = 1.0, H = 0.0;
+      if (b > 0) {
+        const float4 c = ckt[(size_t)b * TILE_PX + p];
+        T = c.x;
+        H = w0 * c.y + w1 * c.z + w2 * c.w;
+      }
       Slot64 q;
-      const int s = cb + lane;
-      slot64(a, s, send, xx, yy, q);
-      const int k = s - s0;
-      const bool bl = q.cand && !(r.term && k == r.nw - 1);
-      const double f = bl ? (1.0 - q.alpha) : 1.0;
-      double P = f;
+      slot64(a, s0 + k, s0 + nw, (double)px, (double)py, q);
+      const bool bl = q.cand && !(term && k == nw - 1);
+      const double f1 = bl ? (1.0 - q.alpha) : 1.0;
+      double P = f1;
       for (int d = 1; d < 32; d <<= 1) {
         const double o = __shfl_up_sync(FULL, P, d);
         if (lane >= d) P *= o;
@@ -634,38 +699,37 @@ __global__ void __launch_bounds__(32) k_backward_fixup(RasterArgs a, const float
       }
       const double Hb = H + (E - e);
       if (q.valid && !q.skip) {
-        double c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         double dlda = 0.0;
         if (bl) {
           const double aT = q.alpha * Tb;
-          c[0] = aT * w0;
-          c[1] = aT * w1;
-          c[2] = aT * w2;
+          acc[0] += aT * w0;
+          acc[1] += aT * w1;
+          acc[2] += aT * w2;
           dlda = Tb * wc - (wimg - Hb - aT * wc) / (1.0 - q.alpha);
         }
         if (!q.capped) {
-          c[3] = (dlda + ws * q.sv * (1.0 - q.sv) / SOFT_TAU) * q.alpha * (1.0 - q.opa);
+          acc[3] += (dlda + ws * q.sv * (1.0 - q.sv) / SOFT_TAU) * q.alpha * (1.0 - q.opa);
           if (bl) {
             const double gp = dlda * q.alpha;
-            c[4] = gp * (q.qa * q.dx + q.qb * q.dy);
-            c[5] = gp * (q.qb * q.dx + q.qc * q.dy);
-            c[6] = gp * (-0.5 * q.dx * q.dx);
-            c[7] = gp * (-q.dx * q.dy);
-            c[8] = gp * (-0.5 * q.dy * q.dy);
+            acc[4] += gp * (q.qa * q.dx + q.qb * q.dy);
+            acc[5] += gp * (q.qb * q.dx + q.qc * q.dy);
+            acc[6] += gp * (-0.5 * q.dx * q.dx);
+            acc[7] += gp * (-q.dx * q.dy);
+            acc[8] += gp * (-0.5 * q.dy * q.dy);
           }
         }
-        float* row = rows + (size_t)inst_row(a, q.g, tx, ty) * 9;
-        for (int j = 0; j < 9; j++) row[j] += (float)c[j];
       }
-      H += __shfl_sync(FULL, E, 31);
-      T *= __shfl_sync(FULL, P, 31);
-      __syncwarp();
+    }
+    if (s0 + k < s1) {
+      float* row = rows + (size_t)inst_row(a, a.inst[s0 + k], tx, ty) * 9;
+      for (int j = 0; j < 9; j++)
+        if (acc[j] != 0.0) row[j] += (float)acc[j];
     }
   }
 }
 
 static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* ranges, const ssr_frame& f,
-                            float band) {
+                            float band, float band_t) {
   RasterArgs a;
   a.width = f.width;
   a.height = f.height;
@@ -676,6 +740,7 @@ static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* 
     a.bg64[i] = (double)f.bg[i];
   }
   a.band = band;
+  a.band_t = band_t;
   a.mean = (const double2*)sp.mean;
   a.conic_opa = (const float4*)sp.conic_opa;
   a.color = (const float4*)sp.color;
@@ -702,17 +767,17 @@ static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* 
 using namespace ssr;
 
 extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss, const int32_t* tile_ranges,
-                           ssr_frame frame, float band, void* stream) {
+                           ssr_frame frame, float band_alpha, float band_t, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int n_tiles = frame.tiles_x * frame.tiles_y;
-  if (n_tiles <= 0 || frame.width <= 0 || frame.height <= 0 || m < 0 || !(band >= 0.f)) {
+  if (n_tiles <= 0 || frame.width <= 0 || frame.height <= 0 || m < 0 || !(band_alpha >= 0.f) || !(band_t >= 0.f)) {
     set_error("ssr_forward: invalid argument");
     return SSR_ERR_INVALID;
   }
-  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, band);
+  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, band_alpha, band_t);
   k_forward<<<n_tiles, TILE_PX, 0, st>>>(a);
   SSR_TRY(check_launch("k_forward"));
-  k_forward_fixup<<<n_tiles, 32, 0, st>>>(a);
+  k_forward_fixup<<<n_tiles, 256, 0, st>>>(a);
   return check_launch("k_forward_fixup");
 }
 
@@ -726,12 +791,12 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     return SSR_ERR_INVALID;
   }
   if (m == 0) return SSR_OK;
-  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f);
+  RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f, 0.f);
   if (layout == 0)
     k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
   else
     k_backward_pixel<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
   SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
-  k_backward_fixup<<<n_tiles, 32, 0, st>>>(a, d_image, d_soft, inst_rows);
+  k_backward_fixup<<<dim3(n_tiles, FIXUP_YBLOCKS), 256, 0, st>>>(a, d_image, d_soft, inst_rows);
   return check_launch("k_backward_fixup");
 }

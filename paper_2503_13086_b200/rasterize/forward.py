@@ -12,9 +12,12 @@ from ..camera import CameraFrame
 from ..errors import InvalidParameter
 from .projection import ProjectedSplats, project_field
 
-# Relative guard band of the fp32 walk's discrete decisions; pixels inside it
-# are re-walked in float64.  The termination band is 2x this.
-GUARD_BAND = 1e-4
+# Relative guard bands of the fp32 walk's discrete decisions; pixels inside
+# either are re-walked in float64.  GUARD_BAND covers the
+# alpha >= 1/255 gate and the 0.99 cap, GUARD_BAND_T the T(1-alpha) < 1e-4
+# termination (whose fp32 error accumulates over the walk).
+GUARD_BAND = 1e-5
+GUARD_BAND_T = 1e-4
 
 
 @dataclass
@@ -53,10 +56,13 @@ class RenderOutput:
         return f
 
 
-def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: float = GUARD_BAND) -> RenderOutput:
+def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: float = None,
+           band_t: float = None) -> RenderOutput:
     """Render the field from ``cam`` over a constant background colour."""
     if workers < 1:
         raise InvalidParameter(f"workers must be >= 1, got {workers}")
+    band = GUARD_BAND if band is None else float(band)
+    band_t = GUARD_BAND_T if band_t is None else float(band_t)
     bg = np.asarray(bg, dtype=np.float64).reshape(3)
     splats = project_field(field, cam)
     dev = splats.tile_ranges.device
@@ -72,5 +78,5 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
         ckpt=e(int(_lib.load().ssr_ckpt_floats(m, n_tiles))),
     )
     _lib.call("ssr_forward", m, splats.struct(), splats.inst_gauss.data_ptr() if m else None,
-              splats.tile_ranges.data_ptr(), out.frame_struct(), float(band), _lib.stream_ptr())
+              splats.tile_ranges.data_ptr(), out.frame_struct(), band, band_t, _lib.stream_ptr())
     return out
