@@ -62,6 +62,8 @@ typedef struct ssr_splats {
   int32_t* rect;       /* N x 4  tile rect (tx0, ty0, tx1, ty1), exclusive upper */
   uint32_t* tiles;     /* N      tiles touched (0 = culled) */
   uint32_t* offset;    /* N      first instance id: tiles scanned in (fp64 depth, row) order */
+  uint32_t* row_offset; /* N     first gradient row: tiles scanned in field-row order, so a
+                            block of consecutive rows owns one contiguous range of inst_rows */
 } ssr_splats;
 
 /* Render-time per-pixel / per-tile state retained for the backward. */
@@ -132,7 +134,7 @@ int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
 /* ---------------------------------------------------------- stage 4 */
 /* kernels.py:106-353: per-instance rows [dcolor rgb, dlogit, dmu xy,
  * dconic abc] (9 floats) stored at the instance's splat-major position
- * (splats.offset[g] + local tile index).  layout 0 = splat-parallel
+ * (splats.row_offset[g] + local tile index).  layout 0 = splat-parallel
  * (Taming-style warp per 32-splat bucket), 1 = pixel-parallel.  Rows of
  * guard-band pixels are added by an fp64 pixel walk. */
 int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,

@@ -183,7 +183,11 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   size_t sb = scan_temp_bytes(n);
   SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb, cnt, off_sorted, (int)n, st), "scan tiles"));
   k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev);
-  return check_launch("k_scatter_offsets");
+  SSR_TRY(check_launch("k_scatter_offsets"));
+  // gradient-row offsets in field-row order (contiguous per block of rows for the chain)
+  size_t sb2 = scan_temp_bytes(n);
+  return check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb2, splats.tiles, splats.row_offset, (int)n, st),
+                    "row-order scan");
 }
 
 extern "C" int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes) {

@@ -75,17 +75,42 @@ __global__ void k_project_aux(Cam cam, int64_t n, int deg, int tiles_x, int tile
 // backward.py:110-206 (geometry half) -- one thread per field row: merge the
 // row's instance rows in splat-major (= ascending tile, bincount) order, then
 // chain d_mu / d_conic through the projection to position, rotation and
-// log-scale in float64.  The merged colour gradient is handed to k_chain_sh
-// in the first three floats of the Gaussian's own first instance row.
-__global__ void __launch_bounds__(128) k_chain_geo(Cam cam, int64_t n, int K, int tiles_x, int tiles_y,
-                                                   const float* __restrict__ pos, const float* __restrict__ rot,
-                                                   const float* __restrict__ ls,
-                                                   const uint32_t* __restrict__ tiles,
-                                                   const uint32_t* __restrict__ offset, float* __restrict__ rows,
-                                                   float* __restrict__ grads, int accumulate,
-                                                   float* __restrict__ stats) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// log-scale in float64.  Rows are stored in field-row order, so a block's 128
+// field rows own one contiguous range of inst_rows, staged through shared
+// memory with coalesced loads.  The merged colour gradient is handed to
+// k_chain_sh in the first three floats of the Gaussian's own first row.
+constexpr int CHAIN_ROWS = 128;
+constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
+__global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(Cam cam, int64_t n, int K, int tiles_x, int tiles_y,
+                                                          const float* __restrict__ pos, const float* __restrict__ rot,
+                                                          const float* __restrict__ ls,
+                                                          const uint32_t* __restrict__ tiles,
+                                                          const uint32_t* __restrict__ roff, float* __restrict__ rows,
+                                                          float* __restrict__ grads, int accumulate,
+                                                          float* __restrict__ stats) {
+  __shared__ __align__(16) float s_rows[CHAIN_STAGE_FLOATS + 4];
+  __shared__ uint64_t mbar;
+  const int64_t i0 = (int64_t)blockIdx.x * CHAIN_ROWS;
+  const int rows_here = (int)min((int64_t)CHAIN_ROWS, n - i0);
+  const uint32_t r_begin = roff[i0];
+  const uint32_t r_end = roff[i0 + rows_here - 1] + tiles[i0 + rows_here - 1];
+  const int64_t n_floats = (int64_t)(r_end - r_begin) * 9;
+  // 16-byte aligned window [a0, a1) covering the block's rows (inst_rows has >= 16 B slack)
+  const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
+  const int pad = (int)((b0 - a0) >> 2);  // floats before the first row
+  const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
+  const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  if (staged) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&mbar, (uint32_t)bytes);
+      bulk_g2s(s_rows, reinterpret_cast<const char*>(rows) + a0, (uint32_t)bytes, &mbar);
+    }
+    mbar_wait(&mbar, 0);
+  }
+  const int64_t i = i0 + threadIdx.x;
+  if (threadIdx.x >= rows_here) return;
   const int S = 11 + 3 * K;
   float* g_pos = grads;
   float* g_rot = grads + 3 * n;
@@ -107,12 +132,13 @@ __global__ void __launch_bounds__(128) k_chain_geo(Cam cam, int64_t n, int K, in
   }
   // bincount merge (backward.py:110-118): ascending tile order
   double pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  float* rw = rows + (int64_t)offset[i] * 9;
+  const float* rw = staged ? s_rows + pad + (int64_t)(roff[i] - r_begin) * 9 : rows + (int64_t)roff[i] * 9;
   for (uint32_t j = 0; j < nt; j++)
     for (int c = 0; c < 9; c++) pr[c] += (double)rw[j * 9 + c];
-  rw[0] = (float)pr[0];
-  rw[1] = (float)pr[1];
-  rw[2] = (float)pr[2];
+  float* dst = rows + (int64_t)roff[i] * 9;
+  dst[0] = (float)pr[0];
+  dst[1] = (float)pr[1];
+  dst[2] = (float)pr[2];
 
   Proj64 P;
   project64(cam, pos + i * 3, rot + i * 4, ls + i * 3, tiles_x, tiles_y, P);
@@ -225,50 +251,111 @@ __global__ void __launch_bounds__(128) k_chain_geo(Cam cam, int64_t n, int K, in
 // sh.py:135-152 (+ backward.py:200) -- SH coefficients and the view-direction
 // path into positions.  128 rows per block; the block's coefficient rows and
 // their gradients move through shared memory so global traffic is coalesced.
+// Templated on the degree so the basis lives in registers; the direction
+// gradient sum_k v_k dY_k/ddir (v_k = sum_c dcol_c coeff_ck) is written out
+// term by term (sh.py:68-111) instead of materialising dY/ddir.
 constexpr int CHAIN_SH_ROWS = 128;
-__global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, int deg,
-                                                            const float* __restrict__ pos,
+
+template <int DEG>
+__device__ __forceinline__ void sh_dir_grad(const double* v, double x, double y, double z, double* g) {
+  const double C1 = 0.4886025119029199;
+  g[0] = g[1] = g[2] = 0.0;
+  if (DEG >= 1) {
+    g[1] += v[1] * (-C1);
+    g[2] += v[2] * C1;
+    g[0] += v[3] * (-C1);
+  }
+  if (DEG >= 2) {
+    const double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
+                 C23 = -1.0925484305920792, C24 = 0.5462742152960396;
+    g[0] += v[4] * (C20 * y) + v[6] * (C22 * (-2.0 * x)) + v[7] * (C23 * z) + v[8] * (C24 * (2.0 * x));
+    g[1] += v[4] * (C20 * x) + v[5] * (C21 * z) + v[6] * (C22 * (-2.0 * y)) + v[8] * (C24 * (-2.0 * y));
+    g[2] += v[5] * (C21 * y) + v[6] * (C22 * (4.0 * z)) + v[7] * (C23 * x);
+  }
+  if (DEG >= 3) {
+    const double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
+                 C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
+                 C36 = -0.5900435899266435;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    g[0] += v[9] * (C30 * 6.0 * x * y) + v[10] * (C31 * y * z) + v[11] * (C32 * (-2.0 * x * y)) +
+            v[12] * (C33 * (-6.0 * x * z)) + v[13] * (C34 * (4.0 * zz - 3.0 * xx - yy)) +
+            v[14] * (C35 * (2.0 * x * z)) + v[15] * (C36 * (3.0 * xx - 3.0 * yy));
+    g[1] += v[9] * (C30 * (3.0 * xx - 3.0 * yy)) + v[10] * (C31 * x * z) + v[11] * (C32 * (4.0 * zz - xx - 3.0 * yy)) +
+            v[12] * (C33 * (-6.0 * y * z)) + v[13] * (C34 * (-2.0 * x * y)) + v[14] * (C35 * (-2.0 * y * z)) +
+            v[15] * (C36 * (-6.0 * x * y));
+    g[2] += v[10] * (C31 * x * y) + v[11] * (C32 * (8.0 * y * z)) + v[12] * (C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy)) +
+            v[13] * (C34 * (8.0 * x * z)) + v[14] * (C35 * (xx - yy));
+  }
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, const float* __restrict__ pos,
                                                             const float* __restrict__ sh,
                                                             const uint32_t* __restrict__ tiles,
-                                                            const uint32_t* __restrict__ offset,
+                                                            const uint32_t* __restrict__ roff,
                                                             const float* __restrict__ rows,
                                                             float* __restrict__ grads, int accumulate) {
-  extern __shared__ float s_sh[];  // [CHAIN_SH_ROWS * 3K] coefficients, then gradients in place
-  const int K = (deg + 1) * (deg + 1);
-  const int W = 3 * K;
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int W = 3 * K;
+  __shared__ __align__(16) float s_sh[CHAIN_SH_ROWS * W];  // coefficients, then their gradients in place
+  __shared__ uint64_t mbar;
   const int64_t i0 = (int64_t)blockIdx.x * CHAIN_SH_ROWS;
   const int rows_here = (int)min((int64_t)CHAIN_SH_ROWS, n - i0);
   const int64_t base = i0 * W;
   const int tot = rows_here * W;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) s_sh[e] = sh[base + e];
+  // TMA bulk load of the block's coefficient rows (base and size are 16-byte
+  // multiples whenever W*4*rows is; otherwise fall back to a strided copy)
+  const bool bulk = ((base * 4) & 15) == 0 && ((tot * 4) & 15) == 0;
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
   __syncthreads();
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&mbar, (uint32_t)(tot * 4));
+      bulk_g2s(s_sh, sh + base, (uint32_t)(tot * 4), &mbar);
+    }
+    mbar_wait(&mbar, 0);
+  } else {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) s_sh[e] = sh[base + e];
+    __syncthreads();
+  }
   const int64_t i = i0 + threadIdx.x;
   float* my = s_sh + threadIdx.x * W;
   if (threadIdx.x < rows_here) {
-    const uint32_t nt = tiles[i];
-    if (nt == 0) {
+    if (tiles[i] == 0) {
+#pragma unroll
       for (int e = 0; e < W; e++) my[e] = 0.f;
     } else {
-      const float* rw = rows + (int64_t)offset[i] * 9;
-      double dir[3], rs, basis[16], col[3];
-      bool lo[3], hi[3];
-      sh_color64(cam, deg, pos + i * 3, my, dir, &rs, basis, col, lo, hi);
+      const float* rw = rows + (int64_t)roff[i] * 9;
+      // sh.py:114-132 in float64 (same op order as the preprocess: identical clamp masks)
+      double off[3];
+      for (int j = 0; j < 3; j++) off[j] = (double)pos[i * 3 + j] - cam.center[j];
+      const double r = sqrt(off[0] * off[0] + off[1] * off[1] + off[2] * off[2]);
+      const double rs = r > 1e-12 ? r : 1e-12;
+      const double dir[3] = {off[0] / rs, off[1] / rs, off[2] / rs};
+      double basis[16];
+      sh_basis64(DEG, dir, basis);
       double dcol[3];
-      for (int c = 0; c < 3; c++) dcol[c] = (lo[c] || hi[c]) ? 0.0 : (double)rw[c];
-      // d_dir = sum_c sum_k dcol_c coeff_ck dY_k/ddir  (sh.py:147-148)
-      double gb[48];
-      sh_basis_grad64(deg, dir, gb);
-      double ddir[3] = {0.0, 0.0, 0.0};
-      for (int k = 0; k < K; k++) {
-        const double vk = dcol[0] * (double)my[k] + dcol[1] * (double)my[K + k] + dcol[2] * (double)my[2 * K + k];
-        ddir[0] += vk * gb[k * 3 + 0];
-        ddir[1] += vk * gb[k * 3 + 1];
-        ddir[2] += vk * gb[k * 3 + 2];
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; k++) acc += (double)my[c * K + k] * basis[k];
+        const double raw = acc + 0.5;
+        dcol[c] = (raw < 0.0 || raw > 1.0) ? 0.0 : (double)rw[c];
       }
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < K; k++)
+        v[k] = dcol[0] * (double)my[k] + dcol[1] * (double)my[K + k] + dcol[2] * (double)my[2 * K + k];
+      double ddir[3];
+      sh_dir_grad<DEG>(v, dir[0], dir[1], dir[2], ddir);
       const double radial = ddir[0] * dir[0] + ddir[1] * dir[1] + ddir[2] * dir[2];
       float* g_pos = grads + i * 3;
+#pragma unroll
       for (int d = 0; d < 3; d++) g_pos[d] += (float)((ddir[d] - radial * dir[d]) / rs);
+#pragma unroll
       for (int c = 0; c < 3; c++)
+#pragma unroll
         for (int k = 0; k < K; k++) my[c * K + k] = (float)(dcol[c] * basis[k]);
     }
   }
@@ -276,6 +363,8 @@ __global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, 
   float* g_sh = grads + 11 * n + base;
   if (accumulate) {
     for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] += s_sh[e];
+  } else if (bulk && ((reinterpret_cast<uintptr_t>(g_sh) & 15) == 0)) {
+    if (threadIdx.x == 0) bulk_s2g(g_sh, s_sh, (uint32_t)(tot * 4));
   } else {
     for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] = s_sh[e];
   }
@@ -341,12 +430,16 @@ extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, co
   // inst_rows is scratch from here on: the geometry pass parks each Gaussian's
   // merged colour gradient in its own first row for the SH pass
   float* rows = const_cast<float*>(inst_rows);
-  k_chain_geo<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(c, n, K, tx, ty, positions, rotations, log_scales,
-                                                           splats.tiles, splats.offset, rows, grads, accumulate,
-                                                           stats);
+  const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
+  k_chain_geo<<<blocks, CHAIN_ROWS, 0, st>>>(c, n, K, tx, ty, positions, rotations, log_scales, splats.tiles,
+                                             splats.row_offset, rows, grads, accumulate, stats);
   SSR_TRY(check_launch("k_chain_geo"));
-  const size_t smem = (size_t)CHAIN_SH_ROWS * 3 * K * sizeof(float);
-  k_chain_sh<<<(unsigned)((n + CHAIN_SH_ROWS - 1) / CHAIN_SH_ROWS), CHAIN_SH_ROWS, smem, st>>>(
-      c, n, sh_degree, positions, sh, splats.tiles, splats.offset, rows, grads, accumulate);
+  const unsigned sblocks = (unsigned)((n + CHAIN_SH_ROWS - 1) / CHAIN_SH_ROWS);
+  switch (sh_degree) {
+    case 0: k_chain_sh<0><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
+    case 1: k_chain_sh<1><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
+    case 2: k_chain_sh<2><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
+    default: k_chain_sh<3><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
+  }
   return check_launch("k_chain_sh");
 }

@@ -30,7 +30,7 @@ struct RasterArgs {
   const double2* conic_opa64;
   const double2* color64;
   const int4* rect;
-  const uint32_t* offset;
+  const uint32_t* row_offset;
   const uint32_t* inst;
   const int2* ranges;
   float* image;
@@ -47,7 +47,7 @@ struct RasterArgs {
 // Splat-major position of the instance of field row g in tile (tx, ty).
 __device__ __forceinline__ uint32_t inst_row(const RasterArgs& a, uint32_t g, int tx, int ty) {
   const int4 r = a.rect[g];
-  return a.offset[g] + (uint32_t)((ty - r.y) * (r.z - r.x) + (tx - r.x));
+  return a.row_offset[g] + (uint32_t)((ty - r.y) * (r.z - r.x) + (tx - r.x));
 }
 
 __device__ __forceinline__ size_t ckpt_base(int s0, int t) { return ((size_t)(s0 >> 5) + (size_t)t) * TILE_PX; }
@@ -747,7 +747,7 @@ static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* 
   a.conic_opa64 = (const double2*)sp.conic_opa64;
   a.color64 = (const double2*)sp.color64;
   a.rect = (const int4*)sp.rect;
-  a.offset = sp.offset;
+  a.row_offset = sp.row_offset;
   a.inst = inst;
   a.ranges = (const int2*)ranges;
   a.image = f.image;

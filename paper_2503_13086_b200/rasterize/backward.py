@@ -120,7 +120,8 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
     m = sp.n_instances
     st = _lib.stream_ptr()
     s = sp.struct()
-    rows = torch.empty(max(m, 1) * 9, dtype=torch.float32, device=dev)
+    # +4 floats of slack: the chain stages 16-byte aligned windows with TMA bulk copies
+    rows = torch.empty(max(m, 1) * 9 + 4, dtype=torch.float32, device=dev)
     if m:
         _lib.call("ssr_backward", LAYOUTS[layout], m, s, sp.inst_gauss.data_ptr(), sp.tile_ranges.data_ptr(),
                   out.frame_struct(), d_image.data_ptr(), _lib.ptr(d_soft), rows.data_ptr(), st)
