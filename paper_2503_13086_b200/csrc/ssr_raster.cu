@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           sdev = 0.f;
         }
         const int jend = min(j0 + BUCKET, n);
+#pragma unroll 4
         for (int j = j0; j < jend; j++) {
           const float4 M = sM[j];
           const float4 A = sA[j];
-          asm volatile("" : "+f"(fpx), "+f"(fpy));  // keep the pixel coordinates in registers
           const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
           const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
           float qpos;
@@ -113,15 +113,19 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
             scnt++;
             continue;
           }
-          if (A.w < 0.f && p2 > 1e-6f * qpos && qpos != 0.f) {  // fragile conic near power > 0
-            flag = true;
-            goto walk_done;
+          // Only near-singular conics (negative staged opacity, warp-uniform)
+          // can round to power > 0: flag the pixel near that decision.
+          if (A.w < 0.f) {
+            if (p2 > 1e-6f * qpos && qpos != 0.f) {
+              flag = true;
+              break;
+            }
+            if (p2 > 0.f) continue;
           }
-          if (p2 > 0.f) continue;
           float alpha = pair_alpha2(fabsf(A.w), p2);
           if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
             flag = true;
-            goto walk_done;
+            break;
           }
           alpha = fminf(alpha, ALPHA_CAP_F);
           const float y = __fmul_rn(alpha, 100.f);
@@ -135,12 +139,12 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
           if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
             flag = true;
-            goto walk_done;
+            break;
           }
           if (test < T_EPS_F) {
             term = true;
             nwk = k0 + j + 1;
-            goto walk_done;
+            break;
           }
           const float w = __fmul_rn(alpha, T);
           const float4 B = sB[j];
@@ -150,8 +154,8 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           hard++;
           T = test;
         }
+        if (flag || term) break;
       }
-    walk_done:
       if (flag || term) done = true;
     }
   }
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
 // l handles live pixel i-l and receives that pixel's running (T, H = w.C_front)
 // from lane l-1 by shuffle.  Lane 0 seeds each pixel from the forward's
 // bucket checkpoint.  No atomics; each instance row is written once.
-__global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
+__global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
   const int t = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -437,6 +441,11 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
     float T = 1.f, H = 0.f;
     const int n_steps = n_live + 31;
     const int last = n_live - 1;
+    // software pipeline: the (list -> pixel data) shared-memory chain of the
+    // next step is issued before this step's arithmetic
+    int jn = -lane;  // pixel list index of step 0
+    int pn = myList[max(min(jn, last), 0)];
+    float4 PBn = sPB[pn];
     for (int i = 0; i < n_steps; i++) {
       float Tin = __shfl_up_sync(FULL, T, 1);
       float Hin = __shfl_up_sync(FULL, H, 1);
@@ -447,10 +456,12 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
       }
       T = Tin;
       H = Hin;
-      const int j = i - lane;
+      const int j = jn, p = pn;
+      const float4 PB = PBn;
+      jn = j + 1;
+      pn = myList[max(min(jn, last), 0)];
+      PBn = sPB[pn];
       const bool inr = live && (unsigned)j < (unsigned)n_live;
-      const int p = myList[inr ? j : 0];
-      const float4 PB = sPB[p];
       const int nwt = __float_as_int(PB.w);
       const int nw = nwt >> 1;
       const float dx = pair_d(PB.x, sm.xi, sm.xf), dy = pair_d(PB.y, sm.yi, sm.yf);
@@ -461,7 +472,8 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
         const float araw = pair_alpha2(opa, p2);
         const bool capped = araw > ALPHA_CAP_F;
         const float alpha = capped ? ALPHA_CAP_F : araw;
-        const bool blended = alpha >= ALPHA_MIN_F && !((nwt & 1) && k == nw - 1);
+        // the terminating slot (k == nw - 1 of a terminated walk) is never blended
+        const bool blended = alpha >= ALPHA_MIN_F && k < nw - (nwt & 1);
         const float4 w = sPA[p];
         float dlda = 0.f;
         if (blended) {
@@ -470,10 +482,10 @@ __global__ void __launch_bounds__(256) k_backward_splat(RasterArgs a, const floa
           g0 = fmaf(aT, w.x, g0);
           g1 = fmaf(aT, w.y, g1);
           g2 = fmaf(aT, w.z, g2);
-          const float one_m = __fsub_rn(1.f, alpha);
+          const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
           const float awc = aT * wc;
           const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
-          dlda = T * wc - __fdividef(sdot, one_m);
+          dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
           H += awc;
           T = __fmul_rn(T, one_m);
         }
