@@ -174,6 +174,17 @@ int ssr_densify_apply(int64_t n, int64_t n_new, int32_t sh_degree, const float* 
                       double log_shrink, float* new_params, float* new_m, float* new_v,
                       void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------- spatial index */
+/* Exact k-NN distances (cKDTree.query replacement; field.py:111-161,279-289):
+ * for every query the k smallest Euclidean distances to the pool, ascending,
+ * +inf when the pool has fewer points.  float64, dense uniform grid:
+ * grid = HOST {bmin x, y, z, cell size} covering pool AND queries, dims = HOST
+ * {nx, ny, nz} (<= 2^26 cells); 1 <= k <= 8. */
+int ssr_knn_workspace(int64_t n_pool, int64_t n_cells, int64_t* bytes);
+int ssr_knn(const double* pool, int64_t n_pool, const double* queries, int64_t n_q, int32_t k,
+            const double* grid, const int32_t* dims, double* out_dist, void* workspace,
+            int64_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------- loss */
 /* losses.py:55-173: w_l1 * L1 + w_ssim * (1 - SSIM) + w_load * std(soft).
  * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,

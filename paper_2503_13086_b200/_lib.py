@@ -67,6 +67,9 @@ _SIGS = {
     "ssr_densify_workspace": [c_int64, ctypes.POINTER(c_int64)],
     "ssr_densify_apply": [c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
+    "ssr_knn_workspace": [c_int64, c_int64, ctypes.POINTER(c_int64)],
+    "ssr_knn": [c_void_p, c_int64, c_void_p, c_int64, c_int32, ctypes.POINTER(c_double),
+                ctypes.POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p],
     "ssr_loss_workspace": [c_int32, c_int32, ctypes.POINTER(c_int64)],
     "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                  c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, 
   const int tot = rows_here * W;
   // TMA bulk load of the block's coefficient rows (base and size are 16-byte
   // multiples whenever W*4*rows is; otherwise fall back to a strided copy)
-  const bool bulk = ((base * 4) & 15) == 0 && ((tot * 4) & 15) == 0;
+  const bool bulk = (reinterpret_cast<uintptr_t>(sh + base) & 15) == 0 && ((tot * 4) & 15) == 0;
   if (threadIdx.x == 0) mbar_init(&mbar, 1);
   __syncthreads();
   if (bulk) {

@@ -176,25 +176,19 @@ class GaussianField:
         """Append one Gaussian per sparse point (field.py:258-301).
 
         Scale init = mean distance to the 3 nearest points of the union of the
-        existing centres and the new points (exact, brute force on the GPU in
-        row blocks); identity rotation; logit(init_opacity); DC from colour.
+        existing centres and the new points (exact k-NN on the GPU grid index,
+        spatial.py); identity rotation; logit(init_opacity); DC from colour.
         """
+        from .spatial import mean_knn_scale
+
         usable = [p for p in points if p.finite]
         n_new = len(usable)
         if n_new == 0:
             return 0
         dev = self.device
         new_pos = torch.tensor(np.stack([p.position for p in usable]), dtype=torch.float64, device=dev)
-        pool = torch.cat([self.positions.double(), new_pos]) if self._n else new_pos
-        if pool.shape[0] > 1:
-            k = min(4, pool.shape[0])
-            dists = []
-            for s in range(0, n_new, 4096):
-                d = torch.cdist(new_pos[s:s + 4096], pool)
-                dists.append(torch.topk(d, k, dim=1, largest=False).values[:, 1:].mean(dim=1))
-            mean_d = torch.clamp(torch.cat(dists), min=1e-7)
-        else:
-            mean_d = torch.full((n_new,), 0.1, dtype=torch.float64, device=dev)
+        # exact 3-NN over (existing centres + new points) on the GPU grid index
+        mean_d = mean_knn_scale(self.positions.double() if self._n else None, new_pos)
         K = self.n_sh_coeffs
         log_scales = torch.log(mean_d)[:, None].repeat(1, 3)
         rot = torch.zeros(n_new, 4, dtype=torch.float64, device=dev)

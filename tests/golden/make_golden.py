@@ -127,6 +127,41 @@ def _edge_params(pos, log_scale, logit, rgb_dc, deg=0, rots=None):
                              np.full(n, logit, np.float32), sh)
 
 
+def expansion_case():
+    """field.py:111-161,258-301: SpatialIndex, filter_new_points, median_nn_spacing, insert_points."""
+    from splatstream.field import SparsePoint, SpatialIndex, filter_new_points, median_nn_spacing
+
+    rng = np.random.default_rng(41)
+    existing = scenes.make_params(2, seed=3, n=700)
+    field = _field(existing)
+    pts = rng.standard_normal((300, 3)) * 2.0
+    pts[:40] = np.asarray(existing.positions[:40], np.float64) + rng.normal(0, 1e-3, (40, 3))  # near duplicates
+    pts[40:45] = pts[45:50]  # exact duplicates among the candidates
+    cols = rng.uniform(0.0, 1.0, (300, 3))
+    cands = [SparsePoint(p, c) for p, c in zip(pts, cols)]
+    sparse = np.asarray(existing.positions, np.float64)
+    idx = SpatialIndex(sparse)
+    queries = rng.standard_normal((200, 3)) * 3.0
+    rec = dict(exp_existing_pos=np.asarray(existing.positions, np.float64), exp_cand_pos=pts, exp_cand_col=cols,
+               exp_queries=queries, exp_min_dist=idx.min_distance(queries),
+               exp_median_nn=median_nn_spacing(sparse))
+    thr = 0.05
+    kept = filter_new_points(idx, cands, thr)
+    rec["exp_threshold"] = thr
+    rec["exp_kept"] = np.array([any(k is c for k in kept) for c in cands])
+    g0 = field.generation
+    n_in = field.insert_points(kept, init_opacity=0.1)
+    rec["exp_n_inserted"] = n_in
+    rec["exp_generation_delta"] = field.generation - g0
+    for k in PARAM_KEYS:
+        rec[f"exp_after_{k}"] = getattr(field, k).copy()
+    for k in PARAM_KEYS:
+        rec[f"in_{k}"] = np.asarray(getattr(existing, k), np.float64)
+    path = os.path.join(HERE, "expansion.npz")
+    np.savez_compressed(path, **rec)
+    print(f"expansion: existing=700 candidates=300 kept={len(kept)} -> {os.path.getsize(path) / 1e6:.2f} MB")
+
+
 def main():
     # config-0 at full size (the reference's own CPU-runnable case)
     p = scenes.make_params(0, seed=0)
@@ -171,6 +206,7 @@ def main():
     rot, tr = look_at([0.2, -0.1, 0.0], [0.0, 0.0, 3.0])
     cam = CameraFrame(1, 64, 48, 60.0, 60.0, 32.0, 24.0, rot, tr)
     run_case("edge_needles_ties", p, cam, bg=(0.05, 0.05, 0.05))
+    expansion_case()
 
 
 if __name__ == "__main__":

@@ -142,3 +142,63 @@ def test_full_config_vs_oracle(cfg, oracle_lib):
     gr = backward(f, out, d_img, d_soft)
     r = grads_report(gr, ref_g)
     assert grads_ok(r), r
+
+
+# ---------------------------------------------------------------- field expansion
+def test_expansion_spatial_index_and_insert():
+    """GPU grid k-NN vs the reference's cKDTree results (golden: expansion.npz)."""
+    from paper_2503_13086_b200 import GaussianField, SparsePoint
+    from paper_2503_13086_b200.spatial import SpatialIndex, filter_new_points, median_nn_spacing
+
+    g = load_golden("expansion")
+    sparse = g["exp_existing_pos"]
+    idx = SpatialIndex(sparse)
+    np.testing.assert_allclose(idx.min_distance(g["exp_queries"]).cpu().numpy(), g["exp_min_dist"], rtol=1e-12)
+    assert median_nn_spacing(sparse) == pytest.approx(float(g["exp_median_nn"]), rel=1e-12)
+    cands = [SparsePoint(p, c) for p, c in zip(g["exp_cand_pos"], g["exp_cand_col"])]
+    kept = filter_new_points(idx, cands, float(g["exp_threshold"]))
+    np.testing.assert_array_equal([any(k is c for k in kept) for c in cands], g["exp_kept"])
+    f = _field(g)
+    g0 = f.generation
+    assert f.insert_points(kept, init_opacity=0.1) == int(g["exp_n_inserted"])
+    assert f.generation - g0 == int(g["exp_generation_delta"])
+    for k in GRAD_CLASSES:
+        np.testing.assert_allclose(getattr(f, k).cpu().numpy(), g[f"exp_after_{k}"], rtol=2e-6, atol=2e-7,
+                                   err_msg=k)
+
+
+def test_spatial_index_edge_cases():
+    from paper_2503_13086_b200.spatial import SpatialIndex, knn_distances
+
+    assert np.isinf(SpatialIndex(np.empty((0, 3))).min_distance([[1.0, 2.0, 3.0]]).cpu().numpy()).all()
+    pts = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    np.testing.assert_array_equal(SpatialIndex(pts).min_distance(pts).cpu().numpy(), 0.0)
+    rng = np.random.default_rng(21)
+    pool = np.concatenate([rng.standard_normal((3000, 3)) * 0.05, rng.uniform(-50, 50, (200, 3))])
+    q = np.concatenate([rng.standard_normal((100, 3)), rng.uniform(-80, 80, (50, 3))])
+    got = knn_distances(pool, q, 4).cpu().numpy()
+    brute = np.sort(np.sqrt(((q[:, None, :] - pool[None, :, :]) ** 2).sum(-1)), axis=1)[:, :4]
+    np.testing.assert_allclose(got, brute, rtol=1e-12)
+
+
+def test_iteration_after_densify_odd_row_count():
+    """Unaligned class offsets (N not a multiple of 4) after densify must not break any kernel."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.field import DensifyOptions
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.train import TrainState, densify, train_iteration
+
+    hp = scenes.make_params(1, seed=5, n=4001)
+    f = GaussianField.from_host(hp)
+    cam = scenes.camera(1, view=2, width=160, height=96)
+    st = TrainState(field=f, optimizer=FieldOptimizer(f, 2.0), weights=LossWeights(),
+                    densify=DensifyOptions(grad_threshold=1e-9), densify_interval=2)
+    target = torch.full((96, 160, 3), 0.3, device="cuda")
+    for _ in range(5):
+        br = train_iteration(st, cam, target, 1e-4)
+    torch.cuda.synchronize()
+    assert len(f) != 4001 and np.isfinite(br.total)
+    assert bool(torch.isfinite(f.flat).all())
