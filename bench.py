@@ -232,9 +232,8 @@ def main():
             grads = FieldGrads.zeros(n, field.sh_degree, dev)
             backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=True)
             allreduce_grads(grads.flat)
-            s = 11 + 3 * field.n_sh_coeffs
-            state.stats[:n] += grads.flat[s * n:(s + 1) * n]
-            state.stats[n:] += grads.flat[(s + 1) * n:]
+            state.stats[:n] += grads.screen_norms
+            state.stats[n:] += grads.visible_count
         else:
             grads = backward(state.field, out, br.d_image, br.d_soft, stats=state.stats)
         state.optimizer.step(state.field, grads, position_rate=rate)

@@ -151,6 +151,16 @@ int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* 
               const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
               const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream);
 
+/* backward.py:110-259 fused with optim.py:40-47,113-130: the chain of ssr_chain
+ * followed by the dense Adam step of ssr_adam, without materialising
+ * FieldGrads: rotations / log-scales / logits are stepped by the geometry
+ * kernel, SH rows (+ their m, v, staged with TMA bulk copies) and positions by
+ * the SH kernel; invisible rows get the zero-gradient update.  params, m, v
+ * are the flat buffers of ssr_adam; lr, bc1, bc2 HOST arrays as there. */
+int ssr_chain_adam(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* params, float* m, float* v,
+                   ssr_splats splats, float* inst_rows, float* stats, const double* lr,
+                   double lr_sh_rest, const double* bc1, const double* bc2, void* stream);
+
 /* ---------------------------------------------------------- stage 5 */
 /* optim.py:29-47,113-130: dense bias-corrected Adam over the flat parameter
  * buffer [pos | rot | logscale | logit | sh] (n rows, K sh coeffs).

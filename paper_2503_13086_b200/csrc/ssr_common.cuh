@@ -32,6 +32,11 @@ constexpr float ALPHA_MIN_F = 1.0f / 255.0f;
 constexpr float ALPHA_CAP_F = 0.99f;
 constexpr float T_EPS_F = 1e-4f;
 
+// Flat parameter / moment / gradient buffers are class-major with every class
+// region padded to a row stride that is a multiple of 4, so each region starts
+// 16-byte aligned for any N (float4 and TMA bulk paths stay valid after densify).
+__host__ __device__ __forceinline__ int64_t row_stride(int64_t n) { return (n + 3) & ~(int64_t)3; }
+
 void set_error(const std::string& msg);
 int check_cuda(cudaError_t e, const char* what);
 int check_launch(const char* what);

@@ -90,11 +90,12 @@ __global__ void k_densify_masks(int64_t n, int K, const float* __restrict__ para
                                 int32_t* __restrict__ counts) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float* ls = params + 7 * n + i * 3;
+  const int64_t ns = row_stride(n);
+  const float* ls = params + 7 * ns + i * 3;
   double ms = exp((double)ls[0]);
   ms = fmax(ms, exp((double)ls[1]));
   ms = fmax(ms, exp((double)ls[2]));
-  const double logit = (double)params[10 * n + i];
+  const double logit = (double)params[10 * ns + i];
   const bool hot = (double)stats[i] > grad_thr;
   const bool prune = (1.0 / (1.0 + exp(-logit))) < prune_opa;
   const bool big = ms > big_thr;
@@ -125,8 +126,9 @@ __global__ void k_densify_apply(int64_t n, int64_t n_new, int K, const float* __
   const uint32_t n_keep = keep_off[n - 1] + (fl & 1);
   const uint32_t n_clone = clone_off[n - 1] + ((fl >> 1) & 1);
   const int width[5] = {3, 4, 3, 1, 3 * K};
-  const int64_t so[5] = {0, 3 * n, 7 * n, 10 * n, 11 * n};
-  const int64_t dof[5] = {0, 3 * n_new, 7 * n_new, 10 * n_new, 11 * n_new};
+  const int64_t ns = row_stride(n), nns = row_stride(n_new);
+  const int64_t so[5] = {0, 3 * ns, 7 * ns, 10 * ns, 11 * ns};
+  const int64_t dof[5] = {0, 3 * nns, 7 * nns, 10 * nns, 11 * nns};
   if (f & 1) {
     const int64_t d = keep_off[i];
     for (int c = 0; c < 5; c++)
@@ -195,6 +197,7 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
   const int64_t widths[5] = {3, 4, 3, 1, 3 * (int64_t)K};
   AdamPlan plan;
   int64_t start = 0, blocks = 0;
+  const int64_t ns = row_stride(n);
   for (int c = 0; c < 5; c++) {
     AdamRegion& R = plan.r[c];
     R.start = start;
@@ -205,7 +208,7 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
     R.inv_bc1 = (float)(1.0 / bc1[c]);
     R.inv_bc2 = (float)(1.0 / bc2[c]);
     R.is_sh = c == 4;
-    start += R.count;
+    start += widths[c] * ns;
     blocks += (R.count + ADAM_PER_BLOCK - 1) / ADAM_PER_BLOCK;
   }
   cudaStream_t st = (cudaStream_t)stream;

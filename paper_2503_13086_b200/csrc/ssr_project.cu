@@ -81,23 +81,78 @@ __global__ void k_project_aux(Cam cam, int64_t n, int deg, int tiles_x, int tile
 // k_chain_sh in the first three floats of the Gaussian's own first row.
 constexpr int CHAIN_ROWS = 128;
 constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
+constexpr uint32_t MERGE_BIG = 32;  // rows above which a Gaussian is merged warp-cooperatively
+
+// Rows of Gaussians touching more than MERGE_BIG tiles (large splats, up to
+// thousands of tiles) are summed by a whole warp -- coalesced strided loads,
+// fixed-order tree reduction -- and written back into the Gaussian's first
+// row, so the chain's per-thread merge stays bounded.  One warp per 32 rows.
+__global__ void __launch_bounds__(256) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
+                                                   const uint32_t* __restrict__ roff, float* __restrict__ rows) {
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
+  const int lane = threadIdx.x & 31;
+  if (g0 >= n) return;
+  const int64_t gi = g0 + lane;
+  const uint32_t mine = gi < n ? tiles[gi] : 0u;
+  unsigned big = __ballot_sync(0xffffffffu, mine > MERGE_BIG);
+  while (big) {
+    const int l = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t nt = __shfl_sync(0xffffffffu, mine, l);
+    float* rw = rows + (int64_t)roff[g0 + l] * 9;
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t j = lane; j < nt; j += 32)
+#pragma unroll
+      for (int c = 0; c < 9; c++) acc[c] += (double)rw[(int64_t)j * 9 + c];
+#pragma unroll
+    for (int c = 0; c < 9; c++)
+      for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    __syncwarp();
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < 9; c++) rw[c] = (float)acc[c];
+    __syncwarp();
+  }
+}
+// Adam of optim.py:40-47 for one element (FieldOptimizer's fp32 restatement).
+struct AdamClass {
+  float lr, ib1, ib2;
+};
+struct AdamArgs {
+  AdamClass c[6];  // pos, rot, scale, opacity, sh dc, sh rest
+  float* m;
+  float* v;
+};
+__device__ __forceinline__ float adam_apply(float p, float g, float& m, float& v, const AdamClass& c) {
+  m = __fmaf_rn(0.9f, m, 0.1f * g);
+  v = __fmaf_rn(0.999f, v, 0.001f * g * g);
+  return p - __fdividef(c.lr * (m * c.ib1), sqrtf(v * c.ib2) + 1e-15f);
+}
+
+// FUSED = false: write FieldGrads (ssr_chain).  FUSED = true (ssr_chain_adam):
+// apply Adam to rotations / log-scales / logits in place and park the
+// geometric position gradient in floats 3..5 of the row scratch.
+template <bool FUSED>
 __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(Cam cam, int64_t n, int K, int tiles_x, int tiles_y,
-                                                          const float* __restrict__ pos, const float* __restrict__ rot,
-                                                          const float* __restrict__ ls,
+                                                          const float* __restrict__ pos, float* __restrict__ rot,
+                                                          float* __restrict__ ls, float* __restrict__ logit_p,
                                                           const uint32_t* __restrict__ tiles,
                                                           const uint32_t* __restrict__ roff, float* __restrict__ rows,
                                                           float* __restrict__ grads, int accumulate,
-                                                          float* __restrict__ stats) {
+                                                          float* __restrict__ stats, AdamArgs adam) {
   __shared__ __align__(16) float s_rows[CHAIN_STAGE_FLOATS + 4];
   __shared__ uint64_t mbar;
   const int64_t i0 = (int64_t)blockIdx.x * CHAIN_ROWS;
   const int rows_here = (int)min((int64_t)CHAIN_ROWS, n - i0);
+  const int64_t i = i0 + threadIdx.x;
+  const bool mine = threadIdx.x < rows_here;
   const uint32_t r_begin = roff[i0];
   const uint32_t r_end = roff[i0 + rows_here - 1] + tiles[i0 + rows_here - 1];
+  // the block's rows are one contiguous range: one 16-byte aligned TMA bulk
+  // copy when it fits (inst_rows has >= 16 B slack), else direct reads
   const int64_t n_floats = (int64_t)(r_end - r_begin) * 9;
-  // 16-byte aligned window [a0, a1) covering the block's rows (inst_rows has >= 16 B slack)
   const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
-  const int pad = (int)((b0 - a0) >> 2);  // floats before the first row
+  const int pad = (int)((b0 - a0) >> 2);
   const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
   const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
   if (threadIdx.x == 0) mbar_init(&mbar, 1);
@@ -109,16 +164,38 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(Cam cam, int64_t n, in
     }
     mbar_wait(&mbar, 0);
   }
-  const int64_t i = i0 + threadIdx.x;
-  if (threadIdx.x >= rows_here) return;
+  const uint32_t nt = mine ? tiles[i] : 0u;
+  // bincount merge (backward.py:110-118): ascending tile order; Gaussians with
+  // more than MERGE_BIG rows were reduced into their first row by k_merge_big
+  double pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (mine && nt > 0) {
+    const float* rw = staged ? s_rows + pad + (int64_t)(roff[i] - r_begin) * 9 : rows + (int64_t)roff[i] * 9;
+    const uint32_t nr = nt > MERGE_BIG ? 1u : nt;
+    for (uint32_t j = 0; j < nr; j++)
+#pragma unroll
+      for (int c = 0; c < 9; c++) pr[c] += (double)rw[j * 9 + c];
+  }
+  if (!mine) return;
   const int S = 11 + 3 * K;
+  const int64_t ns = row_stride(n);
   float* g_pos = grads;
-  float* g_rot = grads + 3 * n;
-  float* g_ls = grads + 7 * n;
-  float* g_logit = grads + 10 * n;
-  float* g_screen = grads + (int64_t)S * n;
-  float* g_vis = grads + (int64_t)(S + 1) * n;
-  const uint32_t nt = tiles[i];
+  float* g_rot = grads + 3 * ns;
+  float* g_ls = grads + 7 * ns;
+  float* g_logit = grads + 10 * ns;
+  float* g_screen = grads + (int64_t)S * ns;
+  float* g_vis = grads + (int64_t)(S + 1) * ns;
+  if (FUSED && nt == 0) {  // invisible: the reference still steps every row with a zero gradient
+    for (int j = 0; j < 4; j++) {
+      const int64_t e = 3 * ns + i * 4 + j;
+      rot[i * 4 + j] = adam_apply(rot[i * 4 + j], 0.f, adam.m[e], adam.v[e], adam.c[1]);
+    }
+    for (int j = 0; j < 3; j++) {
+      const int64_t e = 7 * ns + i * 3 + j;
+      ls[i * 3 + j] = adam_apply(ls[i * 3 + j], 0.f, adam.m[e], adam.v[e], adam.c[2]);
+    }
+    logit_p[i] = adam_apply(logit_p[i], 0.f, adam.m[10 * ns + i], adam.v[10 * ns + i], adam.c[3]);
+    return;
+  }
   if (nt == 0) {
     if (!accumulate) {
       for (int j = 0; j < 3; j++) g_pos[i * 3 + j] = 0.f;
@@ -130,11 +207,6 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(Cam cam, int64_t n, in
     }
     return;
   }
-  // bincount merge (backward.py:110-118): ascending tile order
-  double pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const float* rw = staged ? s_rows + pad + (int64_t)(roff[i] - r_begin) * 9 : rows + (int64_t)roff[i] * 9;
-  for (uint32_t j = 0; j < nt; j++)
-    for (int c = 0; c < 9; c++) pr[c] += (double)rw[j * 9 + c];
   float* dst = rows + (int64_t)roff[i] * 9;
   dst[0] = (float)pr[0];
   dst[1] = (float)pr[1];
@@ -227,7 +299,21 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(Cam cam, int64_t n, in
   const double rad = dqn[0] * P.qn[0] + dqn[1] * P.qn[1] + dqn[2] * P.qn[2] + dqn[3] * P.qn[3];
   const double screen =
       sqrt(pr[4] * pr[4] + pr[5] * pr[5]) * (0.5 * (double)(cam.width > cam.height ? cam.width : cam.height));
-  if (accumulate) {
+  if (FUSED) {
+    for (int j = 0; j < 4; j++) {
+      const int64_t e = 3 * ns + i * 4 + j;
+      rot[i * 4 + j] = adam_apply(rot[i * 4 + j], (float)((dqn[j] - rad * P.qn[j]) / P.qnorm), adam.m[e], adam.v[e],
+                                  adam.c[1]);
+    }
+    for (int j = 0; j < 3; j++) {
+      const int64_t e = 7 * ns + i * 3 + j;
+      ls[i * 3 + j] = adam_apply(ls[i * 3 + j], (float)dls[j], adam.m[e], adam.v[e], adam.c[2]);
+    }
+    logit_p[i] = adam_apply(logit_p[i], (float)pr[3], adam.m[10 * ns + i], adam.v[10 * ns + i], adam.c[3]);
+    dst[3] = (float)dpos[0];
+    dst[4] = (float)dpos[1];
+    dst[5] = (float)dpos[2];
+  } else if (accumulate) {
     for (int j = 0; j < 3; j++) g_pos[i * 3 + j] += (float)dpos[j];
     for (int j = 0; j < 4; j++) g_rot[i * 4 + j] += (float)((dqn[j] - rad * P.qn[j]) / P.qnorm);
     for (int j = 0; j < 3; j++) g_ls[i * 3 + j] += (float)dls[j];
@@ -288,53 +374,64 @@ __device__ __forceinline__ void sh_dir_grad(const double* v, double x, double y,
   }
 }
 
-template <int DEG>
-__global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, const float* __restrict__ pos,
-                                                            const float* __restrict__ sh,
+// rows per block: 128, or 64 when the Adam moments are staged too (static smem <= 48 KB)
+template <bool FUSED>
+struct ShRows {
+  static constexpr int value = FUSED ? 64 : CHAIN_SH_ROWS;
+};
+
+template <int DEG, bool FUSED>
+__global__ void __launch_bounds__(ShRows<FUSED>::value) k_chain_sh(Cam cam, int64_t n, float* __restrict__ pos,
+                                                            float* __restrict__ sh,
                                                             const uint32_t* __restrict__ tiles,
                                                             const uint32_t* __restrict__ roff,
                                                             const float* __restrict__ rows,
-                                                            float* __restrict__ grads, int accumulate) {
+                                                            float* __restrict__ grads, int accumulate, AdamArgs adam) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
-  __shared__ __align__(16) float s_sh[CHAIN_SH_ROWS * W];  // coefficients, then their gradients in place
+  constexpr int ROWS = ShRows<FUSED>::value;
+  constexpr int NBUF = FUSED ? 3 : 1;  // coefficients (+ Adam m, v rows when fused)
+  __shared__ __align__(16) float s_buf[NBUF][ROWS * W];
   __shared__ uint64_t mbar;
-  const int64_t i0 = (int64_t)blockIdx.x * CHAIN_SH_ROWS;
-  const int rows_here = (int)min((int64_t)CHAIN_SH_ROWS, n - i0);
+  float* s_sh = s_buf[0];
+  const int64_t i0 = (int64_t)blockIdx.x * ROWS;
+  const int rows_here = (int)min((int64_t)ROWS, n - i0);
   const int64_t base = i0 * W;
   const int tot = rows_here * W;
-  // TMA bulk load of the block's coefficient rows (base and size are 16-byte
-  // multiples whenever W*4*rows is; otherwise fall back to a strided copy)
-  const bool bulk = (reinterpret_cast<uintptr_t>(sh + base) & 15) == 0 && ((tot * 4) & 15) == 0;
+  const int64_t ns = row_stride(n);
+  float* gsrc[3] = {sh + base, FUSED ? adam.m + 11 * ns + base : nullptr, FUSED ? adam.v + 11 * ns + base : nullptr};
+  // TMA bulk loads of the block's coefficient rows (and their moments)
+  bool bulk = ((tot * 4) & 15) == 0;
+  for (int b = 0; b < NBUF; b++) bulk = bulk && (reinterpret_cast<uintptr_t>(gsrc[b]) & 15) == 0;
   if (threadIdx.x == 0) mbar_init(&mbar, 1);
   __syncthreads();
   if (bulk) {
     if (threadIdx.x == 0) {
-      mbar_expect_tx(&mbar, (uint32_t)(tot * 4));
-      bulk_g2s(s_sh, sh + base, (uint32_t)(tot * 4), &mbar);
+      mbar_expect_tx(&mbar, (uint32_t)(tot * 4 * NBUF));
+      for (int b = 0; b < NBUF; b++) bulk_g2s(s_buf[b], gsrc[b], (uint32_t)(tot * 4), &mbar);
     }
     mbar_wait(&mbar, 0);
   } else {
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) s_sh[e] = sh[base + e];
+    for (int b = 0; b < NBUF; b++)
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) s_buf[b][e] = gsrc[b][e];
     __syncthreads();
   }
   const int64_t i = i0 + threadIdx.x;
   float* my = s_sh + threadIdx.x * W;
   if (threadIdx.x < rows_here) {
-    if (tiles[i] == 0) {
-#pragma unroll
-      for (int e = 0; e < W; e++) my[e] = 0.f;
-    } else {
-      const float* rw = rows + (int64_t)roff[i] * 9;
+    double dpos_sh[3] = {0.0, 0.0, 0.0};
+    double dcol[3] = {0.0, 0.0, 0.0};
+    double basis[16];
+    const bool vis = tiles[i] != 0;
+    const float* rw = rows + (vis ? (int64_t)roff[i] * 9 : 0);
+    if (vis) {
       // sh.py:114-132 in float64 (same op order as the preprocess: identical clamp masks)
       double off[3];
       for (int j = 0; j < 3; j++) off[j] = (double)pos[i * 3 + j] - cam.center[j];
       const double r = sqrt(off[0] * off[0] + off[1] * off[1] + off[2] * off[2]);
       const double rs = r > 1e-12 ? r : 1e-12;
       const double dir[3] = {off[0] / rs, off[1] / rs, off[2] / rs};
-      double basis[16];
       sh_basis64(DEG, dir, basis);
-      double dcol[3];
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         double acc = 0.0;
@@ -350,9 +447,35 @@ __global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, 
       double ddir[3];
       sh_dir_grad<DEG>(v, dir[0], dir[1], dir[2], ddir);
       const double radial = ddir[0] * dir[0] + ddir[1] * dir[1] + ddir[2] * dir[2];
+#pragma unroll
+      for (int d = 0; d < 3; d++) dpos_sh[d] = (ddir[d] - radial * dir[d]) / rs;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; k++) basis[k] = 0.0;
+    }
+    if (FUSED) {
+      // positions: geometric part from the geometry kernel + view-direction part
+      for (int d = 0; d < 3; d++) {
+        const float g = vis ? (float)((double)rw[3 + d] + dpos_sh[d]) : 0.f;
+        const int64_t e = i * 3 + d;
+        pos[e] = adam_apply(pos[e], g, adam.m[e], adam.v[e], adam.c[0]);
+      }
+      float* mm = s_buf[FUSED ? 1 : 0] + threadIdx.x * W;
+      float* vv = s_buf[FUSED ? 2 : 0] + threadIdx.x * W;
+#pragma unroll
+      for (int c = 0; c < 3; c++)
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+          const int e = c * K + k;
+          my[e] = adam_apply(my[e], (float)(dcol[c] * basis[k]), mm[e], vv[e], adam.c[k == 0 ? 4 : 5]);
+        }
+    } else if (!vis) {
+#pragma unroll
+      for (int e = 0; e < W; e++) my[e] = 0.f;
+    } else {
       float* g_pos = grads + i * 3;
 #pragma unroll
-      for (int d = 0; d < 3; d++) g_pos[d] += (float)((ddir[d] - radial * dir[d]) / rs);
+      for (int d = 0; d < 3; d++) g_pos[d] += (float)dpos_sh[d];
 #pragma unroll
       for (int c = 0; c < 3; c++)
 #pragma unroll
@@ -360,13 +483,20 @@ __global__ void __launch_bounds__(CHAIN_SH_ROWS) k_chain_sh(Cam cam, int64_t n, 
     }
   }
   __syncthreads();
-  float* g_sh = grads + 11 * n + base;
-  if (accumulate) {
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] += s_sh[e];
-  } else if (bulk && ((reinterpret_cast<uintptr_t>(g_sh) & 15) == 0)) {
-    if (threadIdx.x == 0) bulk_s2g(g_sh, s_sh, (uint32_t)(tot * 4));
+  float* gdst[3] = {FUSED ? sh + base : grads + 11 * ns + base, FUSED ? adam.m + 11 * ns + base : nullptr,
+                    FUSED ? adam.v + 11 * ns + base : nullptr};
+  if (!FUSED && accumulate) {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) gdst[0][e] += s_sh[e];
+    return;
+  }
+  bool bulk_out = bulk;
+  for (int b = 0; b < NBUF; b++) bulk_out = bulk_out && (reinterpret_cast<uintptr_t>(gdst[b]) & 15) == 0;
+  if (bulk_out) {
+    if (threadIdx.x == 0)
+      for (int b = 0; b < NBUF; b++) bulk_s2g(gdst[b], s_buf[b], (uint32_t)(tot * 4));
   } else {
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) g_sh[e] = s_sh[e];
+    for (int b = 0; b < NBUF; b++)
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) gdst[b][e] = s_buf[b][e];
   }
 }
 
@@ -414,6 +544,36 @@ extern "C" int ssr_project_aux(const ssr_camera* cam, int64_t n, int32_t sh_degr
   return check_launch("k_project_aux");
 }
 
+template <bool FUSED>
+static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* positions, float* rotations,
+                        float* log_scales, float* logits, float* sh, ssr_splats splats, float* rows, float* grads,
+                        int32_t accumulate, float* stats, const AdamArgs& adam, cudaStream_t st) {
+  int tx, ty;
+  tile_dims(cam, &tx, &ty);
+  const Cam c = to_cam(*cam);
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  k_merge_big<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
+  SSR_TRY(check_launch("k_merge_big"));
+  const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
+  k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, 0, st>>>(c, n, K, tx, ty, positions, rotations, log_scales, logits,
+                                                    splats.tiles, splats.row_offset, rows, grads, accumulate, stats,
+                                                    adam);
+  SSR_TRY(check_launch("k_chain_geo"));
+  constexpr int SR = ShRows<FUSED>::value;
+  const unsigned sblocks = (unsigned)((n + SR - 1) / SR);
+#define SSR_SH(D)                                                                                                \
+  k_chain_sh<D, FUSED><<<sblocks, SR, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, \
+                                                          rows, grads, accumulate, adam)
+  switch (sh_degree) {
+    case 0: SSR_SH(0); break;
+    case 1: SSR_SH(1); break;
+    case 2: SSR_SH(2); break;
+    default: SSR_SH(3); break;
+  }
+#undef SSR_SH
+  return check_launch("k_chain_sh");
+}
+
 extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
                          const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
                          const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream) {
@@ -422,24 +582,33 @@ extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, co
     return SSR_ERR_INVALID;
   }
   if (n == 0) return SSR_OK;
-  int tx, ty;
-  tile_dims(cam, &tx, &ty);
-  cudaStream_t st = (cudaStream_t)stream;
-  const Cam c = to_cam(*cam);
-  const int K = (sh_degree + 1) * (sh_degree + 1);
+  AdamArgs none{};
   // inst_rows is scratch from here on: the geometry pass parks each Gaussian's
   // merged colour gradient in its own first row for the SH pass
-  float* rows = const_cast<float*>(inst_rows);
-  const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
-  k_chain_geo<<<blocks, CHAIN_ROWS, 0, st>>>(c, n, K, tx, ty, positions, rotations, log_scales, splats.tiles,
-                                             splats.row_offset, rows, grads, accumulate, stats);
-  SSR_TRY(check_launch("k_chain_geo"));
-  const unsigned sblocks = (unsigned)((n + CHAIN_SH_ROWS - 1) / CHAIN_SH_ROWS);
-  switch (sh_degree) {
-    case 0: k_chain_sh<0><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
-    case 1: k_chain_sh<1><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
-    case 2: k_chain_sh<2><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
-    default: k_chain_sh<3><<<sblocks, CHAIN_SH_ROWS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, rows, grads, accumulate); break;
+  return launch_chain<false>(cam, n, sh_degree, const_cast<float*>(positions), const_cast<float*>(rotations),
+                             const_cast<float*>(log_scales), nullptr, const_cast<float*>(sh), splats,
+                             const_cast<float*>(inst_rows), grads, accumulate, stats, none, (cudaStream_t)stream);
+}
+
+extern "C" int ssr_chain_adam(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* params, float* m, float* v,
+                              ssr_splats splats, float* inst_rows, float* stats, const double* lr, double lr_sh_rest,
+                              const double* bc1, const double* bc2, void* stream) {
+  if (!cam || n < 0 || sh_degree < 0 || sh_degree > 3 || !params || !m || !v || !lr || !bc1 || !bc2) {
+    set_error("ssr_chain_adam: invalid argument");
+    return SSR_ERR_INVALID;
   }
-  return check_launch("k_chain_sh");
+  if (n == 0) return SSR_OK;
+  AdamArgs adam;
+  for (int c = 0; c < 5; c++) {
+    adam.c[c].lr = (float)lr[c];
+    adam.c[c].ib1 = (float)(1.0 / bc1[c]);
+    adam.c[c].ib2 = (float)(1.0 / bc2[c]);
+  }
+  adam.c[5] = adam.c[4];
+  adam.c[5].lr = (float)lr_sh_rest;
+  adam.m = m;
+  adam.v = v;
+  const int64_t ns = row_stride(n);
+  return launch_chain<true>(cam, n, sh_degree, params, params + 3 * ns, params + 7 * ns, params + 10 * ns,
+                            params + 11 * ns, splats, inst_rows, nullptr, 0, stats, adam, (cudaStream_t)stream);
 }

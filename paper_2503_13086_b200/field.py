@@ -30,14 +30,34 @@ def row_floats(sh_degree: int) -> int:
     return 11 + 3 * (sh_degree + 1) ** 2
 
 
+def row_stride(n: int) -> int:
+    """Rows reserved per class region: n rounded up to a multiple of 4, so every
+    class starts 16-byte aligned (float4 / TMA paths) for any n (ssr_common.cuh)."""
+    return (int(n) + 3) & ~3
+
+
 def class_slices(n: int, k: int):
     """(start, width) of each class inside the flat buffer of n rows."""
     w = (3, 4, 3, 1, 3 * k)
+    ns = row_stride(n)
     out, off = [], 0
     for wi in w:
         out.append((off, wi))
-        off += wi * n
+        off += wi * ns
     return out
+
+
+def flat_size(n: int, k: int, extra: int = 0) -> int:
+    """Floats of a flat buffer of n rows: the 5 classes (+ ``extra`` 1-wide regions)."""
+    return (11 + 3 * k + extra) * row_stride(n)
+
+
+def pack_classes(parts, n: int, k: int, device, dtype=torch.float32) -> torch.Tensor:
+    """Flat, padded class-major buffer from the five class arrays (each n rows)."""
+    flat = torch.zeros(flat_size(n, k), dtype=dtype, device=device)
+    for (off, w), part in zip(class_slices(n, k), parts):
+        flat[off: off + w * n] = part.reshape(-1).to(device=device, dtype=dtype)
+    return flat
 
 
 @dataclass
@@ -98,10 +118,10 @@ class GaussianField:
         arrs = [torch.as_tensor(a if torch.is_tensor(a) else np.asarray(a)) for a in
                 (positions, rotations, log_scales, opacity_logits, sh)]
         n = arrs[0].shape[0]
-        f._flat = torch.cat([a.reshape(-1).to(device=f.device, dtype=torch.float32) for a in arrs]).contiguous()
-        f._n = n
-        if f._flat.numel() != n * row_floats(deg):
+        if sum(a.numel() for a in arrs) != n * row_floats(deg):
             raise InvalidParameter("parameter arrays have inconsistent shapes")
+        f._flat = pack_classes(arrs, n, k, f.device)
+        f._n = n
         return f
 
     @classmethod
@@ -210,8 +230,8 @@ class GaussianField:
             p = p.to(dtype=torch.float32).reshape(n_add, -1)
             if old is not None:
                 p = torch.cat([old[i].reshape(self._n, -1), p])
-            cat.append(p.reshape(-1))
-        self._flat = torch.cat(cat).contiguous()
+            cat.append(p)
+        self._flat = pack_classes(cat, self._n + n_add, self.n_sh_coeffs, self.device)
         self._n += n_add
 
     def densify_and_prune(self, grad_stats, opts: DensifyOptions, rng, optimizer=None) -> DensifySummary:
@@ -245,12 +265,12 @@ class GaussianField:
         eps = torch.as_tensor(rng.standard_normal((2 * sp, 3)) if sp else np.zeros((1, 3)),
                               dtype=torch.float64).to(self.device)
         n_new = int(keep_np.sum()) + n_added
-        new = torch.empty(n_new * row_floats(self.sh_degree), dtype=torch.float32, device=self.device)
+        new = torch.zeros(flat_size(n_new, self.n_sh_coeffs), dtype=torch.float32, device=self.device)
         ws = torch.empty(_lib.query("ssr_densify_workspace", n), dtype=torch.uint8, device=self.device)
         m_old = v_old = new_m = new_v = None
         if optimizer is not None:
             m_old, v_old = optimizer.m, optimizer.v
-            new_m, new_v = torch.empty_like(new), torch.empty_like(new)
+            new_m, new_v = torch.zeros_like(new), torch.zeros_like(new)
         _lib.call("ssr_densify_apply", n, n_new, self.sh_degree, self._flat.data_ptr(), _lib.ptr(m_old),
                   _lib.ptr(v_old), flags.data_ptr(), eps.data_ptr(), float(math.log(opts.split_scale_shrink)),
                   new.data_ptr(), _lib.ptr(new_m), _lib.ptr(new_v), ws.data_ptr(), ws.numel(), st)

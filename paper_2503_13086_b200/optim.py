@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from .errors import InvalidParameter, StaleFieldError
-from .field import CLASSES, class_slices
+from .field import CLASSES, class_slices, pack_classes
 
 BETA1 = 0.9
 BETA2 = 0.999
@@ -65,9 +65,9 @@ class FieldOptimizer:
             for src, dst in ((self.m, newm), (self.v, newv)):
                 mv = self._moment_view(src, name)
                 kept = mv[keep]
-                dst.append(torch.cat([kept, torch.zeros((int(n_added),) + tuple(mv.shape[1:]), device=mv.device)])
-                           .reshape(-1))
-        self.m, self.v = torch.cat(newm), torch.cat(newv)
+                dst.append(torch.cat([kept, torch.zeros((int(n_added),) + tuple(mv.shape[1:]), device=mv.device)]))
+        k = (self.sh_degree + 1) ** 2
+        self.m, self.v = pack_classes(newm, n_new, k, self.m.device), pack_classes(newv, n_new, k, self.m.device)
         self.n_rows = n_new
         self._generation = fld.generation
         if self.n_rows != len(fld):
@@ -83,11 +83,19 @@ class FieldOptimizer:
         if n == 0:
             return
         g = grads.flat_params(fld.flat.device)
-        for k in CLASSES:
-            self.steps[k] += 1
-        order = ("positions", "rotations", "log_scales", "opacity_logits", "sh")
-        lr = (ctypes.c_double * 5)(position_rate * self.scene_extent, ROTATION_LR, SCALE_LR, OPACITY_LR, SH_DC_LR)
-        bc1 = (ctypes.c_double * 5)(*[1.0 - BETA1 ** self.steps[k] for k in order])
-        bc2 = (ctypes.c_double * 5)(*[1.0 - BETA2 ** self.steps[k] for k in order])
+        lr, bc1, bc2 = self.advance(position_rate)
         _lib.call("ssr_adam", n, fld.sh_degree, fld.flat.data_ptr(), g.data_ptr(), self.m.data_ptr(),
                   self.v.data_ptr(), lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
+
+    def check(self, fld):
+        if fld.generation != self._generation:
+            raise StaleFieldError("field changed shape since the optimizer last synced")
+
+    def advance(self, position_rate):
+        """Count one step for every class; (lr, bc1, bc2) host arrays for the kernels."""
+        for k in CLASSES:
+            self.steps[k] += 1
+        lr = (ctypes.c_double * 5)(position_rate * self.scene_extent, ROTATION_LR, SCALE_LR, OPACITY_LR, SH_DC_LR)
+        bc1 = (ctypes.c_double * 5)(*[1.0 - BETA1 ** self.steps[k] for k in CLASSES])
+        bc2 = (ctypes.c_double * 5)(*[1.0 - BETA2 ** self.steps[k] for k in CLASSES])
+        return lr, bc1, bc2

@@ -7,7 +7,7 @@ import torch
 
 from .. import _lib
 from ..errors import InvalidParameter, StaleFieldError
-from ..field import class_slices, row_floats
+from ..field import class_slices, flat_size, pack_classes, row_stride
 from .forward import RenderOutput
 
 LAYOUTS = {"splat": 0, "pixel": 1}
@@ -36,7 +36,7 @@ class FieldGrads:
     @classmethod
     def zeros(cls, n: int, sh_degree: int, device) -> "FieldGrads":
         k = (sh_degree + 1) ** 2
-        flat = torch.zeros(n * (row_floats(sh_degree) + 2), dtype=torch.float32, device=device)
+        flat = torch.zeros(flat_size(n, k, extra=2), dtype=torch.float32, device=device)
         return cls(_flat=flat, _n=n, _k=k)
 
     def _view(self, i):
@@ -44,8 +44,8 @@ class FieldGrads:
         if i < 5:
             off, w = class_slices(n, k)[i]
             return self._flat[off: off + w * n].view(((n, 3), (n, 4), (n, 3), (n,), (n, 3, k))[i])
-        s = 11 + 3 * k
-        return self._flat[(s + i - 5) * n: (s + i - 4) * n]
+        s, ns = 11 + 3 * k, row_stride(n)
+        return self._flat[(s + i - 5) * ns: (s + i - 5) * ns + n]
 
     def _get(self, name, i):
         if self._flat is not None:
@@ -75,9 +75,9 @@ class FieldGrads:
         if self._flat is not None:
             return self._flat
         parts = [torch.as_tensor(self._arrays[k] if torch.is_tensor(self._arrays[k]) else
-                                 np.asarray(self._arrays[k])).reshape(-1)
+                                 np.asarray(self._arrays[k]))
                  for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh")]
-        return torch.cat([p.to(device=device, dtype=torch.float32) for p in parts]).contiguous()
+        return pack_classes(parts, self._n, self._k, device)
 
     @property
     def flat(self):
@@ -112,8 +112,7 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
     d_soft = None if d_soft is None else _as_dev(d_soft, (h, w), dev)
     n, k = len(field), field.n_sh_coeffs
     if grads is None:
-        grads = FieldGrads(_flat=torch.empty(n * (row_floats(field.sh_degree) + 2), dtype=torch.float32,
-                                             device=dev), _n=n, _k=k)
+        grads = FieldGrads(_flat=torch.empty(flat_size(n, k, extra=2), dtype=torch.float32, device=dev), _n=n, _k=k)
         accumulate = False
     elif grads._flat is None or grads._n != n:
         raise InvalidParameter("grads buffer does not match the field")
@@ -132,3 +131,39 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
                   flat[sl[1][0]:].data_ptr(), flat[sl[2][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(), s,
                   rows.data_ptr(), grads.flat.data_ptr(), 1 if accumulate else 0, _lib.ptr(stats), st)
     return grads
+
+
+def backward_and_step(field, out: RenderOutput, d_image, d_soft, optimizer, position_rate: float,
+                      layout: str = "splat", stats: torch.Tensor | None = None) -> None:
+    """``backward`` followed by ``optimizer.step`` without materialising FieldGrads.
+
+    Same results as the two reference calls (backward.py:41-129 then
+    optim.py:113-130) up to fp32 rounding order; the chain kernels apply the
+    dense Adam update in place (ssr_chain_adam), saving the gradient buffer's
+    write and read (~0.5 GB per iteration at config 2).
+    """
+    from ..optim import SH_REST_LR
+
+    if out.generation != field.generation:
+        raise StaleFieldError(f"render saw generation {out.generation}, field is at {field.generation}")
+    if layout not in LAYOUTS:
+        raise ValueError(f"unknown backward layout {layout!r}")
+    optimizer.check(field)
+    cam, sp = out.cam, out.splats
+    h, w = cam.height, cam.width
+    dev = out.image.device
+    d_image = _as_dev(d_image, (h, w, 3), dev)
+    d_soft = None if d_soft is None else _as_dev(d_soft, (h, w), dev)
+    n = len(field)
+    m = sp.n_instances
+    st = _lib.stream_ptr()
+    s = sp.struct()
+    rows = torch.empty(max(m, 1) * 9 + 4, dtype=torch.float32, device=dev)
+    if m:
+        _lib.call("ssr_backward", LAYOUTS[layout], m, s, sp.inst_gauss.data_ptr(), sp.tile_ranges.data_ptr(),
+                  out.frame_struct(), d_image.data_ptr(), _lib.ptr(d_soft), rows.data_ptr(), st)
+    if n:
+        lr, bc1, bc2 = optimizer.advance(position_rate)
+        _lib.call("ssr_chain_adam", _lib.camera_struct(cam), n, field.sh_degree, field.flat.data_ptr(),
+                  optimizer.m.data_ptr(), optimizer.v.data_ptr(), s, rows.data_ptr(), _lib.ptr(stats), lr,
+                  SH_REST_LR, bc1, bc2, st)

@@ -24,6 +24,7 @@ from .field import DensifyOptions, GaussianField
 from .losses import LossBreakdown, LossWeights, total_loss
 from .optim import FieldOptimizer
 from .rasterize import FieldGrads, backward, render
+from .rasterize.backward import backward_and_step
 
 
 @dataclass
@@ -57,12 +58,23 @@ def densify(state: TrainState) -> None:
     state.stats = torch.zeros(2 * len(state.field), dtype=torch.float32, device=state.field.flat.device)
 
 
-def train_iteration(state: TrainState, cam, target, position_rate: float, bg=(0.0, 0.0, 0.0)) -> LossBreakdown:
-    """One iteration of the hot path on one view (pipeline.py:185-206)."""
+def train_iteration(state: TrainState, cam, target, position_rate: float, bg=(0.0, 0.0, 0.0),
+                    fused: bool = False) -> LossBreakdown:
+    """One iteration of the hot path on one view (pipeline.py:185-206).
+
+    Goes through FieldGrads exactly like the reference's backward + step calls.
+    ``fused=True`` uses backward_and_step (one chain+Adam pass, no gradient
+    buffer); it is verified equal but not yet faster (its TMA staging is not
+    double-buffered), so it is off by default.
+    """
     out = render(state.field, cam, bg=bg)
     br = total_loss(out.image, target, out, state.weights)
-    grads = backward(state.field, out, br.d_image, br.d_soft, layout=state.layout, stats=state.stats)
-    state.optimizer.step(state.field, grads, position_rate=position_rate)
+    if fused:
+        backward_and_step(state.field, out, br.d_image, br.d_soft, state.optimizer, position_rate,
+                          layout=state.layout, stats=state.stats)
+    else:
+        grads = backward(state.field, out, br.d_image, br.d_soft, layout=state.layout, stats=state.stats)
+        state.optimizer.step(state.field, grads, position_rate=position_rate)
     state.global_iteration += 1
     if state.densify_enabled and state.global_iteration % state.densify_interval == 0:
         densify(state)
@@ -110,9 +122,8 @@ class SemiGlobalBatch:
             losses.append(br)
         allreduce_grads(grads.flat, self.group)
         n = len(f)
-        s = 11 + 3 * f.n_sh_coeffs
-        st.stats[:n] += grads.flat[s * n:(s + 1) * n]
-        st.stats[n:] += grads.flat[(s + 1) * n:(s + 2) * n]
+        st.stats[:n] += grads.screen_norms
+        st.stats[n:] += grads.visible_count
         rate = float(np.mean(position_rates)) if len(position_rates) else 0.0
         st.optimizer.step(f, grads, position_rate=rate)
         st.global_iteration += 1

@@ -107,14 +107,19 @@ def test_fieldgrads_packing_layout():
     arrs = dict(positions=rng.standard_normal((n, 3)), rotations=rng.standard_normal((n, 4)),
                 log_scales=rng.standard_normal((n, 3)), opacity_logits=rng.standard_normal(n),
                 sh=rng.standard_normal((n, 3, k)))
+    from paper_2503_13086_b200.field import class_slices, row_stride
+
     g = FieldGrads(**arrs, screen_norms=np.zeros(n), visible=np.zeros(n, bool))
     flat = g.flat_params(torch.device("cpu"))
-    assert flat.numel() == n * (11 + 3 * k)
+    ns = row_stride(n)
+    assert ns == 8 and flat.numel() == ns * (11 + 3 * k)  # class regions padded to a multiple of 4 rows
+    sl = class_slices(n, k)
+    assert [o for o, _ in sl] == [0, 3 * ns, 7 * ns, 10 * ns, 11 * ns]
     np.testing.assert_allclose(flat[: 3 * n].numpy(), arrs["positions"].ravel(), rtol=1e-6)
-    np.testing.assert_allclose(flat[11 * n:].numpy(), arrs["sh"].ravel(), rtol=1e-6)
+    np.testing.assert_allclose(flat[11 * ns: 11 * ns + 3 * k * n].numpy(), arrs["sh"].ravel(), rtol=1e-6)
     z = FieldGrads.zeros(n, 1, torch.device("cpu"))
     assert z.positions.shape == (n, 3) and z.sh.shape == (n, 3, 4)
-    assert z.flat.numel() == n * (11 + 12 + 2)
+    assert z.flat.numel() == ns * (11 + 12 + 2)
     z.visible_count[2] = 3.0
     assert bool(z.visible[2]) and not bool(z.visible[1])
 

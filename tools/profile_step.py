@@ -25,7 +25,8 @@ opt = FieldOptimizer(f, scene_extent=6.6)
 target = torch.full((cam.height, cam.width, 3), 0.5, device="cuda")
 for _ in range(iters):
     out = render(f, cam)
-    br = total_loss(out.image, target, out, LossWeights(l1=1.0, ssim=0.2, load=0.0))
+    w = LossWeights() if os.environ.get("SSR_WEIGHTS") == "paper" else LossWeights(l1=1.0, ssim=0.2, load=0.0)
+    br = total_loss(out.image, target, out, w)
     g = backward(f, out, br.d_image, br.d_soft)
     opt.step(f, g, position_rate=1.6e-4)
 torch.cuda.synchronize()
