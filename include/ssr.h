@@ -79,6 +79,10 @@ typedef struct ssr_frame {
   uint8_t* flagged;    /* H x W  1 = pixel re-walked in fp64 (guard band) */
   int32_t* tile_info;  /* n_tiles x 2  (max n_walk, flagged pixel count) */
   float* ckpt;         /* ssr_ckpt_floats(M, n_tiles) floats: (T, C_front rgb) per bucket/pixel */
+  int32_t* fix_list;   /* ssr_fix_list_ints(W, H, n_tiles) int32, written by ssr_forward: [0] flagged
+                        * pixels, [1] flagged tiles, then n_tiles slots (first pixel entry of each
+                        * flagged tile, unordered), then W*H pixel entries (tile << 8 | pixel in tile),
+                        * contiguous per tile and in pixel order within it */
 } ssr_frame;
 
 const char* ssr_last_error(void);
@@ -127,6 +131,9 @@ int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles);
  * guard-band re-walk of pixels whose discrete decisions sit within a relative
  * band of a threshold: band_alpha around the alpha >= 1/255
  * gate and the 0.99 cap, band_t around the T(1 - alpha) < 1e-4 termination. */
+/* Size of ssr_frame.fix_list. */
+int64_t ssr_fix_list_ints(int32_t width, int32_t height, int32_t n_tiles);
+
 int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
                 const int32_t* tile_ranges, ssr_frame frame, float band_alpha, float band_t,
                 void* stream);

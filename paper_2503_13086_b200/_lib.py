@@ -36,7 +36,7 @@ class SsrFrame(ctypes.Structure):
     _fields_ = [("width", c_int32), ("height", c_int32), ("tiles_x", c_int32), ("tiles_y", c_int32),
                 ("bg", c_float * 3)] + [(k, c_void_p) for k in (
                     "image", "t_final", "n_walk", "terminated", "hard_count", "soft_count", "flagged",
-                    "tile_info", "ckpt")]
+                    "tile_info", "ckpt", "fix_list")]
 
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -55,6 +55,7 @@ _SIGS = {
     "ssr_bin_tiles": [c_int64, c_int64, c_int32, c_int32, SsrSplats, c_void_p, c_void_p, c_void_p, c_int64,
                       c_void_p],
     "ssr_ckpt_floats": [c_int64, c_int32],
+    "ssr_fix_list_ints": [c_int32, c_int32, c_int32],
     "ssr_forward": [c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_float, c_float, c_void_p],
     "ssr_backward": [c_int32, c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_void_p, c_void_p, c_void_p,
                      c_void_p],
@@ -77,7 +78,7 @@ _SIGS = {
     "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                  c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
 }
-_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64}
+_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_fix_list_ints": c_int64}
 
 EXPORTS = tuple(_SIGS)
 

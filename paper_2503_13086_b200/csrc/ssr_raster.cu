@@ -42,7 +42,12 @@ struct RasterArgs {
   uint8_t* flagged;
   int2* tile_info;
   float4* ckpt;
+  int* fix;  // fix_list: [0] pixels, [1] tiles, tile slots, pixel entries
+  int n_tiles;
 };
+
+__device__ __forceinline__ int* fix_tiles(const RasterArgs& a) { return a.fix + 2; }
+__device__ __forceinline__ int* fix_pixels(const RasterArgs& a) { return a.fix + 2 + a.n_tiles; }
 
 // Splat-major position of the instance of field row g in tile (tx, ty).
 __device__ __forceinline__ uint32_t inst_row(const RasterArgs& a, uint32_t g, int tx, int ty) {
@@ -174,12 +179,31 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   // per-tile (max n_walk over unflagged pixels, flagged count)
   int mw = (inside && !flag) ? nwk : 0;
   for (int o = 16; o > 0; o >>= 1) mw = max(mw, __shfl_xor_sync(FULL, mw, o));
-  if ((tid & 31) == 0) sMax[tid >> 5] = mw;
-  const int nflag = __syncthreads_count(inside && flag);
+  const bool fl = inside && flag;
+  const unsigned fm = __ballot_sync(FULL, fl);
+  __shared__ int sCnt[8];
+  __shared__ int sBase;
+  if ((tid & 31) == 0) {
+    sMax[tid >> 5] = mw;
+    sCnt[tid >> 5] = __popc(fm);
+  }
+  const int nflag = __syncthreads_count(fl);
   if (tid == 0) {
     int m = 0;
     for (int w = 0; w < 8; w++) m = max(m, sMax[w]);
     a.tile_info[t] = make_int2(m, nflag);
+    if (nflag) {  // reserve this tile's block of the compact fix-up lists
+      sBase = atomicAdd(&a.fix[0], nflag);
+      fix_tiles(a)[atomicAdd(&a.fix[1], 1)] = sBase;
+    }
+  }
+  if (nflag) {
+    __syncthreads();
+    if (fl) {
+      int r = __popc(fm & ((1u << (tid & 31)) - 1u));
+      for (int w = 0; w < (tid >> 5); w++) r += sCnt[w];
+      fix_pixels(a)[sBase + r] = (t << 8) | tid;
+    }
   }
 }
 
@@ -195,24 +219,43 @@ struct Slot64 {
   uint32_t g;
 };
 
+// The per-slot field data a float64 walk needs (independent of the pixel).
+struct SlotRaw {
+  bool valid;
+  uint32_t g;
+  double2 m, c0, c1, k0, k1;
+};
+
+__device__ __forceinline__ void load_slot(const RasterArgs& a, int s, int s1, SlotRaw& r) {
+  r.valid = s < s1;
+  if (!r.valid) return;
+  r.g = a.inst[s];
+  r.m = a.mean[r.g];
+  r.c0 = a.conic_opa64[2 * r.g];
+  r.c1 = a.conic_opa64[2 * r.g + 1];
+  r.k0 = a.color64[2 * r.g];
+  r.k1 = a.color64[2 * r.g + 1];
+}
+
 // kernels.py:68-89 for one slot in float64, mirroring the reference's op order.
-__device__ __forceinline__ void slot64(const RasterArgs& a, int s, int s1, double xx, double yy, Slot64& q) {
-  q.valid = s < s1;
+// `with_sv` = false skips the soft-count sigmoid (only the backward fix-up
+// without a soft-count gradient does that; q.sv is then 0).
+__device__ __forceinline__ void eval_slot(const SlotRaw& r, bool valid, double xx, double yy, Slot64& q,
+                                          bool with_sv = true) {
+  q.valid = valid;
   q.skip = true;
   q.cand = false;
   q.capped = false;
   q.alpha = 0.0;
   q.sv = 0.0;
-  if (!q.valid) return;
-  q.g = a.inst[s];
-  const double2 m = a.mean[q.g];
-  const double2 c0 = a.conic_opa64[2 * q.g], c1 = a.conic_opa64[2 * q.g + 1];
-  q.qa = c0.x;
-  q.qb = c0.y;
-  q.qc = c1.x;
-  q.opa = c1.y;
-  q.dx = __dsub_rn(xx, m.x);
-  q.dy = __dsub_rn(yy, m.y);
+  if (!valid) return;
+  q.g = r.g;
+  q.qa = r.c0.x;
+  q.qb = r.c0.y;
+  q.qc = r.c1.x;
+  q.opa = r.c1.y;
+  q.dx = __dsub_rn(xx, r.m.x);
+  q.dy = __dsub_rn(yy, r.m.y);
   const double t1 = __dmul_rn(__dmul_rn(q.qa, q.dx), q.dx);
   const double t2 = __dmul_rn(__dmul_rn(q.qc, q.dy), q.dy);
   const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), __dmul_rn(__dmul_rn(q.qb, q.dx), q.dy));
@@ -222,12 +265,11 @@ __device__ __forceinline__ void slot64(const RasterArgs& a, int s, int s1, doubl
   q.capped = alpha > ALPHA_CAP;
   if (q.capped) alpha = ALPHA_CAP;
   q.alpha = alpha;
-  q.sv = 1.0 / (1.0 + exp(-(alpha - ALPHA_MIN) / SOFT_TAU));
+  if (with_sv) q.sv = 1.0 / (1.0 + exp(-(alpha - ALPHA_MIN) / SOFT_TAU));
   q.cand = alpha >= ALPHA_MIN;
-  const double2 k0 = a.color64[2 * q.g], k1 = a.color64[2 * q.g + 1];
-  q.col[0] = k0.x;
-  q.col[1] = k0.y;
-  q.col[2] = k1.x;
+  q.col[0] = r.k0.x;
+  q.col[1] = r.k0.y;
+  q.col[2] = r.k1.x;
 }
 
 struct Pix64 {
@@ -243,11 +285,27 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
   const int lane = threadIdx.x & 31;
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, soft = 0.0;
   int hard = 0, nw = s1 - s0, term = 0;
+  // Two-stage prefetch: the next chunk's field data and the index of the one
+  // after it are in flight while the current chunk is evaluated.
+  SlotRaw cur;
+  load_slot(a, s0 + lane, s1, cur);
+  uint32_t g_next = s0 + 32 + lane < s1 ? a.inst[s0 + 32 + lane] : 0u;
   for (int cb = s0; cb < s1; cb += 32) {
     if (ck && cb > s0 && lane == 0)
       ck[(size_t)((cb - s0) >> 5) * TILE_PX] = make_float4((float)T, (float)C0, (float)C1, (float)C2);
+    SlotRaw nxt;
+    nxt.valid = cb + 32 + lane < s1;
+    if (nxt.valid) {
+      nxt.g = g_next;
+      nxt.m = a.mean[g_next];
+      nxt.c0 = a.conic_opa64[2 * g_next];
+      nxt.c1 = a.conic_opa64[2 * g_next + 1];
+      nxt.k0 = a.color64[2 * g_next];
+      nxt.k1 = a.color64[2 * g_next + 1];
+    }
+    g_next = cb + 64 + lane < s1 ? a.inst[cb + 64 + lane] : 0u;
     Slot64 q;
-    slot64(a, cb + lane, s1, xx, yy, q);
+    eval_slot(cur, cur.valid, xx, yy, q);
     const double f = q.cand ? (1.0 - q.alpha) : 1.0;
     double P = f;
     for (int d = 1; d < 32; d <<= 1) {
@@ -274,6 +332,7 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
       break;
     }
     T = T * __shfl_sync(FULL, P, 31);
+    cur = nxt;
   }
   r.T = T;
   r.C[0] = C0;
@@ -285,43 +344,19 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
   r.term = term;
 }
 
-// Block-wide list of a tile's flagged pixels, in pixel order.
-__device__ __forceinline__ int flagged_list(const RasterArgs& a, int tx, int ty, int* list, int* wcount) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int px = tx * TILE + (tid & 15), py = ty * TILE + (tid >> 4);
-  const bool f = px < a.width && py < a.height && a.flagged[(size_t)py * a.width + px];
-  const unsigned m = __ballot_sync(FULL, f);
-  if (lane == 0) wcount[warp] = __popc(m);
-  __syncthreads();
-  int base = 0, total = 0;
-  for (int w = 0; w < 8; w++) {
-    if (w < warp) base += wcount[w];
-    total += wcount[w];
-  }
-  if (f) list[base + __popc(m & ((1u << lane) - 1u))] = tid;
-  __syncthreads();
-  return total;
-}
-
-// Forward fix-up: one CTA (8 warps) per tile with flagged pixels; each warp
-// re-walks flagged pixels in float64 (pixels are independent).
+// Forward fix-up: persistent grid, one warp per flagged pixel of the compact
+// list k_forward built (pixels are independent).
 __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
-  const int t = blockIdx.x;
-  const int2 info = a.tile_info[t];
-  if (info.y == 0) return;
-  __shared__ int list[TILE_PX];
-  __shared__ int wcount[8];
-  __shared__ int smax;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-  const int nflag = flagged_list(a, tx, ty, list, wcount);
-  if (threadIdx.x == 0) smax = info.x;
-  __syncthreads();
-  const int2 rg = a.ranges[t];
-  for (int f = warp; f < nflag; f += 8) {
-    const int p = list[f];
+  const int lane = threadIdx.x & 31;
+  const int nw_total = gridDim.x * 8, count = a.fix[0];
+  const int* px_list = fix_pixels(a);
+  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < count; i += nw_total) {
+    const int e = px_list[i];
+    const int t = e >> 8, p = e & 255;
+    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
     const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
     const size_t pix = (size_t)py * a.width + px;
+    const int2 rg = a.ranges[t];
     Pix64 r;
     walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt + ckpt_base(rg.x, t) + p);
     if (lane == 0) {
@@ -333,11 +368,10 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
       a.term[pix] = (uint8_t)r.term;
       a.hard[pix] = r.hard;
       a.soft[pix] = r.soft;
-      atomicMax(&smax, r.nw);
+      // tile_info.x stays an upper bound of the tile's n_walk (buckets to visit).
+      atomicMax(&a.tile_info[t].x, r.nw);
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) a.tile_info[t].x = smax;
 }
 
 // ------------------------------------------------------------------ backward, splat-parallel (fp32)
@@ -654,90 +688,129 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
 // without atomics, and parallel over buckets.  Backward decisions do not
 // depend on T (termination comes from n_walk / terminated), so fp32 seeds only
 // perturb gradient values, never which slots blend.
-constexpr int FIXUP_YBLOCKS = 8;  // gridDim.y; warp w of block y takes buckets y*8+w, +64, ...
+struct FixPix {
+  double w0, w1, w2, ws, wimg;
+  int nw, term, p;
+};
+// Persistent grid, one CTA per flagged tile (compact list from k_forward);
+// warp w takes buckets w, w+8, ...
 __global__ void __launch_bounds__(256) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
-  const int t = blockIdx.x;
-  const int2 info = a.tile_info[t];
-  if (info.y == 0) return;
-  const int nb = (info.x + 31) >> 5;
-  if ((int)blockIdx.y * 8 >= nb) return;
-  __shared__ int list[TILE_PX];
-  __shared__ int wcount[8];
+  __shared__ FixPix sp[TILE_PX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-  const int nflag = flagged_list(a, tx, ty, list, wcount);
-  const int2 rg = a.ranges[t];
-  const int s0 = rg.x, s1 = rg.y;
-  const float4* ckt = a.ckpt + ckpt_base(s0, t);
-  for (int b = blockIdx.y * 8 + warp; b < nb; b += FIXUP_YBLOCKS * 8) {
-    const int kb = b * 32, k = kb + lane;
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int f = 0; f < nflag; f++) {
-      const int p = list[f];
+  const int n_ft = a.fix[1];
+  for (int it = blockIdx.x; it < n_ft; it += gridDim.x) {
+    const int start = fix_tiles(a)[it];
+    const int t = fix_pixels(a)[start] >> 8;
+    const int2 info = a.tile_info[t];
+    const int nflag = info.y, nb = (info.x + 31) >> 5;
+    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+    __syncthreads();  // previous tile's sp[] readers are done
+    // Per-pixel inputs, loaded once per tile (shared by the CTA's buckets).
+    if ((int)threadIdx.x < nflag) {
+      const int p = fix_pixels(a)[start + threadIdx.x] & 255;
       const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
       const size_t pix = (size_t)py * a.width + px;
-      const int nw = a.n_walk[pix];
-      if (nw <= kb) continue;  // warp-uniform
-      const int term = a.term[pix];
-      const double w0 = d_image[pix * 3], w1 = d_image[pix * 3 + 1], w2 = d_image[pix * 3 + 2];
-      const double ws = d_soft ? (double)d_soft[pix] : 0.0;
-      const double wimg =
-          w0 * (double)a.image[pix * 3] + w1 * (double)a.image[pix * 3 + 1] + w2 * (double)a.image[pix * 3 + 2];
-      double T = 1.0, H = 0.0;
-      if (b > 0) {
-        const float4 c = ckt[(size_t)b * TILE_PX + p];
-        T = c.x;
-        H = w0 * c.y + w1 * c.z + w2 * c.w;
-      }
-      Slot64 q;
-      slot64(a, s0 + k, s0 + nw, (double)px, (double)py, q);
-      const bool bl = q.cand && !(term && k == nw - 1);
-      const double f1 = bl ? (1.0 - q.alpha) : 1.0;
-      double P = f1;
-      for (int d = 1; d < 32; d <<= 1) {
-        const double o = __shfl_up_sync(FULL, P, d);
-        if (lane >= d) P *= o;
-      }
-      double Pex = __shfl_up_sync(FULL, P, 1);
-      if (lane == 0) Pex = 1.0;
-      const double Tb = T * Pex;
-      const double wc = bl ? (w0 * q.col[0] + w1 * q.col[1] + w2 * q.col[2]) : 0.0;
-      const double e = bl ? q.alpha * Tb * wc : 0.0;
-      double E = e;  // inclusive prefix sum of w.(c alpha T)
-      for (int d = 1; d < 32; d <<= 1) {
-        const double o = __shfl_up_sync(FULL, E, d);
-        if (lane >= d) E += o;
-      }
-      const double Hb = H + (E - e);
-      if (q.valid && !q.skip) {
-        double dlda = 0.0;
-        if (bl) {
-          const double aT = q.alpha * Tb;
-          acc[0] += aT * w0;
-          acc[1] += aT * w1;
-          acc[2] += aT * w2;
-          dlda = Tb * wc - (wimg - Hb - aT * wc) / (1.0 - q.alpha);
+      FixPix q;
+      q.w0 = d_image[pix * 3];
+      q.w1 = d_image[pix * 3 + 1];
+      q.w2 = d_image[pix * 3 + 2];
+      q.ws = d_soft ? (double)d_soft[pix] : 0.0;
+      q.wimg = q.w0 * (double)a.image[pix * 3] + q.w1 * (double)a.image[pix * 3 + 1] +
+               q.w2 * (double)a.image[pix * 3 + 2];
+      q.nw = a.n_walk[pix];
+      q.term = a.term[pix];
+      q.p = p;
+      sp[threadIdx.x] = q;
+    }
+    __syncthreads();
+    const int2 rg = a.ranges[t];
+    const int s0 = rg.x, s1 = rg.y;
+    const float4* ckt = a.ckpt + ckpt_base(s0, t);
+    const bool soft_grad = d_soft != nullptr;
+    for (int b = warp; b < nb; b += 8) {
+      const int kb = b * 32, k = kb + lane;
+      // The bucket's slots, loaded once for all flagged pixels.
+      SlotRaw raw;
+      load_slot(a, s0 + k, s1, raw);
+      double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      float4 cnext = make_float4(1.f, 0.f, 0.f, 0.f);
+      int f = 0;
+      while (f < nflag && sp[f].nw <= kb) f++;  // warp-uniform
+      if (f < nflag && b > 0) cnext = ckt[(size_t)b * TILE_PX + sp[f].p];
+      while (f < nflag) {
+        const FixPix q = sp[f];
+        const float4 c = cnext;
+        int fn = f + 1;
+        while (fn < nflag && sp[fn].nw <= kb) fn++;
+        if (fn < nflag && b > 0) cnext = ckt[(size_t)b * TILE_PX + sp[fn].p];
+        const int px = tx * TILE + (q.p & 15), py = ty * TILE + (q.p >> 4);
+        double T = 1.0, H = 0.0;
+        if (b > 0) {
+          T = c.x;
+          H = q.w0 * c.y + q.w1 * c.z + q.w2 * c.w;
         }
-        if (!q.capped) {
-          acc[3] += (dlda + ws * q.sv * (1.0 - q.sv) / SOFT_TAU) * q.alpha * (1.0 - q.opa);
+        Slot64 s;
+        eval_slot(raw, k < q.nw && raw.valid, (double)px, (double)py, s, soft_grad);
+        const bool bl = s.cand && !(q.term && k == q.nw - 1);
+        const double f1 = bl ? (1.0 - s.alpha) : 1.0;
+        double P = f1;
+        for (int d = 1; d < 32; d <<= 1) {
+          const double o = __shfl_up_sync(FULL, P, d);
+          if (lane >= d) P *= o;
+        }
+        double Pex = __shfl_up_sync(FULL, P, 1);
+        if (lane == 0) Pex = 1.0;
+        const double Tb = T * Pex;
+        const double wc = bl ? (q.w0 * s.col[0] + q.w1 * s.col[1] + q.w2 * s.col[2]) : 0.0;
+        const double e = bl ? s.alpha * Tb * wc : 0.0;
+        double E = e;  // inclusive prefix sum of w.(c alpha T)
+        for (int d = 1; d < 32; d <<= 1) {
+          const double o = __shfl_up_sync(FULL, E, d);
+          if (lane >= d) E += o;
+        }
+        const double Hb = H + (E - e);
+        if (s.valid && !s.skip) {
+          double dlda = 0.0;
           if (bl) {
-            const double gp = dlda * q.alpha;
-            acc[4] += gp * (q.qa * q.dx + q.qb * q.dy);
-            acc[5] += gp * (q.qb * q.dx + q.qc * q.dy);
-            acc[6] += gp * (-0.5 * q.dx * q.dx);
-            acc[7] += gp * (-q.dx * q.dy);
-            acc[8] += gp * (-0.5 * q.dy * q.dy);
+            const double aT = s.alpha * Tb;
+            acc[0] += aT * q.w0;
+            acc[1] += aT * q.w1;
+            acc[2] += aT * q.w2;
+            dlda = Tb * wc - (q.wimg - Hb - aT * wc) / (1.0 - s.alpha);
+          }
+          if (!s.capped) {
+            acc[3] += (dlda + q.ws * s.sv * (1.0 - s.sv) / SOFT_TAU) * s.alpha * (1.0 - s.opa);
+            if (bl) {
+              const double gp = dlda * s.alpha;
+              acc[4] += gp * (s.qa * s.dx + s.qb * s.dy);
+              acc[5] += gp * (s.qb * s.dx + s.qc * s.dy);
+              acc[6] += gp * (-0.5 * s.dx * s.dx);
+              acc[7] += gp * (-s.dx * s.dy);
+              acc[8] += gp * (-0.5 * s.dy * s.dy);
+            }
           }
         }
+        f = fn;
+      }
+      if (raw.valid) {
+        float* row = rows + (size_t)inst_row(a, raw.g, tx, ty) * 9;
+        for (int j = 0; j < 9; j++)
+          if (acc[j] != 0.0) row[j] += (float)acc[j];
       }
     }
-    if (s0 + k < s1) {
-      float* row = rows + (size_t)inst_row(a, a.inst[s0 + k], tx, ty) * 9;
-      for (int j = 0; j < 9; j++)
-        if (acc[j] != 0.0) row[j] += (float)acc[j];
-    }
   }
+}
+
+static int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+extern "C" int64_t ssr_fix_list_ints(int32_t width, int32_t height, int32_t n_tiles) {
+  return 2 + (int64_t)n_tiles + (int64_t)width * height;
 }
 
 static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* ranges, const ssr_frame& f,
@@ -771,6 +844,8 @@ static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* 
   a.flagged = f.flagged;
   a.tile_info = (int2*)f.tile_info;
   a.ckpt = (float4*)f.ckpt;
+  a.fix = f.fix_list;
+  a.n_tiles = f.tiles_x * f.tiles_y;
   return a;
 }
 
@@ -787,9 +862,14 @@ extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_ga
     return SSR_ERR_INVALID;
   }
   RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, band_alpha, band_t);
+  if (!frame.fix_list) {
+    set_error("ssr_forward: frame.fix_list is required");
+    return SSR_ERR_INVALID;
+  }
+  if (cudaMemsetAsync(frame.fix_list, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return check_launch("fix_list reset");
   k_forward<<<n_tiles, TILE_PX, 0, st>>>(a);
   SSR_TRY(check_launch("k_forward"));
-  k_forward_fixup<<<n_tiles, 256, 0, st>>>(a);
+  k_forward_fixup<<<num_sms() * 4, 256, 0, st>>>(a);
   return check_launch("k_forward_fixup");
 }
 
@@ -809,6 +889,10 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
   else
     k_backward_pixel<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
   SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
-  k_backward_fixup<<<dim3(n_tiles, FIXUP_YBLOCKS), 256, 0, st>>>(a, d_image, d_soft, inst_rows);
+  if (!frame.fix_list) {
+    set_error("ssr_backward: frame.fix_list is required");
+    return SSR_ERR_INVALID;
+  }
+  k_backward_fixup<<<num_sms() * 3, 256, 0, st>>>(a, d_image, d_soft, inst_rows);
   return check_launch("k_backward_fixup");
 }

@@ -38,6 +38,7 @@ class RenderOutput:
     flagged: torch.Tensor = dc_field(default=None, repr=False)  # (H, W) uint8 guard-band pixels
     tile_info: torch.Tensor = dc_field(default=None, repr=False)  # (n_tiles, 2) int32
     ckpt: torch.Tensor = dc_field(default=None, repr=False)  # bucket checkpoints (T, C_front)
+    fix_list: torch.Tensor = dc_field(default=None, repr=False)  # compact flagged pixel / tile lists
 
     @property
     def n_visible(self) -> int:
@@ -50,7 +51,7 @@ class RenderOutput:
         for i in range(3):
             f.bg[i] = float(self.bg[i])
         for k in ("image", "t_final", "n_walk", "terminated", "hard_count", "soft_count", "flagged", "tile_info",
-                  "ckpt"):
+                  "ckpt", "fix_list"):
             t = getattr(self, k)
             setattr(f, k, t.data_ptr() if t.numel() else None)
         return f
@@ -76,6 +77,7 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
         generation=field.generation, workers=workers, flagged=e(h, w, dt=torch.uint8),
         tile_info=e(n_tiles, 2, dt=torch.int32),
         ckpt=e(int(_lib.load().ssr_ckpt_floats(m, n_tiles))),
+        fix_list=e(int(_lib.load().ssr_fix_list_ints(w, h, n_tiles)), dt=torch.int32),
     )
     _lib.call("ssr_forward", m, splats.struct(), splats.inst_gauss.data_ptr() if m else None,
               splats.tile_ranges.data_ptr(), out.frame_struct(), band, band_t, _lib.stream_ptr())
