@@ -244,11 +244,14 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # prime the caching allocator with every view's buffer sizes (instance counts
+    # differ per view), then the W warm-up steps proper
+    for k in range(len(cams) // world):
+        step(k)
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
     # ---------------- timed region (device time, CUDA events on the launching stream)
-    _lib.enable_timers(True)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -260,6 +263,11 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
+    # per-ABI-call device times, from a separate (untimed) pass: the event pairs
+    # around every call would otherwise perturb the timed region
+    _lib.enable_timers(True)
+    for k in range(min(args.steps, 5)):
+        step(args.warmup + k)
     stage_ms = _lib.timer_ms()
     _lib.enable_timers(False)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)

@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
 
   float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, sdev = 0.f;
   double sbig = 0.0;
-  int hard = 0, nwk = s1 - s0, scnt = 0;
+  // every walked slot is exactly one of: far or small-alpha (soft term S0 +
+  // deviation), skipped fragile (no term), or large-alpha (exact sigmoid), so
+  // the S0 count is n_walk - n_big and the common paths count nothing
+  int hard = 0, nwk = s1 - s0, nbig = 0;
   bool term = false, flag = false, done = !inside;
   float4* ck = a.ckpt + ckpt_base(s0, t) + tid;
 
@@ -114,10 +117,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
           float qpos;
           const float p2 = pair_power2(dxx, dxy, dyy, A.x, A.y, A.z, qpos);
-          if (p2 < FAR_POWER2) {
-            scnt++;
-            continue;
-          }
+          if (p2 < FAR_POWER2) continue;  // soft term S0, nothing else
           // Only near-singular conics (negative staged opacity, warp-uniform)
           // can round to power > 0: flag the pixel near that decision.
           if (A.w < 0.f) {
@@ -125,21 +125,26 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
               flag = true;
               break;
             }
-            if (p2 > 0.f) continue;
+            if (p2 > 0.f) {
+              nbig++;  // skipped: no soft term (counted out of the S0 total)
+              continue;
+            }
           }
           float alpha = pair_alpha2(fabsf(A.w), p2);
+          // common path: alpha < 2.5e-3 is below 1/255 and far from both guard
+          // bands, so it only adds its soft-count deviation
+          const float y = __fmul_rn(alpha, 100.f);
+          if (y < SOFT_Y0) {
+            sdev += soft_dev_poly(y);
+            continue;
+          }
           if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
             flag = true;
             break;
           }
           alpha = fminf(alpha, ALPHA_CAP_F);
-          const float y = __fmul_rn(alpha, 100.f);
-          if (y < SOFT_Y0) {
-            scnt++;
-            sdev += soft_dev_poly(y);
-          } else {
-            sbig += (double)soft_sigmoid_accurate(alpha);
-          }
+          nbig++;
+          sbig += (double)soft_sigmoid_accurate(alpha);
           if (alpha < ALPHA_MIN_F) continue;
           const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
           if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
     a.n_walk[pix] = nwk;
     a.term[pix] = term ? 1 : 0;
     a.hard[pix] = hard;
-    a.soft[pix] = (double)scnt * SOFT_S0 + (sbig + (double)sdev);
+    a.soft[pix] = (double)(nwk - nbig) * SOFT_S0 + (sbig + (double)sdev);
     a.flagged[pix] = flag ? 1 : 0;
   }
   // per-tile (max n_walk over unflagged pixels, flagged count)
@@ -381,6 +386,122 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
 // l handles live pixel i-l and receives that pixel's running (T, H = w.C_front)
 // from lane l-1 by shuffle.  Lane 0 seeds each pixel from the forward's
 // bucket checkpoint.  No atomics; each instance row is written once.
+//
+// The pixel list of a bucket is padded with 32 sentinel entries on both sides
+// (pixel 256: blend limit 0), so the stream needs no bounds checks.  The mean
+// gradient is accumulated as sum(gp dx), sum(gp dy) and mapped through the
+// conic once per row (linear), so a contributing pair costs ~30 instructions.
+constexpr int BW_PAD = 32;
+constexpr int BW_LIST = BW_PAD + TILE_PX + BW_PAD;
+
+struct BwSplat {
+  StagedMean sm;
+  StagedConic q;
+  float opa, cr, cg, cbl, p2_min;
+};
+
+struct BwAcc {
+  float g0, g1, g2, g3, sx, sy, g6, g7, g8;
+};
+
+// One bucket's stream.  SOFT = false: the tile carries no soft-count gradient,
+// so only blended pairs contribute; sPB.w holds the blend limit n_walk - term.
+// SOFT = true: sPB.w holds n_walk << 1 | terminated and every walked pair with
+// alpha below the cap adds its soft term.
+template <bool SOFT>
+__device__ __forceinline__ void bw_stream(const float4* __restrict__ sPA, const float4* __restrict__ sPB,
+                                          const uint16_t* __restrict__ list, const float2* __restrict__ seed,
+                                          int n_live, int lane, int k, const BwSplat& s, BwAcc& g) {
+  float T = 1.f, H = 0.f;
+  const int n_steps = n_live + 31;
+  int jn = BW_PAD - lane;  // padded list index of step 0
+  int pn = list[jn];
+  float4 PBn = sPB[pn];
+#pragma unroll 2
+  for (int i = 0; i < n_steps; i++) {
+    float Tin = __shfl_up_sync(FULL, T, 1);
+    float Hin = __shfl_up_sync(FULL, H, 1);
+    const float2 sd = seed[i];  // broadcast read (garbage past n_live: sentinel steps)
+    if (lane == 0) {
+      Tin = sd.x;
+      Hin = sd.y;
+    }
+    T = Tin;
+    H = Hin;
+    const int p = pn;
+    const float4 PB = PBn;
+    jn++;
+    pn = list[jn];
+    PBn = sPB[pn];
+    const int lim = __float_as_int(PB.w);
+    const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
+    const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+    float qpos;
+    const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
+    if (!SOFT) {
+      const float araw = pair_alpha2(s.opa, p2);
+      if (k < lim && p2 <= 0.f && p2 >= s.p2_min && araw >= ALPHA_MIN_F) {
+        const float alpha = fminf(araw, ALPHA_CAP_F);
+        const float4 w = sPA[p];
+        const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+        const float aT = alpha * T;
+        g.g0 = fmaf(aT, w.x, g.g0);
+        g.g1 = fmaf(aT, w.y, g.g1);
+        g.g2 = fmaf(aT, w.z, g.g2);
+        const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
+        const float awc = aT * wc;
+        const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
+        const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
+        H += awc;
+        T = __fmul_rn(T, one_m);
+        const float gp = araw > ALPHA_CAP_F ? 0.f : dlda * alpha;  // capped: no opacity/geometry path
+        g.g3 += gp;
+        g.sx = fmaf(gp, dx, g.sx);
+        g.sy = fmaf(gp, dy, g.sy);
+        g.g6 = fmaf(gp, dxx, g.g6);
+        g.g7 = fmaf(gp, dxy, g.g7);
+        g.g8 = fmaf(gp, dyy, g.g8);
+      }
+    } else {
+      const int nw = lim >> 1;
+      if (k < nw && p2 <= 0.f && p2 >= s.p2_min) {
+        const float araw = pair_alpha2(s.opa, p2);
+        const bool capped = araw > ALPHA_CAP_F;
+        const float alpha = capped ? ALPHA_CAP_F : araw;
+        // the terminating slot (k == nw - 1 of a terminated walk) is never blended
+        const bool blended = alpha >= ALPHA_MIN_F && k < nw - (lim & 1);
+        const float4 w = sPA[p];
+        float dlda = 0.f;
+        if (blended) {
+          const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+          const float aT = alpha * T;
+          g.g0 = fmaf(aT, w.x, g.g0);
+          g.g1 = fmaf(aT, w.y, g.g1);
+          g.g2 = fmaf(aT, w.z, g.g2);
+          const float one_m = __fsub_rn(1.f, alpha);
+          const float awc = aT * wc;
+          const float sdot = PB.z - H - awc;
+          dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
+          H += awc;
+          T = __fmul_rn(T, one_m);
+        }
+        if (!capped) {
+          const float sv = soft_sigmoid(alpha);
+          g.g3 = fmaf(fmaf(w.w * sv * (1.f - sv), 100.f, dlda), alpha, g.g3);
+          if (blended) {
+            const float gp = dlda * alpha;
+            g.sx = fmaf(gp, dx, g.sx);
+            g.sy = fmaf(gp, dy, g.sy);
+            g.g6 = fmaf(gp, dxx, g.g6);
+            g.g7 = fmaf(gp, dxy, g.g7);
+            g.g8 = fmaf(gp, dyy, g.g8);
+          }
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
   const int t = blockIdx.x;
@@ -392,34 +513,47 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
 
-  __shared__ float4 sPA[TILE_PX];  // dL/dr, dL/dg, dL/db, dL/dsoft
-  __shared__ float4 sPB[TILE_PX];  // pixel x, y (tile-relative), w . image, n_walk << 1 | terminated
-  __shared__ float2 sSeed[8][TILE_PX];  // per warp: (T, H) entering the bucket, i-th live pixel
-  __shared__ uint8_t sList[8][TILE_PX];  // per warp: live pixels of the current bucket
+  __shared__ float4 sPA[TILE_PX];      // dL/dr, dL/dg, dL/db, dL/dsoft
+  __shared__ float4 sPB[TILE_PX + 1];  // pixel x, y (tile-relative), w . image, walk limit; [256] = sentinel
+  __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
+  __shared__ uint16_t sList[8][BW_LIST];     // per warp: live pixels of the current bucket, padded
+  bool soft_px = false;
   {
     const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
-    int nwt = 0;
+    int nw = 0, term = 0;
     float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
     float wimg = 0.f;
     if (px < a.width && py < a.height) {
       const size_t pix = (size_t)py * a.width + px;
-      if (!a.flagged[pix]) nwt = (a.n_walk[pix] << 1) | (a.term[pix] ? 1 : 0);
+      if (!a.flagged[pix]) {
+        nw = a.n_walk[pix];
+        term = a.term[pix] ? 1 : 0;
+      }
       w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
       wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
     }
+    soft_px = w.w != 0.f;
     sPA[tid] = w;
-    sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(nwt));
+    // does any pixel of the tile carry a soft-count gradient?  If not, pairs
+    // with alpha < 1/255 (and terminating slots) contribute exactly nothing.
+    const bool us = __syncthreads_or(soft_px);
+    const int lim = us ? ((nw << 1) | term) : nw - term;
+    sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(lim));
+    if (tid < 8)
+      for (int e = 0; e < BW_PAD; e++) {
+        sList[tid][e] = TILE_PX;
+        sList[tid][BW_PAD + TILE_PX + e] = TILE_PX;
+      }
+    if (tid == 0) sPB[TILE_PX] = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    soft_px = us;
   }
   __syncthreads();
-
-  // does any pixel of the tile carry a soft-count gradient?  If not, pairs
-  // with alpha < 1/255 contribute exactly nothing and are skipped (uniform).
-  const bool use_soft = __syncthreads_or(sPA[tid].w != 0.f);
+  const bool use_soft = soft_px;
 
   const int nb = (maxw + 31) >> 5;
   const float4* ckt = a.ckpt + ckpt_base(s0, t);
   const unsigned lt_mask = (1u << lane) - 1u;
-  uint8_t* const myList = sList[warp];
+  uint16_t* const myList = sList[warp] + BW_PAD;
   float2* const mySeed = sSeed[warp];
   for (int b = warp; b < nb; b += 8) {
     const int kb = b * 32;
@@ -428,11 +562,14 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
 #pragma unroll
     for (int c = 0; c < 8; c++) {
       const int p = c * 32 + lane;
-      const bool lv = (__float_as_int(sPB[p].w) >> 1) > kb;
+      const int lim = __float_as_int(sPB[p].w);
+      const bool lv = (use_soft ? (lim >> 1) : lim) > kb;
       const unsigned msk = __ballot_sync(FULL, lv);
-      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint8_t)p;
+      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint16_t)p;
       n_live += __popc(msk);
     }
+    // sentinels after the live pixels (the padding after 256 entries is fixed)
+    if (n_live + lane < TILE_PX) myList[n_live + lane] = TILE_PX;
     __syncwarp();
     for (int j = lane; j < n_live; j += 32) {
       const int p = myList[j];
@@ -447,111 +584,48 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
     __syncwarp();
     const int k = kb + lane;
     const bool live = k < maxw;
-    float ca = 0.f, cb = 0.f, cc = 0.f, opa = 0.f, cr = 0.f, cg = 0.f, cbl = 0.f;
-    StagedConic q = {0.f, 0.f, 0.f};
-    StagedMean sm = {0.f, 0.f, 0.f, 0.f};
-    float p2_min = FAR_POWER2;  // pairs below this contribute nothing
+    BwSplat s;
+    s.sm = {0.f, 0.f, 0.f, 0.f};
+    s.q = {0.f, 0.f, 0.f};
+    s.opa = s.cr = s.cg = s.cbl = 0.f;
+    s.p2_min = __int_as_float(0x7f800000);  // +inf: lanes past the walks never contribute
+    float ca = 0.f, cb = 0.f, cc = 0.f;
     uint32_t orow = 0;
     if (live) {
       const uint32_t g = a.inst[s0 + k];
       const double2 m = a.mean[g];
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
-      sm = stage_mean(m.x, m.y, x00, y00);
+      s.sm = stage_mean(m.x, m.y, x00, y00);
       ca = co.x;
       cb = co.y;
       cc = co.z;
-      opa = fabsf(co.w);
-      q = stage_conic(ca, cb, cc);
-      cr = col.x;
-      cg = col.y;
-      cbl = col.z;
+      s.opa = fabsf(co.w);
+      s.q = stage_conic(ca, cb, cc);
+      s.cr = col.x;
+      s.cg = col.y;
+      s.cbl = col.z;
       orow = inst_row(a, g, tx, ty);
       // without soft gradients only alpha >= 1/255 matters: alpha < 0.999/255
       // is certain below log2(0.999 / (255 opacity))
-      if (!use_soft) p2_min = fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / opa));
+      s.p2_min = use_soft ? FAR_POWER2 : fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / s.opa));
     }
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
-    float T = 1.f, H = 0.f;
-    const int n_steps = n_live + 31;
-    const int last = n_live - 1;
-    // software pipeline: the (list -> pixel data) shared-memory chain of the
-    // next step is issued before this step's arithmetic
-    int jn = -lane;  // pixel list index of step 0
-    int pn = myList[max(min(jn, last), 0)];
-    float4 PBn = sPB[pn];
-    for (int i = 0; i < n_steps; i++) {
-      float Tin = __shfl_up_sync(FULL, T, 1);
-      float Hin = __shfl_up_sync(FULL, H, 1);
-      const float2 sd = mySeed[min(i, last)];  // broadcast read
-      if (lane == 0) {
-        Tin = sd.x;
-        Hin = sd.y;
-      }
-      T = Tin;
-      H = Hin;
-      const int j = jn, p = pn;
-      const float4 PB = PBn;
-      jn = j + 1;
-      pn = myList[max(min(jn, last), 0)];
-      PBn = sPB[pn];
-      const bool inr = live && (unsigned)j < (unsigned)n_live;
-      const int nwt = __float_as_int(PB.w);
-      const int nw = nwt >> 1;
-      const float dx = pair_d(PB.x, sm.xi, sm.xf), dy = pair_d(PB.y, sm.yi, sm.yf);
-      const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
-      float qpos;
-      const float p2 = pair_power2(dxx, dxy, dyy, q.a2, q.b2, q.c2, qpos);
-      if (inr && k < nw && p2 <= 0.f && p2 >= p2_min) {
-        const float araw = pair_alpha2(opa, p2);
-        const bool capped = araw > ALPHA_CAP_F;
-        const float alpha = capped ? ALPHA_CAP_F : araw;
-        // the terminating slot (k == nw - 1 of a terminated walk) is never blended
-        const bool blended = alpha >= ALPHA_MIN_F && k < nw - (nwt & 1);
-        const float4 w = sPA[p];
-        float dlda = 0.f;
-        if (blended) {
-          const float wc = w.x * cr + w.y * cg + w.z * cbl;
-          const float aT = alpha * T;
-          g0 = fmaf(aT, w.x, g0);
-          g1 = fmaf(aT, w.y, g1);
-          g2 = fmaf(aT, w.z, g2);
-          const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
-          const float awc = aT * wc;
-          const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
-          dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
-          H += awc;
-          T = __fmul_rn(T, one_m);
-        }
-        if (!capped) {
-          float gs = dlda;
-          if (use_soft) {
-            const float sv = soft_sigmoid(alpha);
-            gs = fmaf(w.w * sv * (1.f - sv), 100.f, gs);
-          }
-          g3 = fmaf(gs, alpha, g3);
-          if (blended) {
-            const float gp = dlda * alpha;
-            g4 = fmaf(gp, ca * dx + cb * dy, g4);
-            g5 = fmaf(gp, cb * dx + cc * dy, g5);
-            g6 = fmaf(gp, dxx, g6);
-            g7 = fmaf(gp, dxy, g7);
-            g8 = fmaf(gp, dyy, g8);
-          }
-        }
-      }
-    }
+    BwAcc g = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (use_soft)
+      bw_stream<true>(sPA, sPB, sList[warp], mySeed, n_live, lane, k, s, g);
+    else
+      bw_stream<false>(sPA, sPB, sList[warp], mySeed, n_live, lane, k, s, g);
     if (live) {
       float* r = rows + (size_t)orow * 9;
-      r[0] = g0;
-      r[1] = g1;
-      r[2] = g2;
-      r[3] = g3 * (1.f - opa);
-      r[4] = g4;
-      r[5] = g5;
-      r[6] = -0.5f * g6;
-      r[7] = -g7;
-      r[8] = -0.5f * g8;
+      r[0] = g.g0;
+      r[1] = g.g1;
+      r[2] = g.g2;
+      r[3] = g.g3 * (1.f - s.opa);
+      r[4] = ca * g.sx + cb * g.sy;
+      r[5] = cb * g.sx + cc * g.sy;
+      r[6] = -0.5f * g.g6;
+      r[7] = -g.g7;
+      r[8] = -0.5f * g.g8;
     }
     __syncwarp();
   }
