@@ -43,6 +43,7 @@ def _args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", type=int, default=0, help="1: chain + Adam in one pass (backward_and_step)")
     return ap.parse_args()
 
 
@@ -203,7 +204,7 @@ def main():
     from paper_2503_13086_b200.losses import LossWeights, total_loss
     from paper_2503_13086_b200.optim import FieldOptimizer
     from paper_2503_13086_b200.rasterize import backward, render
-    from paper_2503_13086_b200.rasterize.backward import FieldGrads
+    from paper_2503_13086_b200.rasterize.backward import FieldGrads, backward_and_step
     from paper_2503_13086_b200.train import TrainState, allreduce_grads
 
     rank, world, local = _dist()
@@ -234,9 +235,12 @@ def main():
             allreduce_grads(grads.flat)
             state.stats[:n] += grads.screen_norms
             state.stats[n:] += grads.visible_count
+        elif args.fused:
+            backward_and_step(state.field, out, br.d_image, br.d_soft, state.optimizer, rate, stats=state.stats)
         else:
             grads = backward(state.field, out, br.d_image, br.d_soft, stats=state.stats)
-        state.optimizer.step(state.field, grads, position_rate=rate)
+        if world > 1 or not args.fused:
+            state.optimizer.step(state.field, grads, position_rate=rate)
         state.global_iteration += 1
         return br
 

@@ -55,7 +55,7 @@ typedef struct ssr_camera {
 typedef struct ssr_splats {
   double* mean;        /* N x 2  projected mean (u, v), fp64 */
   float* conic_opa;    /* N x 4  (conic a, b, c, opacity), fp32 */
-  float* color;        /* N x 4  clamped SH colour (r, g, b, 0), fp32 */
+  float* color;        /* N x 4  clamped SH colour (r, g, b), .w = int bits: channel c not clamped */
   double* conic_opa64; /* N x 4  fp64 copies for the guard-band fix-up */
   double* color64;     /* N x 4 */
   double* depth;       /* N      camera-space z, fp64 */
@@ -149,7 +149,7 @@ int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* i
                  const float* d_soft, float* inst_rows, void* stream);
 
 /* backward.py:110-259 + sh.py:135-152: merge rows per splat (bincount
- * order) and chain through projection/SH in fp64.  grads is the flat
+ * order) and chain through projection/SH in fp32 (ssr_chain.cu).  grads is the flat
  * FieldGrads buffer [pos 3N | rot 4N | logscale 3N | logit N | sh 3KN |
  * screen_norm N | visible N].  accumulate!=0 adds into it (view batches);
  * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible.

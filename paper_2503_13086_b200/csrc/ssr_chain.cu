@@ -1,0 +1,672 @@
+// Stage 4 gradient chain (rasterize/backward.py:110-259, sh.py:68-152) in
+// float32: merge each splat's instance rows (bincount order), chain d_mu /
+// d_conic through the EWA projection into position, rotation and log-scale,
+// and d_colour through the SH evaluation into the coefficients and position.
+//
+// The preprocess (ssr_project.cu) must reproduce the reference's fp64 culling,
+// rects and depth order bit for bit, so it runs in float64; the chain only has
+// to meet the 1e-3 relative-L2 gradient bar, so it runs in float32 (~1e-6
+// relative), which halves its registers and lets it stream at HBM rate.
+//
+// Two kernels per call:
+//  * k_chain_geo: one thread per field row, 128 rows per CTA; the CTA's rows
+//    own one contiguous range of inst_rows (field-row order), staged into
+//    shared memory by one TMA bulk copy.  Writes the geometric gradients and
+//    parks the merged colour gradient (and, fused, the geometric position
+//    gradient) in the row's first instance row for the SH kernel.
+//  * k_chain_sh: four lanes per row, each owning a quarter of every colour
+//    channel's coefficients, read and written as coalesced float4 streams
+//    straight from HBM (no shared-memory transpose); channel sums and the
+//    direction gradient are reduced over the four lanes with shuffles.
+// FUSED (ssr_chain_adam) applies the dense Adam step in place instead of
+// writing FieldGrads: the gradient buffer's write and read disappear.
+#include "ssr_common.cuh"
+
+namespace ssr {
+
+constexpr unsigned FULLMASK = 0xffffffffu;
+
+struct CamF {
+  float R[9], t[3], fx, fy, center[3];
+  int width, height;
+};
+
+static CamF to_camf(const ssr_camera& c) {
+  CamF o;
+  for (int i = 0; i < 9; i++) o.R[i] = (float)c.R[i];
+  for (int i = 0; i < 3; i++) {
+    o.t[i] = (float)c.t[i];
+    o.center[i] = (float)c.center[i];
+  }
+  o.fx = (float)c.fx;
+  o.fy = (float)c.fy;
+  o.width = c.width;
+  o.height = c.height;
+  return o;
+}
+
+// Adam of optim.py:40-47 for one element (same expression as k_adam).
+struct AdamClassF {
+  float lr, ib1, ib2;
+};
+struct AdamArgsF {
+  AdamClassF c[6];  // pos, rot, scale, opacity, sh dc, sh rest
+  float* m;
+  float* v;
+};
+__device__ __forceinline__ float adam_step(float p, float g, float& m, float& v, const AdamClassF& c) {
+  return adam_update(p, g, m, v, c.lr, c.ib1, c.ib2);
+}
+
+// ------------------------------------------------------------------ merge of large splats
+// Rows of Gaussians touching more than MERGE_BIG tiles (large splats, up to
+// thousands of tiles) are summed by a whole warp -- coalesced strided loads,
+// fixed-order tree reduction -- into the Gaussian's first row, so the chain's
+// per-thread merge stays bounded.  One warp per 32 rows.
+constexpr uint32_t MERGE_BIG = 32;
+
+__global__ void __launch_bounds__(256) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
+                                                   const uint32_t* __restrict__ roff, float* __restrict__ rows) {
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
+  const int lane = threadIdx.x & 31;
+  if (g0 >= n) return;
+  const int64_t gi = g0 + lane;
+  const uint32_t mine = gi < n ? tiles[gi] : 0u;
+  unsigned big = __ballot_sync(FULLMASK, mine > MERGE_BIG);
+  while (big) {
+    const int l = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t nt = __shfl_sync(FULLMASK, mine, l);
+    float* rw = rows + (int64_t)roff[g0 + l] * 9;
+    float acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t j = lane; j < nt; j += 32)
+#pragma unroll
+      for (int c = 0; c < 9; c++) acc[c] += rw[(int64_t)j * 9 + c];
+#pragma unroll
+    for (int c = 0; c < 9; c++)
+      for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(FULLMASK, acc[c], o);
+    __syncwarp();
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < 9; c++) rw[c] = acc[c];
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ geometry chain
+constexpr int CHAIN_ROWS = 128;
+constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
+
+template <bool FUSED>
+__global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
+                                                          float* __restrict__ rot, float* __restrict__ ls,
+                                                          float* __restrict__ logit_p,
+                                                          const uint32_t* __restrict__ tiles,
+                                                          const uint32_t* __restrict__ roff, float* __restrict__ rows,
+                                                          float* __restrict__ grads, int S, int accumulate,
+                                                          float* __restrict__ stats, AdamArgsF adam) {
+  __shared__ __align__(16) float s_rows[CHAIN_STAGE_FLOATS + 4];
+  __shared__ uint64_t mbar;
+  const int64_t i0 = (int64_t)blockIdx.x * CHAIN_ROWS;
+  const int rows_here = (int)min((int64_t)CHAIN_ROWS, n - i0);
+  const int64_t i = i0 + threadIdx.x;
+  const bool mine = threadIdx.x < rows_here;
+  const uint32_t r_begin = roff[i0];
+  const uint32_t r_end = roff[i0 + rows_here - 1] + tiles[i0 + rows_here - 1];
+  // the CTA's rows are one contiguous range: one 16-byte aligned TMA bulk
+  // copy when it fits (inst_rows has >= 16 B slack), else direct reads
+  const int64_t n_floats = (int64_t)(r_end - r_begin) * 9;
+  const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
+  const int pad = (int)((b0 - a0) >> 2);
+  const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
+  const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  if (staged) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&mbar, (uint32_t)bytes);
+      bulk_g2s(s_rows, reinterpret_cast<const char*>(rows) + a0, (uint32_t)bytes, &mbar);
+    }
+    mbar_wait(&mbar, 0);
+  }
+  if (!mine) return;
+  const uint32_t nt = tiles[i];
+  // bincount merge (backward.py:110-118): ascending tile order; Gaussians with
+  // more than MERGE_BIG rows were reduced into their first row by k_merge_big
+  float pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (nt > 0) {
+    const float* rw = staged ? s_rows + pad + (int64_t)(roff[i] - r_begin) * 9 : rows + (int64_t)roff[i] * 9;
+    const uint32_t nr = nt > MERGE_BIG ? 1u : nt;
+    for (uint32_t j = 0; j < nr; j++)
+#pragma unroll
+      for (int c = 0; c < 9; c++) pr[c] += rw[j * 9 + c];
+  }
+  const int64_t ns = row_stride(n);
+  float* g_pos = grads;
+  float* g_rot = grads + 3 * ns;
+  float* g_ls = grads + 7 * ns;
+  float* g_logit = grads + 10 * ns;
+  float* g_screen = grads + (int64_t)S * ns;
+  float* g_vis = grads + (int64_t)(S + 1) * ns;
+  const float4 q4 = *reinterpret_cast<const float4*>(rot + i * 4);
+  // fused: the rows' moments are loaded up front so their latency overlaps the chain
+  float4 m_rot, v_rot;
+  float m_ls[3], v_ls[3], m_lo = 0.f, v_lo = 0.f;
+  if (FUSED) {
+    m_rot = *reinterpret_cast<const float4*>(adam.m + 3 * ns + i * 4);
+    v_rot = *reinterpret_cast<const float4*>(adam.v + 3 * ns + i * 4);
+    for (int j = 0; j < 3; j++) {
+      m_ls[j] = adam.m[7 * ns + i * 3 + j];
+      v_ls[j] = adam.v[7 * ns + i * 3 + j];
+    }
+    m_lo = adam.m[10 * ns + i];
+    v_lo = adam.v[10 * ns + i];
+  }
+  float grot[4] = {0.f, 0.f, 0.f, 0.f}, dls[3] = {0.f, 0.f, 0.f}, dpos[3] = {0.f, 0.f, 0.f}, screen = 0.f;
+  float* dst = rows + (int64_t)roff[i] * 9;
+  if (nt > 0) {
+    dst[0] = pr[0];
+    dst[1] = pr[1];
+    dst[2] = pr[2];
+
+    // ---- forward quantities of projection.py:76-128 (float32 restatement)
+    const float px = pos[i * 3], py = pos[i * 3 + 1], pz = pos[i * 3 + 2];
+    const float* R = cam.R;
+    const float x = R[0] * px + R[1] * py + R[2] * pz + cam.t[0];
+    const float y = R[3] * px + R[4] * py + R[5] * pz + cam.t[1];
+    const float z = R[6] * px + R[7] * py + R[8] * pz + cam.t[2];
+    const float fx = cam.fx, fy = cam.fy;
+    const float limx = 1.3f * ((float)cam.width / (2.f * fx)), limy = 1.3f * ((float)cam.height / (2.f * fy));
+    const float iz = 1.f / z;
+    const float txr = x * iz, tyr = y * iz;
+    const float mulx = (txr > -limx && txr < limx) ? 1.f : 0.f;
+    const float muly = (tyr > -limy && tyr < limy) ? 1.f : 0.f;
+    const float txc = fminf(fmaxf(txr, -limx), limx), tyc = fminf(fmaxf(tyr, -limy), limy);
+    // field.py:40-75: R(q) from the normalised quaternion, M = R diag(e^s)
+    const float qnorm = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+    const float iq = 1.f / qnorm;
+    const float qw = q4.x * iq, qx = q4.y * iq, qy = q4.z * iq, qz = q4.w * iq;
+    float rm[9];
+    rm[0] = 1.f - 2.f * (qy * qy + qz * qz);
+    rm[1] = 2.f * (qx * qy - qw * qz);
+    rm[2] = 2.f * (qx * qz + qw * qy);
+    rm[3] = 2.f * (qx * qy + qw * qz);
+    rm[4] = 1.f - 2.f * (qx * qx + qz * qz);
+    rm[5] = 2.f * (qy * qz - qw * qx);
+    rm[6] = 2.f * (qx * qz - qw * qy);
+    rm[7] = 2.f * (qy * qz + qw * qx);
+    rm[8] = 1.f - 2.f * (qx * qx + qy * qy);
+    const float sc[3] = {__expf(ls[i * 3]), __expf(ls[i * 3 + 1]), __expf(ls[i * 3 + 2])};
+    float m[9], cw[9], tmp[9], cc[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) m[a * 3 + b] = rm[a * 3 + b] * sc[b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) cw[a * 3 + b] = m[a * 3] * m[b * 3] + m[a * 3 + 1] * m[b * 3 + 1] + m[a * 3 + 2] * m[b * 3 + 2];
+    // cc = R cw R^T
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) tmp[a * 3 + b] = R[a * 3] * cw[b] + R[a * 3 + 1] * cw[3 + b] + R[a * 3 + 2] * cw[6 + b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) cc[a * 3 + b] = tmp[a * 3] * R[b * 3] + tmp[a * 3 + 1] * R[b * 3 + 1] + tmp[a * 3 + 2] * R[b * 3 + 2];
+    const float fx_z = fx * iz, fy_z = fy * iz;
+    const float j02 = -fx * txc * iz, j12 = -fy * tyc * iz;
+    const float A = fx_z * (fx_z * cc[0] + j02 * cc[2]) + j02 * (fx_z * cc[2] + j02 * cc[8]) + 0.3f;
+    const float B = fx_z * (fy_z * cc[1] + j12 * cc[2]) + j02 * (fy_z * cc[5] + j12 * cc[8]);
+    const float C = fy_z * (fy_z * cc[4] + j12 * cc[5]) + j12 * (fy_z * cc[5] + j12 * cc[8]) + 0.3f;
+    const float idet = 1.f / (A * C - B * B);
+    const float qa = C * idet, qb = -B * idet, qc = A * idet;
+
+    // ---- backward.py:502-515: conic -> V2, g_v2 = -Q G Q
+    const float g00 = pr[6], g01 = 0.5f * pr[7], g11 = pr[8];
+    const float t00 = qa * g00 + qb * g01, t01 = qa * g01 + qb * g11;
+    const float t10 = qb * g00 + qc * g01, t11 = qb * g01 + qc * g11;
+    const float gv2[4] = {-(t00 * qa + t01 * qb), -(t00 * qb + t01 * qc), -(t10 * qa + t11 * qb),
+                          -(t10 * qb + t11 * qc)};
+    const float J[6] = {fx_z, 0.f, j02, 0.f, fy_z, j12};
+    // gJ = 2 gv2 J cc ; gv3 = J^T gv2 J
+    float jc[6];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) jc[a * 3 + l] = J[a * 3] * cc[l] + J[a * 3 + 1] * cc[3 + l] + J[a * 3 + 2] * cc[6 + l];
+    float gJ[6];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) gJ[a * 3 + l] = 2.f * (gv2[a * 2] * jc[l] + gv2[a * 2 + 1] * jc[3 + l]);
+    float gj[6];  // gv2 J
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) gj[a * 3 + l] = gv2[a * 2] * J[l] + gv2[a * 2 + 1] * J[3 + l];
+    float gv3[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) gv3[a * 3 + l] = J[a] * gj[l] + J[3 + a] * gj[3 + l];
+    // gw = R^T gv3 R
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) tmp[a * 3 + l] = R[a] * gv3[l] + R[3 + a] * gv3[3 + l] + R[6 + a] * gv3[6 + l];
+    float gw[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int l = 0; l < 3; l++) gw[a * 3 + l] = tmp[a * 3] * R[l] + tmp[a * 3 + 1] * R[3 + l] + tmp[a * 3 + 2] * R[6 + l];
+    // backward.py:537-553: J and the projected mean -> camera point -> world
+    const float iz2 = iz * iz;
+    float dcx = gJ[2] * (-fx * mulx * iz2);
+    float dcy = gJ[5] * (-fy * muly * iz2);
+    float dcz = gJ[0] * (-fx * iz2) + gJ[4] * (-fy * iz2) + gJ[2] * fx * (mulx * x * iz + txc) * iz2 +
+                gJ[5] * fy * (muly * y * iz + tyc) * iz2;
+    dcx += pr[4] * fx * iz;
+    dcy += pr[5] * fy * iz;
+    dcz += -pr[4] * fx * x * iz2 - pr[5] * fy * y * iz2;
+    dpos[0] = dcx * R[0] + dcy * R[3] + dcz * R[6];
+    dpos[1] = dcx * R[1] + dcy * R[4] + dcz * R[7];
+    dpos[2] = dcx * R[2] + dcy * R[5] + dcz * R[8];
+    // _cov_to_rotation_scale (backward.py:562-612)
+    float gs[9], dm[9], drot[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) gs[a * 3 + b] = gw[a * 3 + b] + gw[b * 3 + a];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        dm[a * 3 + k] = gs[a * 3] * m[k] + gs[a * 3 + 1] * m[3 + k] + gs[a * 3 + 2] * m[6 + k];
+        drot[a * 3 + k] = dm[a * 3 + k] * sc[k];
+      }
+#pragma unroll
+    for (int j = 0; j < 3; j++) dls[j] = (dm[j] * rm[j] + dm[3 + j] * rm[3 + j] + dm[6 + j] * rm[6 + j]) * sc[j];
+    const float dqw = 2.f * (-qz * drot[1] + qy * drot[2] + qz * drot[3] - qx * drot[5] - qy * drot[6] + qx * drot[7]);
+    const float dqx = 2.f * (qy * drot[1] + qz * drot[2] + qy * drot[3] - 2.f * qx * drot[4] - qw * drot[5] +
+                             qz * drot[6] + qw * drot[7] - 2.f * qx * drot[8]);
+    const float dqy = 2.f * (-2.f * qy * drot[0] + qx * drot[1] + qw * drot[2] + qx * drot[3] + qz * drot[5] -
+                             qw * drot[6] + qz * drot[7] - 2.f * qy * drot[8]);
+    const float dqz = 2.f * (-2.f * qz * drot[0] - qw * drot[1] + qx * drot[2] + qw * drot[3] - 2.f * qz * drot[4] +
+                             qy * drot[5] + qx * drot[6] + qy * drot[7]);
+    const float rad = dqw * qw + dqx * qx + dqy * qy + dqz * qz;
+    grot[0] = (dqw - rad * qw) * iq;
+    grot[1] = (dqx - rad * qx) * iq;
+    grot[2] = (dqy - rad * qy) * iq;
+    grot[3] = (dqz - rad * qz) * iq;
+    screen = sqrtf(pr[4] * pr[4] + pr[5] * pr[5]) * (0.5f * (float)max(cam.width, cam.height));
+  }  // visible
+  const bool vis = nt > 0;
+  if (FUSED) {
+    // dense Adam: invisible rows step with a zero gradient like the reference
+    float4 qn;
+    qn.x = adam_step(q4.x, grot[0], m_rot.x, v_rot.x, adam.c[1]);
+    qn.y = adam_step(q4.y, grot[1], m_rot.y, v_rot.y, adam.c[1]);
+    qn.z = adam_step(q4.z, grot[2], m_rot.z, v_rot.z, adam.c[1]);
+    qn.w = adam_step(q4.w, grot[3], m_rot.w, v_rot.w, adam.c[1]);
+    *reinterpret_cast<float4*>(rot + i * 4) = qn;
+    *reinterpret_cast<float4*>(adam.m + 3 * ns + i * 4) = m_rot;
+    *reinterpret_cast<float4*>(adam.v + 3 * ns + i * 4) = v_rot;
+    for (int j = 0; j < 3; j++) {
+      ls[i * 3 + j] = adam_step(ls[i * 3 + j], dls[j], m_ls[j], v_ls[j], adam.c[2]);
+      adam.m[7 * ns + i * 3 + j] = m_ls[j];
+      adam.v[7 * ns + i * 3 + j] = v_ls[j];
+    }
+    logit_p[i] = adam_step(logit_p[i], pr[3], m_lo, v_lo, adam.c[3]);
+    adam.m[10 * ns + i] = m_lo;
+    adam.v[10 * ns + i] = v_lo;
+    if (vis) {
+      dst[3] = dpos[0];
+      dst[4] = dpos[1];
+      dst[5] = dpos[2];
+    }
+  } else if (accumulate) {
+    if (vis) {
+      for (int j = 0; j < 3; j++) g_pos[i * 3 + j] += dpos[j];
+      for (int j = 0; j < 4; j++) g_rot[i * 4 + j] += grot[j];
+      for (int j = 0; j < 3; j++) g_ls[i * 3 + j] += dls[j];
+      g_logit[i] += pr[3];
+      g_screen[i] += screen;
+      g_vis[i] += 1.f;
+    }
+  } else {
+    for (int j = 0; j < 3; j++) g_pos[i * 3 + j] = dpos[j];
+    *reinterpret_cast<float4*>(g_rot + i * 4) = make_float4(grot[0], grot[1], grot[2], grot[3]);
+    for (int j = 0; j < 3; j++) g_ls[i * 3 + j] = dls[j];
+    g_logit[i] = pr[3];
+    g_screen[i] = screen;
+    g_vis[i] = vis ? 1.f : 0.f;
+  }
+  if (stats && vis) {
+    stats[i] += screen;
+    stats[n + i] += 1.f;
+  }
+}
+
+// ------------------------------------------------------------------ SH chain
+// sh.py:36-65 basis in float32.
+template <int DEG>
+__device__ __forceinline__ void sh_basis32(float x, float y, float z, float* b) {
+  b[0] = 0.28209479177387814f;
+  if (DEG >= 1) {
+    b[1] = -0.4886025119029199f * y;
+    b[2] = 0.4886025119029199f * z;
+    b[3] = -0.4886025119029199f * x;
+  }
+  if (DEG >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    b[4] = 1.0925484305920792f * (x * y);
+    b[5] = -1.0925484305920792f * (y * z);
+    b[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+    b[7] = -1.0925484305920792f * (x * z);
+    b[8] = 0.5462742152960396f * (xx - yy);
+    if (DEG >= 3) {
+      b[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+      b[10] = 2.890611442640554f * (x * y) * z;
+      b[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+      b[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      b[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+      b[14] = 1.445305721320277f * z * (xx - yy);
+      b[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+    }
+  }
+}
+
+// sum_k v_k dY_k/ddir (sh.py:68-111), written term by term.
+template <int DEG>
+__device__ __forceinline__ void sh_dir_grad32(const float* v, float x, float y, float z, float* g) {
+  const float C1 = 0.4886025119029199f;
+  g[0] = g[1] = g[2] = 0.f;
+  if (DEG >= 1) {
+    g[1] += v[1] * (-C1);
+    g[2] += v[2] * C1;
+    g[0] += v[3] * (-C1);
+  }
+  if (DEG >= 2) {
+    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+                C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+    g[0] += v[4] * (C20 * y) + v[6] * (C22 * (-2.f * x)) + v[7] * (C23 * z) + v[8] * (C24 * (2.f * x));
+    g[1] += v[4] * (C20 * x) + v[5] * (C21 * z) + v[6] * (C22 * (-2.f * y)) + v[8] * (C24 * (-2.f * y));
+    g[2] += v[5] * (C21 * y) + v[6] * (C22 * (4.f * z)) + v[7] * (C23 * x);
+  }
+  if (DEG >= 3) {
+    const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+                C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                C36 = -0.5900435899266435f;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    g[0] += v[9] * (C30 * 6.f * x * y) + v[10] * (C31 * y * z) + v[11] * (C32 * (-2.f * x * y)) +
+            v[12] * (C33 * (-6.f * x * z)) + v[13] * (C34 * (4.f * zz - 3.f * xx - yy)) +
+            v[14] * (C35 * (2.f * x * z)) + v[15] * (C36 * (3.f * xx - 3.f * yy));
+    g[1] += v[9] * (C30 * (3.f * xx - 3.f * yy)) + v[10] * (C31 * x * z) + v[11] * (C32 * (4.f * zz - xx - 3.f * yy)) +
+            v[12] * (C33 * (-6.f * y * z)) + v[13] * (C34 * (-2.f * x * y)) + v[14] * (C35 * (-2.f * y * z)) +
+            v[15] * (C36 * (-6.f * x * y));
+    g[2] += v[10] * (C31 * x * y) + v[11] * (C32 * (8.f * y * z)) + v[12] * (C33 * (6.f * zz - 3.f * xx - 3.f * yy)) +
+            v[13] * (C34 * (8.f * x * z)) + v[14] * (C35 * (xx - yy));
+  }
+}
+
+constexpr int SH_LANES = 4;
+constexpr int SH_THREADS = 256;
+constexpr int SH_ROWS = SH_THREADS / SH_LANES;
+
+// Lane q of a row owns coefficients k = q*KL + j (j < KL, k < K) of every
+// channel; at SH3 that is one float4 per channel, read and written directly.
+template <int DEG, bool FUSED>
+__global__ void __launch_bounds__(SH_THREADS) k_chain_sh(CamF cam, int64_t n, float* __restrict__ pos,
+                                                         float* __restrict__ sh, const uint32_t* __restrict__ tiles,
+                                                         const uint32_t* __restrict__ roff,
+                                                         const float4* __restrict__ color,
+                                                         const float* __restrict__ rows, float* __restrict__ grads,
+                                                         int accumulate, AdamArgsF adam) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int W = 3 * K;
+  constexpr int KL = (K + 3) / 4;
+  constexpr bool VEC = (K == 16);
+  const int64_t i = (int64_t)blockIdx.x * SH_ROWS + (threadIdx.x >> 2);
+  const int q = threadIdx.x & 3;
+  const bool row_ok = i < n;
+  const int64_t ii = row_ok ? i : n - 1;  // out-of-range lanes shadow the last row (shuffles need them)
+  const int64_t ns = row_stride(n);
+  const bool vis = row_ok && tiles[ii] != 0;
+  const float* rw = rows + (vis ? (int64_t)roff[ii] * 9 : 0);
+  float* shrow = sh + ii * W;
+  float* grow = FUSED ? nullptr : grads + 11 * ns + ii * W;
+
+  // the lane's coefficients: c[ch][j] = sh[ch*K + q*KL + j]
+  float cf[3][KL];
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    if (VEC) {
+      const float4 v4 = *reinterpret_cast<const float4*>(shrow + ch * K + q * 4);
+      cf[ch][0] = v4.x;
+      cf[ch][1] = v4.y;
+      cf[ch][2] = v4.z;
+      cf[ch][3] = v4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < KL; j++) {
+        const int k = q * KL + j;
+        cf[ch][j] = k < K ? shrow[ch * K + k] : 0.f;
+      }
+    }
+  }
+  // fused: the lane's moments (and lane 0's position moments) loaded up front
+  float mf[3][KL], vf[3][KL];
+  float mp[3] = {0.f, 0.f, 0.f}, vp[3] = {0.f, 0.f, 0.f};
+  if (FUSED) {
+    const float* mrow = adam.m + 11 * ns + ii * W;
+    const float* vrow = adam.v + 11 * ns + ii * W;
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+      if (VEC) {
+        const float4 a4 = *reinterpret_cast<const float4*>(mrow + ch * K + q * 4);
+        const float4 b4 = *reinterpret_cast<const float4*>(vrow + ch * K + q * 4);
+        mf[ch][0] = a4.x, mf[ch][1] = a4.y, mf[ch][2] = a4.z, mf[ch][3] = a4.w;
+        vf[ch][0] = b4.x, vf[ch][1] = b4.y, vf[ch][2] = b4.z, vf[ch][3] = b4.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < KL; j++) {
+          const int k = q * KL + j;
+          mf[ch][j] = k < K ? mrow[ch * K + k] : 0.f;
+          vf[ch][j] = k < K ? vrow[ch * K + k] : 0.f;
+        }
+      }
+    }
+    if (q == 0)
+      for (int d = 0; d < 3; d++) {
+        mp[d] = adam.m[ii * 3 + d];
+        vp[d] = adam.v[ii * 3 + d];
+      }
+  }
+  // direction (sh.py:114-124), recomputed by each lane
+  const float ox = pos[ii * 3] - cam.center[0], oy = pos[ii * 3 + 1] - cam.center[1],
+              oz = pos[ii * 3 + 2] - cam.center[2];
+  const float r = sqrtf(ox * ox + oy * oy + oz * oz);
+  const float rs = fmaxf(r, 1e-12f);
+  const float irs = 1.f / rs;
+  const float dx = ox * irs, dy = oy * irs, dz = oz * irs;
+  float basis[16];
+  sh_basis32<DEG>(dx, dy, dz, basis);
+  float bown[KL];  // basis of the lane's coefficients
+#pragma unroll
+  for (int j = 0; j < KL; j++) {
+    float b = 0.f;
+#pragma unroll
+    for (int qq = 0; qq < 4; qq++)
+      if (qq * KL + j < K) b = (q == qq) ? basis[qq * KL + j] : b;
+    bown[j] = (q * KL + j < K) ? b : 0.f;
+  }
+  // colour gradient through the clamp (sh.py:128-131); the masks were decided
+  // by the float64 preprocess (colour .w bits), not re-derived in fp32
+  float dcol[3] = {0.f, 0.f, 0.f};
+  if (vis) {
+    const int pass = __float_as_int(color[ii].w);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) dcol[ch] = (pass >> ch) & 1 ? rw[ch] : 0.f;
+  }
+  // direction gradient: v_k = sum_c dcol_c coeff_ck for the lane's k (zero
+  // elsewhere), contracted with dY/ddir, reduced over the 4 lanes
+  float vfull[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) vfull[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const int qq = k / KL, j = k % KL;
+    const float vk = dcol[0] * cf[0][j] + dcol[1] * cf[1][j] + dcol[2] * cf[2][j];
+    vfull[k] = (q == qq) ? vk : 0.f;
+  }
+  float gd[3];
+  sh_dir_grad32<DEG>(vfull, dx, dy, dz, gd);
+#pragma unroll
+  for (int d = 0; d < 3; d++) {
+    gd[d] += __shfl_xor_sync(FULLMASK, gd[d], 1);
+    gd[d] += __shfl_xor_sync(FULLMASK, gd[d], 2);
+  }
+  const float radial = gd[0] * dx + gd[1] * dy + gd[2] * dz;
+  const float dpos_sh[3] = {(gd[0] - radial * dx) * irs, (gd[1] - radial * dy) * irs, (gd[2] - radial * dz) * irs};
+  if (!row_ok) return;
+
+  if (FUSED) {
+    // positions: geometric part from the geometry kernel + view-direction part
+    if (q == 0) {
+      for (int d = 0; d < 3; d++) {
+        const float g = vis ? rw[3 + d] + dpos_sh[d] : 0.f;
+        const int64_t e = i * 3 + d;
+        pos[e] = adam_step(pos[e], g, mp[d], vp[d], adam.c[0]);
+        adam.m[e] = mp[d];
+        adam.v[e] = vp[d];
+      }
+    }
+    float* mrow = adam.m + 11 * ns + i * W;
+    float* vrow = adam.v + 11 * ns + i * W;
+    const AdamClassF c_dc = adam.c[4], c_rest = adam.c[5];
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+      float pn[KL];
+#pragma unroll
+      for (int j = 0; j < KL; j++)
+        pn[j] = adam_step(cf[ch][j], dcol[ch] * bown[j], mf[ch][j], vf[ch][j], (q * KL + j == 0) ? c_dc : c_rest);
+      if (VEC) {
+        *reinterpret_cast<float4*>(shrow + ch * K + q * 4) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+        *reinterpret_cast<float4*>(mrow + ch * K + q * 4) = make_float4(mf[ch][0], mf[ch][1], mf[ch][2], mf[ch][3]);
+        *reinterpret_cast<float4*>(vrow + ch * K + q * 4) = make_float4(vf[ch][0], vf[ch][1], vf[ch][2], vf[ch][3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < KL; j++) {
+          const int k = q * KL + j;
+          if (k < K) {
+            shrow[ch * K + k] = pn[j];
+            mrow[ch * K + k] = mf[ch][j];
+            vrow[ch * K + k] = vf[ch][j];
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (q == 0 && vis) {
+    float* g_pos = grads + i * 3;
+#pragma unroll
+    for (int d = 0; d < 3; d++) g_pos[d] += dpos_sh[d];
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    if (VEC) {
+      float4 g4 = make_float4(dcol[ch] * bown[0], dcol[ch] * bown[1], dcol[ch] * bown[2], dcol[ch] * bown[3]);
+      float4* dstp = reinterpret_cast<float4*>(grow + ch * K + q * 4);
+      if (accumulate) {
+        const float4 o = *dstp;
+        g4.x += o.x;
+        g4.y += o.y;
+        g4.z += o.z;
+        g4.w += o.w;
+      }
+      *dstp = g4;
+    } else {
+#pragma unroll
+      for (int j = 0; j < KL; j++) {
+        const int k = q * KL + j;
+        if (k < K) {
+          const float g = dcol[ch] * bown[j];
+          grow[ch * K + k] = accumulate ? grow[ch * K + k] + g : g;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace ssr
+
+using namespace ssr;
+
+template <bool FUSED>
+static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* positions, float* rotations,
+                        float* log_scales, float* logits, float* sh, ssr_splats splats, float* rows, float* grads,
+                        int32_t accumulate, float* stats, const AdamArgsF& adam, cudaStream_t st) {
+  const CamF c = to_camf(*cam);
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  k_merge_big<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
+  SSR_TRY(check_launch("k_merge_big"));
+  const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
+  k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, 0, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
+                                                    splats.row_offset, rows, grads, 11 + 3 * K, accumulate, stats,
+                                                    adam);
+  SSR_TRY(check_launch("k_chain_geo"));
+  const unsigned sblocks = (unsigned)((n + SH_ROWS - 1) / SH_ROWS);
+#define SSR_SH(D)                                                                                       \
+  k_chain_sh<D, FUSED><<<sblocks, SH_THREADS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, \
+                                                        (const float4*)splats.color, rows, grads, accumulate, adam)
+  switch (sh_degree) {
+    case 0: SSR_SH(0); break;
+    case 1: SSR_SH(1); break;
+    case 2: SSR_SH(2); break;
+    default: SSR_SH(3); break;
+  }
+#undef SSR_SH
+  return check_launch("k_chain_sh");
+}
+
+extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
+                         const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
+                         const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream) {
+  if (!cam || n < 0 || sh_degree < 0 || sh_degree > 3 || !grads) {
+    set_error("ssr_chain: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  if (n == 0) return SSR_OK;
+  AdamArgsF none{};
+  // inst_rows is scratch from here on: the geometry pass parks each Gaussian's
+  // merged colour gradient in its own first row for the SH pass
+  return launch_chain<false>(cam, n, sh_degree, const_cast<float*>(positions), const_cast<float*>(rotations),
+                             const_cast<float*>(log_scales), nullptr, const_cast<float*>(sh), splats,
+                             const_cast<float*>(inst_rows), grads, accumulate, stats, none, (cudaStream_t)stream);
+}
+
+extern "C" int ssr_chain_adam(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* params, float* m, float* v,
+                              ssr_splats splats, float* inst_rows, float* stats, const double* lr, double lr_sh_rest,
+                              const double* bc1, const double* bc2, void* stream) {
+  if (!cam || n < 0 || sh_degree < 0 || sh_degree > 3 || !params || !m || !v || !lr || !bc1 || !bc2) {
+    set_error("ssr_chain_adam: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  if (n == 0) return SSR_OK;
+  AdamArgsF adam;
+  for (int c = 0; c < 5; c++) {
+    adam.c[c].lr = (float)lr[c];
+    adam.c[c].ib1 = (float)(1.0 / bc1[c]);
+    adam.c[c].ib2 = (float)(1.0 / bc2[c]);
+  }
+  adam.c[5] = adam.c[4];
+  adam.c[5].lr = (float)lr_sh_rest;
+  adam.m = m;
+  adam.v = v;
+  const int64_t ns = row_stride(n);
+  return launch_chain<true>(cam, n, sh_degree, params, params + 3 * ns, params + 7 * ns, params + 10 * ns,
+                            params + 11 * ns, splats, inst_rows, nullptr, 0, stats, adam, (cudaStream_t)stream);
+}

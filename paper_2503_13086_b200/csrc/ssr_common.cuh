@@ -428,4 +428,19 @@ __device__ __forceinline__ float soft_sigmoid(float alpha) {
   return __fdividef(1.0f, 1.0f + e);
 }
 
+// Adam of optim.py:40-47 for one float32 element: m, v updated in place,
+// returns the new parameter.  sqrt.approx (MUFU, 2^-22 relative) keeps v = 0
+// (rows never seen) off the IEEE sqrt's special-case path.  Shared by k_adam
+// and the fused chain so both paths round identically.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float adam_update(float p, float g, float& m, float& v, float lr, float ib1, float ib2) {
+  m = __fmaf_rn(0.9f, m, 0.1f * g);
+  v = __fmaf_rn(0.999f, v, 0.001f * g * g);
+  return p - __fdividef(lr * (m * ib1), sqrt_approx(v * ib2) + 1e-15f);
+}
+
 }  // namespace ssr

@@ -29,9 +29,7 @@ constexpr int ADAM_PER_THREAD = 8;  // two float4 per thread
 constexpr int64_t ADAM_PER_BLOCK = (int64_t)ADAM_THREADS * ADAM_PER_THREAD;
 
 __device__ __forceinline__ float adam_one(float p, float g, float& m, float& v, float lr, float ib1, float ib2) {
-  m = __fmaf_rn(0.9f, m, 0.1f * g);
-  v = __fmaf_rn(0.999f, v, 0.001f * g * g);
-  return p - __fdividef(lr * (m * ib1), sqrtf(v * ib2) + 1e-15f);
+  return adam_update(p, g, m, v, lr, ib1, ib2);
 }
 
 template <int K>

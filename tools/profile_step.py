@@ -27,7 +27,12 @@ for _ in range(iters):
     out = render(f, cam)
     w = LossWeights() if os.environ.get("SSR_WEIGHTS") == "paper" else LossWeights(l1=1.0, ssim=0.2, load=0.0)
     br = total_loss(out.image, target, out, w)
-    g = backward(f, out, br.d_image, br.d_soft)
-    opt.step(f, g, position_rate=1.6e-4)
+    if os.environ.get("SSR_FUSED") == "1":
+        from paper_2503_13086_b200.rasterize.backward import backward_and_step
+
+        backward_and_step(f, out, br.d_image, br.d_soft, opt, 1.6e-4)
+    else:
+        g = backward(f, out, br.d_image, br.d_soft)
+        opt.step(f, g, position_rate=1.6e-4)
 torch.cuda.synchronize()
 print("flagged", int(out.flagged.sum()), "P", int(out.n_walk.sum()), "M", out.splats.n_instances)
