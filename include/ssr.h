@@ -77,11 +77,13 @@ typedef struct ssr_frame {
   int32_t* hard_count; /* H x W */
   double* soft_count;  /* H x W  float64: counts reach 10^4, the bar is 1e-4 absolute */
   uint8_t* flagged;    /* H x W  1 = pixel re-walked in fp64 (guard band) */
-  int32_t* tile_info;  /* n_tiles x 2  (max n_walk, flagged pixel count) */
+  int32_t* tile_info;  /* n_tiles x 4  (max n_walk, flagged pixel count, max n_walk of a flagged pixel, 0) */
   float* ckpt;         /* ssr_ckpt_floats(M, n_tiles) floats: (T, C_front rgb) per bucket/pixel */
   int32_t* fix_list;   /* ssr_fix_list_ints(W, H, n_tiles) int32, written by ssr_forward: [0] flagged
-                        * pixels, [1] flagged tiles, then n_tiles slots (first pixel entry of each
-                        * flagged tile, unordered), then W*H pixel entries (tile << 8 | pixel in tile),
+                        * pixels, [1] flagged tiles, [2] backward fix-up buckets, [3] spare,
+                        * then n_tiles slots (first pixel entry of each
+                        * flagged tile, unordered), n_tiles bucket-plan
+                        * slots, then W*H pixel entries (tile << 8 | pixel in tile),
                         * contiguous per tile and in pixel order within it */
 } ssr_frame;
 

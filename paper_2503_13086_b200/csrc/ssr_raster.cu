@@ -13,6 +13,8 @@
 // gradient rows are added by an fp64 pixel walk (backward fix-up); the fp32
 // backward kernels skip them, so fp32 never has to agree with fp64 near a
 // threshold.
+#include <climits>
+
 #include "ssr_common.cuh"
 
 namespace ssr {
@@ -40,14 +42,21 @@ struct RasterArgs {
   int* hard;
   double* soft;
   uint8_t* flagged;
-  int2* tile_info;
+  int4* tile_info;  // (max n_walk, flagged pixels, max fp64 n_walk of a flagged pixel, first flagged slot)
   float4* ckpt;
-  int* fix;  // fix_list: [0] pixels, [1] tiles, tile slots, pixel entries
+  int* fix;  // fix_list: [0] pixels, [1] tiles, [2] fix-up buckets, [3] spare, tile slots, bucket plan,
+             // pixel entries
   int n_tiles;
 };
 
-__device__ __forceinline__ int* fix_tiles(const RasterArgs& a) { return a.fix + 2; }
-__device__ __forceinline__ int* fix_pixels(const RasterArgs& a) { return a.fix + 2 + a.n_tiles; }
+constexpr int FIX_HEAD = 4;
+__device__ __forceinline__ int* fix_tiles(const RasterArgs& a) { return a.fix + FIX_HEAD; }
+__device__ __forceinline__ int* fix_plan(const RasterArgs& a) { return a.fix + FIX_HEAD + a.n_tiles; }
+__device__ __forceinline__ int* fix_pixels(const RasterArgs& a) { return a.fix + FIX_HEAD + 2 * a.n_tiles; }
+// per pixel (y * W + x): the walk slot of a flagged pixel's first ambiguous decision
+__device__ __forceinline__ int* fix_kflag(const RasterArgs& a) {
+  return a.fix + FIX_HEAD + 2 * a.n_tiles + (size_t)a.width * a.height;
+}
 
 // Splat-major position of the instance of field row g in tile (tx, ty).
 __device__ __forceinline__ uint32_t inst_row(const RasterArgs& a, uint32_t g, int tx, int ty) {
@@ -123,6 +132,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           if (A.w < 0.f) {
             if (p2 > 1e-6f * qpos && qpos != 0.f) {
               flag = true;
+            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
               break;
             }
             if (p2 > 0.f) {
@@ -140,6 +150,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           }
           if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
             flag = true;
+            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
             break;
           }
           alpha = fminf(alpha, ALPHA_CAP_F);
@@ -149,6 +160,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
           if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
             flag = true;
+            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
             break;
           }
           if (test < T_EPS_F) {
@@ -180,23 +192,34 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
     a.hard[pix] = hard;
     a.soft[pix] = (double)(nwk - nbig) * SOFT_S0 + (sbig + (double)sdev);
     a.flagged[pix] = flag ? 1 : 0;
+    // every decision before the flagged slot was unambiguous, so the fp32
+    // backward handles those slots of a flagged pixel and the fp64 fix-up the rest
+    if (flag) fix_kflag(a)[pix] = nwk;
   }
-  // per-tile (max n_walk over unflagged pixels, flagged count)
+  // per-tile (max n_walk over unflagged pixels, flagged count, first flagged slot)
   int mw = (inside && !flag) ? nwk : 0;
-  for (int o = 16; o > 0; o >>= 1) mw = max(mw, __shfl_xor_sync(FULL, mw, o));
+  int kf = (inside && flag) ? nwk : INT_MAX;
+  for (int o = 16; o > 0; o >>= 1) {
+    mw = max(mw, __shfl_xor_sync(FULL, mw, o));
+    kf = min(kf, __shfl_xor_sync(FULL, kf, o));
+  }
   const bool fl = inside && flag;
   const unsigned fm = __ballot_sync(FULL, fl);
-  __shared__ int sCnt[8];
+  __shared__ int sCnt[8], sKf[8];
   __shared__ int sBase;
   if ((tid & 31) == 0) {
     sMax[tid >> 5] = mw;
     sCnt[tid >> 5] = __popc(fm);
+    sKf[tid >> 5] = kf;
   }
   const int nflag = __syncthreads_count(fl);
   if (tid == 0) {
-    int m = 0;
-    for (int w = 0; w < 8; w++) m = max(m, sMax[w]);
-    a.tile_info[t] = make_int2(m, nflag);
+    int m = 0, kmin = INT_MAX;
+    for (int w = 0; w < 8; w++) {
+      m = max(m, sMax[w]);
+      kmin = min(kmin, sKf[w]);
+    }
+    a.tile_info[t] = make_int4(m, nflag, 0, kmin);
     if (nflag) {  // reserve this tile's block of the compact fix-up lists
       sBase = atomicAdd(&a.fix[0], nflag);
       fix_tiles(a)[atomicAdd(&a.fix[1], 1)] = sBase;
@@ -373,8 +396,10 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
       a.term[pix] = (uint8_t)r.term;
       a.hard[pix] = r.hard;
       a.soft[pix] = r.soft;
-      // tile_info.x stays an upper bound of the tile's n_walk (buckets to visit).
+      // tile_info.x stays an upper bound of the tile's n_walk (buckets to visit);
+      // .z bounds the buckets the backward fix-up visits for this tile
       atomicMax(&a.tile_info[t].x, r.nw);
+      atomicMax(&a.tile_info[t].z, r.nw);
     }
   }
 }
@@ -528,6 +553,8 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       if (!a.flagged[pix]) {
         nw = a.n_walk[pix];
         term = a.term[pix] ? 1 : 0;
+      } else {
+        nw = fix_kflag(a)[pix];  // slots before the ambiguous one; the fp64 fix-up adds the rest
       }
       w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
       wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
@@ -665,6 +692,8 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
     if (!a.flagged[pix]) {
       nw = a.n_walk[pix];
       term = a.term[pix];
+    } else {
+      nw = fix_kflag(a)[pix];  // slots before the ambiguous one; the fp64 fix-up adds the rest
     }
     w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
     wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
@@ -762,72 +791,123 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
 // without atomics, and parallel over buckets.  Backward decisions do not
 // depend on T (termination comes from n_walk / terminated), so fp32 seeds only
 // perturb gradient values, never which slots blend.
-struct FixPix {
-  double w0, w1, w2, ws, wimg;
-  int nw, term, p;
-};
-// Persistent grid, one CTA per flagged tile (compact list from k_forward);
-// warp w takes buckets w, w+8, ...
-__global__ void __launch_bounds__(256) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
-                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
-  __shared__ FixPix sp[TILE_PX];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Buckets of flagged tile slot `it` the backward fix-up visits: from the one
+// holding the tile's first flagged slot to the end of its longest flagged walk.
+__device__ __forceinline__ int fix_tile_buckets(const RasterArgs& a, int it) {
+  const int4 ti = a.tile_info[fix_pixels(a)[fix_tiles(a)[it]] >> 8];
+  return max(0, ((ti.z + 31) >> 5) - (ti.w >> 5));
+}
+
+// Bucket plan of the backward fix-up: exclusive prefix over the flagged tiles
+// of their bucket counts (one CTA; <= n_tiles entries), total in fix[2].
+__global__ void __launch_bounds__(1024) k_fix_plan(RasterArgs a) {
+  __shared__ int s_part[32];
   const int n_ft = a.fix[1];
-  for (int it = blockIdx.x; it < n_ft; it += gridDim.x) {
-    const int start = fix_tiles(a)[it];
-    const int t = fix_pixels(a)[start] >> 8;
-    const int2 info = a.tile_info[t];
-    const int nflag = info.y, nb = (info.x + 31) >> 5;
-    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-    __syncthreads();  // previous tile's sp[] readers are done
-    // Per-pixel inputs, loaded once per tile (shared by the CTA's buckets).
-    if ((int)threadIdx.x < nflag) {
-      const int p = fix_pixels(a)[start + threadIdx.x] & 255;
-      const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
-      const size_t pix = (size_t)py * a.width + px;
-      FixPix q;
-      q.w0 = d_image[pix * 3];
-      q.w1 = d_image[pix * 3 + 1];
-      q.w2 = d_image[pix * 3 + 2];
-      q.ws = d_soft ? (double)d_soft[pix] : 0.0;
-      q.wimg = q.w0 * (double)a.image[pix * 3] + q.w1 * (double)a.image[pix * 3 + 1] +
-               q.w2 * (double)a.image[pix * 3 + 2];
-      q.nw = a.n_walk[pix];
-      q.term = a.term[pix];
-      q.p = p;
-      sp[threadIdx.x] = q;
+  const int per = (n_ft + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(lo + per, n_ft);
+  int sum = 0;
+  for (int it = lo; it < hi; it++) sum += fix_tile_buckets(a, it);
+  // block exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = sum;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(FULL, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_part[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = s_part[lane], vi = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(FULL, vi, d);
+      if (lane >= d) vi += o;
     }
-    __syncthreads();
+    s_part[lane] = vi - v;
+    if (lane == 31) a.fix[2] = vi;
+  }
+  __syncthreads();
+  int run = s_part[warp] + incl - sum;
+  for (int it = lo; it < hi; it++) {
+    fix_plan(a)[it] = run;
+    run += fix_tile_buckets(a, it);
+  }
+}
+
+// Work items are the (flagged tile, bucket) pairs of the plan, strided
+// statically over every warp of a persistent grid (no tile-sized serial
+// chains; deterministic).  A warp loads its bucket's 32 slots and the tile's
+// flagged-pixel inputs (lane f holds pixel f, broadcast by shuffles) in
+// parallel, walks the flagged pixels in pixel order (seeded from the
+// checkpoints the forward fix-up wrote) and adds each slot's float64 sum to its
+// row with one plain add: every row is owned by exactly one item.
+__global__ void __launch_bounds__(256, 2) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
+                                                           const float* __restrict__ d_soft, float* __restrict__ rows) {
+  const int lane = threadIdx.x & 31;
+  const int n_ft = a.fix[1];
+  const int n_items = a.fix[2];
+  const int n_warps = gridDim.x * (blockDim.x >> 5);
+  const bool soft_grad = d_soft != nullptr;
+  const int* plan = fix_plan(a);
+  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_items; item += n_warps) {
+    // tile of this item: last plan entry <= item
+    int lo = 0, hi = n_ft - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (plan[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int it = lo;
+    const int start = fix_tiles(a)[it];
+    const int* plist = fix_pixels(a) + start;
+    const int t = plist[0] >> 8;
+    const int4 ti = a.tile_info[t];
+    const int nflag = ti.y;
+    const int b = (ti.w >> 5) + item - plan[lo];
+    const int kb = b * 32, k = kb + lane;
+    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
     const int2 rg = a.ranges[t];
     const int s0 = rg.x, s1 = rg.y;
     const float4* ckt = a.ckpt + ckpt_base(s0, t);
-    const bool soft_grad = d_soft != nullptr;
-    for (int b = warp; b < nb; b += 8) {
-      const int kb = b * 32, k = kb + lane;
-      // The bucket's slots, loaded once for all flagged pixels.
-      SlotRaw raw;
-      load_slot(a, s0 + k, s1, raw);
-      double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      float4 cnext = make_float4(1.f, 0.f, 0.f, 0.f);
-      int f = 0;
-      while (f < nflag && sp[f].nw <= kb) f++;  // warp-uniform
-      if (f < nflag && b > 0) cnext = ckt[(size_t)b * TILE_PX + sp[f].p];
-      while (f < nflag) {
-        const FixPix q = sp[f];
-        const float4 c = cnext;
-        int fn = f + 1;
-        while (fn < nflag && sp[fn].nw <= kb) fn++;
-        if (fn < nflag && b > 0) cnext = ckt[(size_t)b * TILE_PX + sp[fn].p];
-        const int px = tx * TILE + (q.p & 15), py = ty * TILE + (q.p >> 4);
-        double T = 1.0, H = 0.0;
-        if (b > 0) {
-          T = c.x;
-          H = q.w0 * c.y + q.w1 * c.z + q.w2 * c.w;
-        }
-        Slot64 s;
-        eval_slot(raw, k < q.nw && raw.valid, (double)px, (double)py, s, soft_grad);
-        const bool bl = s.cand && !(q.term && k == q.nw - 1);
-        const double f1 = bl ? (1.0 - s.alpha) : 1.0;
+    SlotRaw raw;
+    load_slot(a, s0 + k, s1, raw);
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int f0 = 0; f0 < nflag; f0 += 32) {
+      // lane f - f0 loads flagged pixel f's inputs
+      int my_p = 0, my_nw = 0, my_term = 0, my_kf = 0;
+      double my_w0 = 0.0, my_w1 = 0.0, my_w2 = 0.0, my_ws = 0.0, my_wimg = 0.0;
+      float4 my_ck = make_float4(1.f, 0.f, 0.f, 0.f);
+      if (f0 + lane < nflag) {
+        my_p = plist[f0 + lane] & 255;
+        const size_t pix = (size_t)(ty * TILE + (my_p >> 4)) * a.width + tx * TILE + (my_p & 15);
+        my_nw = a.n_walk[pix];
+        my_term = a.term[pix];
+        my_kf = fix_kflag(a)[pix];
+        my_w0 = d_image[pix * 3];
+        my_w1 = d_image[pix * 3 + 1];
+        my_w2 = d_image[pix * 3 + 2];
+        my_ws = soft_grad ? (double)d_soft[pix] : 0.0;
+        my_wimg = my_w0 * (double)a.image[pix * 3] + my_w1 * (double)a.image[pix * 3 + 1] +
+                  my_w2 * (double)a.image[pix * 3 + 2];
+        if (b > 0 && my_nw > kb) my_ck = ckt[(size_t)b * TILE_PX + my_p];
+      }
+      // pixels whose fp64 part [kflag, n_walk) meets this bucket
+      const unsigned walks = __ballot_sync(FULL, f0 + lane < nflag && my_nw > kb && my_kf < kb + 32);
+      for (unsigned rem = walks; rem; rem &= rem - 1) {
+        const int f = __ffs(rem) - 1;
+        const int p = __shfl_sync(FULL, my_p, f), nw = __shfl_sync(FULL, my_nw, f);
+        const int term = __shfl_sync(FULL, my_term, f), kf = __shfl_sync(FULL, my_kf, f);
+        const double w0 = __shfl_sync(FULL, my_w0, f), w1 = __shfl_sync(FULL, my_w1, f),
+                     w2 = __shfl_sync(FULL, my_w2, f), ws = __shfl_sync(FULL, my_ws, f),
+                     wimg = __shfl_sync(FULL, my_wimg, f);
+        const float ckx = __shfl_sync(FULL, my_ck.x, f), cky = __shfl_sync(FULL, my_ck.y, f),
+                    ckz = __shfl_sync(FULL, my_ck.z, f), ckw = __shfl_sync(FULL, my_ck.w, f);
+        const int px = tx * TILE + (p & 15), py = ty * TILE + (p >> 4);
+        const double T = (double)ckx;
+        const double H = w0 * cky + w1 * ckz + w2 * ckw;
+        Slot64 sl;
+        eval_slot(raw, k < nw && raw.valid, (double)px, (double)py, sl, soft_grad);
+        const bool bl = sl.cand && !(term && k == nw - 1);
+        const double f1 = bl ? (1.0 - sl.alpha) : 1.0;
         double P = f1;
         for (int d = 1; d < 32; d <<= 1) {
           const double o = __shfl_up_sync(FULL, P, d);
@@ -836,42 +916,41 @@ __global__ void __launch_bounds__(256) k_backward_fixup(RasterArgs a, const floa
         double Pex = __shfl_up_sync(FULL, P, 1);
         if (lane == 0) Pex = 1.0;
         const double Tb = T * Pex;
-        const double wc = bl ? (q.w0 * s.col[0] + q.w1 * s.col[1] + q.w2 * s.col[2]) : 0.0;
-        const double e = bl ? s.alpha * Tb * wc : 0.0;
+        const double wc = bl ? (w0 * sl.col[0] + w1 * sl.col[1] + w2 * sl.col[2]) : 0.0;
+        const double e = bl ? sl.alpha * Tb * wc : 0.0;
         double E = e;  // inclusive prefix sum of w.(c alpha T)
         for (int d = 1; d < 32; d <<= 1) {
           const double o = __shfl_up_sync(FULL, E, d);
           if (lane >= d) E += o;
         }
         const double Hb = H + (E - e);
-        if (s.valid && !s.skip) {
+        if (sl.valid && !sl.skip && k >= kf) {  // earlier slots: the fp32 backward's
           double dlda = 0.0;
           if (bl) {
-            const double aT = s.alpha * Tb;
-            acc[0] += aT * q.w0;
-            acc[1] += aT * q.w1;
-            acc[2] += aT * q.w2;
-            dlda = Tb * wc - (q.wimg - Hb - aT * wc) / (1.0 - s.alpha);
+            const double aT = sl.alpha * Tb;
+            acc[0] += aT * w0;
+            acc[1] += aT * w1;
+            acc[2] += aT * w2;
+            dlda = Tb * wc - (wimg - Hb - aT * wc) / (1.0 - sl.alpha);
           }
-          if (!s.capped) {
-            acc[3] += (dlda + q.ws * s.sv * (1.0 - s.sv) / SOFT_TAU) * s.alpha * (1.0 - s.opa);
+          if (!sl.capped) {
+            acc[3] += (dlda + ws * sl.sv * (1.0 - sl.sv) / SOFT_TAU) * sl.alpha * (1.0 - sl.opa);
             if (bl) {
-              const double gp = dlda * s.alpha;
-              acc[4] += gp * (s.qa * s.dx + s.qb * s.dy);
-              acc[5] += gp * (s.qb * s.dx + s.qc * s.dy);
-              acc[6] += gp * (-0.5 * s.dx * s.dx);
-              acc[7] += gp * (-s.dx * s.dy);
-              acc[8] += gp * (-0.5 * s.dy * s.dy);
+              const double gp = dlda * sl.alpha;
+              acc[4] += gp * (sl.qa * sl.dx + sl.qb * sl.dy);
+              acc[5] += gp * (sl.qb * sl.dx + sl.qc * sl.dy);
+              acc[6] += gp * (-0.5 * sl.dx * sl.dx);
+              acc[7] += gp * (-sl.dx * sl.dy);
+              acc[8] += gp * (-0.5 * sl.dy * sl.dy);
             }
           }
         }
-        f = fn;
       }
-      if (raw.valid) {
-        float* row = rows + (size_t)inst_row(a, raw.g, tx, ty) * 9;
-        for (int j = 0; j < 9; j++)
-          if (acc[j] != 0.0) row[j] += (float)acc[j];
-      }
+    }
+    if (raw.valid) {
+      float* row = rows + (size_t)inst_row(a, raw.g, tx, ty) * 9;
+      for (int j = 0; j < 9; j++)
+        if (acc[j] != 0.0) row[j] += (float)acc[j];
     }
   }
 }
@@ -884,7 +963,7 @@ static int num_sms() {
 }
 
 extern "C" int64_t ssr_fix_list_ints(int32_t width, int32_t height, int32_t n_tiles) {
-  return 2 + (int64_t)n_tiles + (int64_t)width * height;
+  return FIX_HEAD + 2 * (int64_t)n_tiles + 2 * (int64_t)width * height;
 }
 
 static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* ranges, const ssr_frame& f,
@@ -916,7 +995,7 @@ static RasterArgs make_args(ssr_splats sp, const uint32_t* inst, const int32_t* 
   a.hard = f.hard_count;
   a.soft = f.soft_count;
   a.flagged = f.flagged;
-  a.tile_info = (int2*)f.tile_info;
+  a.tile_info = (int4*)f.tile_info;
   a.ckpt = (float4*)f.ckpt;
   a.fix = f.fix_list;
   a.n_tiles = f.tiles_x * f.tiles_y;
@@ -940,7 +1019,8 @@ extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_ga
     set_error("ssr_forward: frame.fix_list is required");
     return SSR_ERR_INVALID;
   }
-  if (cudaMemsetAsync(frame.fix_list, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return check_launch("fix_list reset");
+  if (cudaMemsetAsync(frame.fix_list, 0, FIX_HEAD * sizeof(int32_t), st) != cudaSuccess)
+    return check_launch("fix_list reset");
   k_forward<<<n_tiles, TILE_PX, 0, st>>>(a);
   SSR_TRY(check_launch("k_forward"));
   k_forward_fixup<<<num_sms() * 4, 256, 0, st>>>(a);
@@ -967,6 +1047,8 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     set_error("ssr_backward: frame.fix_list is required");
     return SSR_ERR_INVALID;
   }
-  k_backward_fixup<<<num_sms() * 3, 256, 0, st>>>(a, d_image, d_soft, inst_rows);
+  k_fix_plan<<<1, 1024, 0, st>>>(a);
+  SSR_TRY(check_launch("k_fix_plan"));
+  k_backward_fixup<<<num_sms() * 2, 256, 0, st>>>(a, d_image, d_soft, inst_rows);
   return check_launch("k_backward_fixup");
 }

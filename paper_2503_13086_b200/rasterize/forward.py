@@ -36,7 +36,7 @@ class RenderOutput:
     generation: int
     workers: int = dc_field(default=1, repr=False)
     flagged: torch.Tensor = dc_field(default=None, repr=False)  # (H, W) uint8 guard-band pixels
-    tile_info: torch.Tensor = dc_field(default=None, repr=False)  # (n_tiles, 2) int32
+    tile_info: torch.Tensor = dc_field(default=None, repr=False)  # (n_tiles, 4) int32
     ckpt: torch.Tensor = dc_field(default=None, repr=False)  # bucket checkpoints (T, C_front)
     fix_list: torch.Tensor = dc_field(default=None, repr=False)  # compact flagged pixel / tile lists
 
@@ -75,7 +75,7 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
         image=e(h, w, 3), t_final=e(h, w), n_walk=e(h, w, dt=torch.int32), terminated=e(h, w, dt=torch.uint8),
         hard_count=e(h, w, dt=torch.int32), soft_count=e(h, w, dt=torch.float64), splats=splats, cam=cam, bg=bg,
         generation=field.generation, workers=workers, flagged=e(h, w, dt=torch.uint8),
-        tile_info=e(n_tiles, 2, dt=torch.int32),
+        tile_info=e(n_tiles, 4, dt=torch.int32),
         ckpt=e(int(_lib.load().ssr_ckpt_floats(m, n_tiles))),
         fix_list=e(int(_lib.load().ssr_fix_list_ints(w, h, n_tiles)), dt=torch.int32),
     )

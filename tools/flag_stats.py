@@ -9,7 +9,7 @@ f = GaussianField.from_host(hp)
 for v in (8, 1):
     cam = scenes.camera(2, view=v)
     out = render(f, cam)
-    ti = out.tile_info.view(-1, 2).cpu().numpy() if hasattr(out, "tile_info") else None
+    ti = out.tile_info.view(-1, 4).cpu().numpy() if hasattr(out, "tile_info") else None
 
     if ti is not None:
         nf = ti[:, 1]; nx = ti[:, 0]
