@@ -1,10 +1,11 @@
 // Stage 2: tile-key duplication, prefix scan and the (tile, depth) sort
 // (rasterize/projection.py:165-191), as a depth pre-sort + stable tile sort:
 //
-//  1. the N Gaussians are radix-sorted by fp32(depth64) bits (culled rows
-//     keyed last); runs of equal fp32 keys are re-ordered by (fp64 depth,
-//     field row).  fp64 -> fp32 rounding is monotone, so this is exactly the
-//     reference's fp64 depth order with row-index tie-break;
+//  1. the N Gaussians are radix-sorted by a 24-bit monotone key of
+//     fp32(depth64) (culled rows keyed last); runs of equal keys are
+//     re-ordered by (fp64 depth, field row).  Rounding and the key map are
+//     monotone, so this is exactly the reference's fp64 depth order with
+//     row-index tie-break;
 //  2. tiles-touched counts are scanned in that order, so every Gaussian's
 //     instances are emitted at depth-ordered positions (splats.offset);
 //  3. one stable LSD radix sort over the tile id alone (ceil(log2 n_tiles)
@@ -20,13 +21,26 @@ namespace ssr {
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// 24-bit depth keys (3 radix passes instead of 4): the fp32 bit pattern of a
+// kept depth (> ZNEAR > 0, so monotone in the depth) minus that of ZNEAR,
+// shifted right by DEPTH_KEY_SHIFT (16 consecutive fp32 depths per key, ~1e-6
+// relative) and clamped below the culled key.  The mapping is monotone, so
+// equal-key runs only need re-ordering by (fp64 depth, row): k_depth_tiefix.
+constexpr int DEPTH_KEY_BITS = 24;
+constexpr int DEPTH_KEY_SHIFT = 4;
+constexpr uint32_t DEPTH_KEY_CULLED = (1u << DEPTH_KEY_BITS) - 1u;
+
 __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const uint32_t* __restrict__ tiles,
                                                     const double* __restrict__ depth, uint32_t* __restrict__ keys,
                                                     uint32_t* __restrict__ vals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  // depth > ZNEAR > 0 for kept rows, so the float bit pattern is monotone
-  keys[i] = tiles[i] ? __float_as_uint(__double2float_rn(depth[i])) : 0xffffffffu;
+  uint32_t key = DEPTH_KEY_CULLED;
+  if (tiles[i]) {
+    const uint32_t b = __float_as_uint(__double2float_rn(depth[i])) - __float_as_uint((float)ZNEAR);
+    key = min(b >> DEPTH_KEY_SHIFT, DEPTH_KEY_CULLED - 1u);
+  }
+  keys[i] = key;
   vals[i] = (uint32_t)i;
 }
 
@@ -37,7 +51,7 @@ __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t*
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t key = keys[s];
-  if (key == 0xffffffffu) return;
+  if (key == DEPTH_KEY_CULLED) return;
   const bool head = (s == 0) || (keys[s - 1] != key);
   if (!head || s + 1 >= n || keys[s + 1] != key) return;
   int64_t e = s + 1;
@@ -75,23 +89,43 @@ __global__ void k_zero_total(uint32_t* total) {
   if (threadIdx.x == 0) *total = 0u;
 }
 
-// One thread per field row writes its tiles at its depth-ordered offset;
-// emission order inside a row is ty-outer / tx-inner (projection.py:175-182).
+// Every field row writes its tiles at its depth-ordered offset; emission order
+// inside a row is ty-outer / tx-inner (projection.py:175-182).  Rows with at
+// most DUP_SMALL tiles are written by their own thread; larger rows (big
+// splats, up to thousands of tiles) by the whole warp, lane-strided and
+// coalesced, so one large splat no longer serialises its warp.
+constexpr uint32_t DUP_SMALL = 16;
+
 __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const uint32_t* __restrict__ tiles,
                                                    const uint32_t* __restrict__ offset, const int4* __restrict__ rect,
                                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t nt = tiles[i];
-  if (nt == 0) return;
-  const int4 r = rect[i];
-  uint32_t o = offset[i];
-  for (int ty = r.y; ty < r.w; ty++) {
-    const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
-    for (int tx = r.x; tx < r.z; tx++) {
-      keys[o] = row + (uint32_t)tx;
-      vals[o] = (uint32_t)i;
-      o++;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nt = i < n ? tiles[i] : 0u;
+  if (nt > 0 && nt <= DUP_SMALL) {
+    const int4 r = rect[i];
+    uint32_t o = offset[i];
+    for (int ty = r.y; ty < r.w; ty++) {
+      const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
+      for (int tx = r.x; tx < r.z; tx++) {
+        keys[o] = row + (uint32_t)tx;
+        vals[o] = (uint32_t)i;
+        o++;
+      }
+    }
+  }
+  unsigned big = __ballot_sync(0xffffffffu, nt > DUP_SMALL);
+  while (big) {
+    const int l = __ffs(big) - 1;
+    big &= big - 1;
+    const int64_t g = i - lane + l;
+    const int4 r = rect[g];
+    const uint32_t o = offset[g];
+    const uint32_t w = (uint32_t)(r.z - r.x), cnt = __shfl_sync(0xffffffffu, nt, l);
+    for (uint32_t j = lane; j < cnt; j += 32) {
+      const uint32_t ty = (uint32_t)r.y + j / w, tx = (uint32_t)r.x + j % w;
+      keys[o + j] = ty * (uint32_t)tiles_x + tx;
+      vals[o + j] = (uint32_t)g;
     }
   }
 }
@@ -172,9 +206,9 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   const unsigned blocks = (unsigned)((n + 255) / 256);
   k_depth_keys<<<blocks, 256, 0, st>>>(n, splats.tiles, splats.depth, keys_in, vals_in);
   SSR_TRY(check_launch("k_depth_keys"));
-  size_t tb = sort32_temp_bytes(n, 32);
-  SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)temp, tb, keys_in, keys_out, vals_in, order, (int)n, 0, 32,
-                                                     st),
+  size_t tb = sort32_temp_bytes(n, DEPTH_KEY_BITS);
+  SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)temp, tb, keys_in, keys_out, vals_in, order, (int)n, 0,
+                                                     DEPTH_KEY_BITS, st),
                      "depth sort"));
   k_depth_tiefix<<<blocks, 256, 0, st>>>(n, keys_out, order, splats.depth);
   SSR_TRY(check_launch("k_depth_tiefix"));

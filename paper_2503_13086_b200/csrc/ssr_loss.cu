@@ -36,12 +36,21 @@ __device__ __forceinline__ double block_sum64(double v, double* red) {
   return s;
 }
 
+// Register-blocked separable blur: the horizontal pass gives each thread 8
+// consecutive outputs of one row (18 loads per map for 88 taps), the vertical
+// pass 4 consecutive outputs of one column (14 loads per map for 44 taps), so
+// shared-memory traffic is ~1/4 of a per-output 11-tap loop.
+constexpr int HSEG = 8;                 // horizontal outputs per thread
+constexpr int HITEMS = LH * (LT / HSEG);  // 168
+constexpr int VSEG = 4;                 // vertical outputs per thread (32 x 8 = 256 items)
+constexpr int HZS = LT + 1;             // padded row stride of the horizontal results
+
 __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
                                                   const float* __restrict__ tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
                                                   LossAcc* acc) {
   __shared__ float sx[LH][LH + 1], sy[LH][LH + 1];
-  __shared__ float hz[5][LH][LT];
+  __shared__ float hz[5][LH][HZS];
   __shared__ double red[8];
   const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
   const int tid = threadIdx.x;
@@ -49,68 +58,91 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
   const int n_crop_w = W - 2 * HALO, n_crop_h = H - 2 * HALO;
   const double mw = 1.0 / ((double)n_crop_w * n_crop_h * 3.0);
   const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+  float wv[11];
+#pragma unroll
+  for (int t = 0; t < 11; t++) wv[t] = c_win[t];
   double l1 = 0.0, ss = 0.0;
   for (int ch = 0; ch < 3; ch++) {
-    for (int e = tid; e < LH * LH; e += blockDim.x) {
-      const int r = e / LH, c = e % LH;
-      const int gr = r0 - HALO + r, gc = c0 - HALO + c;
-      const bool in = gr >= 0 && gr < H && gc >= 0 && gc < W;
-      const size_t pi = (size_t)gr * W + gc;
-      sx[r][c] = in ? img[pi * 3 + ch] : 0.f;
-      sy[r][c] = in ? tgt[pi * 3 + ch] : 0.f;
+    // 8 rows x 32 columns per pass, no div/mod per element
+    for (int r = tid >> 5; r < LH; r += 8) {
+      const int gr = r0 - HALO + r;
+      const bool rin = gr >= 0 && gr < H;
+      for (int c = tid & 31; c < LH; c += 32) {
+        const int gc = c0 - HALO + c;
+        const bool in = rin && gc >= 0 && gc < W;
+        const size_t pi = (size_t)gr * W + gc;
+        sx[r][c] = in ? img[pi * 3 + ch] : 0.f;
+        sy[r][c] = in ? tgt[pi * 3 + ch] : 0.f;
+      }
     }
     __syncthreads();
-    for (int e = tid; e < LH * LT; e += blockDim.x) {
-      const int r = e / LT, c = e % LT;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+    if (tid < HITEMS) {
+      const int r = tid / (LT / HSEG), cs = (tid % (LT / HSEG)) * HSEG;
+      float xv[HSEG + 10], yv[HSEG + 10];
 #pragma unroll
-      for (int t = 0; t < 11; t++) {
-        const float x = sx[r][c + t], y = sy[r][c + t], w = c_win[t];
-        a0 += w * x;
-        a1 += w * y;
-        a2 += w * x * x;
-        a3 += w * y * y;
-        a4 += w * x * y;
+      for (int j = 0; j < HSEG + 10; j++) {
+        xv[j] = sx[r][cs + j];
+        yv[j] = sy[r][cs + j];
       }
-      hz[0][r][c] = a0;
-      hz[1][r][c] = a1;
-      hz[2][r][c] = a2;
-      hz[3][r][c] = a3;
-      hz[4][r][c] = a4;
+      // one map at a time: the map's inputs (x, y, x^2, y^2, xy) are formed once
+      // per input element, then 11 FMAs per output
+#pragma unroll
+      for (int k = 0; k < 5; k++) {
+        float in[HSEG + 10];
+#pragma unroll
+        for (int j = 0; j < HSEG + 10; j++)
+          in[j] = k == 0 ? xv[j] : k == 1 ? yv[j] : k == 2 ? xv[j] * xv[j] : k == 3 ? yv[j] * yv[j] : xv[j] * yv[j];
+#pragma unroll
+        for (int o = 0; o < HSEG; o++) {
+          float v = 0.f;
+#pragma unroll
+          for (int t = 0; t < 11; t++) v = fmaf(wv[t], in[o + t], v);
+          hz[k][r][cs + o] = v;
+        }
+      }
     }
     __syncthreads();
-    for (int e = tid; e < LT * LT; e += blockDim.x) {
-      const int r = e / LT, c = e % LT;
-      const int gr = r0 + r, gc = c0 + c;
-      if (gr >= H || gc >= W) continue;
-      float mx = 0.f, my = 0.f, gx2 = 0.f, gy2 = 0.f, gxy = 0.f;
+    {
+      const int c = tid % LT, rs = (tid / LT) * VSEG;
+      float mom[5][VSEG];
 #pragma unroll
-      for (int t = 0; t < 11; t++) {
-        const float w = c_win[t];
-        mx += w * hz[0][r + t][c];
-        my += w * hz[1][r + t][c];
-        gx2 += w * hz[2][r + t][c];
-        gy2 += w * hz[3][r + t][c];
-        gxy += w * hz[4][r + t][c];
+      for (int k = 0; k < 5; k++) {
+        float col[VSEG + 10];
+#pragma unroll
+        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[k][rs + j][c];
+#pragma unroll
+        for (int o = 0; o < VSEG; o++) {
+          float v = 0.f;
+#pragma unroll
+          for (int t = 0; t < 11; t++) v += wv[t] * col[o + t];
+          mom[k][o] = v;
+        }
       }
-      const float vx = gx2 - mx * mx, vy = gy2 - my * my, cv = gxy - mx * my;
-      const float a1 = 2.f * mx * my + C1, a2 = 2.f * cv + C2;
-      const float b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
-      const float smap = (a1 * a2) / (b1 * b2);
-      const bool crop = gr >= HALO && gr < H - HALO && gc >= HALO && gc < W - HALO;
-      const size_t pi = (size_t)gr * W + gc;
-      float dmu = 0.f, dg2 = 0.f, dxy = 0.f;
-      if (crop) {
-        ss += (double)smap;
-        const float m = (float)mw;
-        dmu = m * (2.f * my * (a2 - a1) / (b1 * b2) - 2.f * mx * smap * (1.f / b1 - 1.f / b2));
-        dg2 = m * (-smap / b2);
-        dxy = m * (2.f * a1 / (b1 * b2));
+#pragma unroll
+      for (int o = 0; o < VSEG; o++) {
+        const int r = rs + o;
+        const int gr = r0 + r, gc = c0 + c;
+        if (gr >= H || gc >= W) continue;
+        const float mx = mom[0][o], my = mom[1][o], gx2 = mom[2][o], gy2 = mom[3][o], gxy = mom[4][o];
+        const float vx = gx2 - mx * mx, vy = gy2 - my * my, cv = gxy - mx * my;
+        const float a1 = 2.f * mx * my + C1, a2 = 2.f * cv + C2;
+        const float b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
+        const float smap = (a1 * a2) / (b1 * b2);
+        const bool crop = gr >= HALO && gr < H - HALO && gc >= HALO && gc < W - HALO;
+        const size_t pi = (size_t)gr * W + gc;
+        float dmu = 0.f, dg2 = 0.f, dxy = 0.f;
+        if (crop) {
+          ss += (double)smap;
+          const float m = (float)mw;
+          dmu = m * (2.f * my * (a2 - a1) / (b1 * b2) - 2.f * mx * smap * (1.f / b1 - 1.f / b2));
+          dg2 = m * (-smap / b2);
+          dxy = m * (2.f * a1 / (b1 * b2));
+        }
+        dmaps[(size_t)(ch * 3 + 0) * HW + pi] = dmu;
+        dmaps[(size_t)(ch * 3 + 1) * HW + pi] = dg2;
+        dmaps[(size_t)(ch * 3 + 2) * HW + pi] = dxy;
+        l1 += (double)fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
       }
-      dmaps[(size_t)(ch * 3 + 0) * HW + pi] = dmu;
-      dmaps[(size_t)(ch * 3 + 1) * HW + pi] = dg2;
-      dmaps[(size_t)(ch * 3 + 2) * HW + pi] = dxy;
-      l1 += (double)fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
     }
     __syncthreads();
   }
@@ -171,54 +203,72 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
                                                   double w_l1, double w_ssim, double w_load,
                                                   float* __restrict__ d_image, float* __restrict__ d_soft) {
   __shared__ float sm[3][LH][LH + 1];
-  __shared__ float hz[3][LH][LT];
+  __shared__ float hz[3][LH][HZS];
   const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
   const int tid = threadIdx.x;
   const size_t HW = (size_t)W * H;
   const float gl1 = (float)(w_l1 / (double)(HW * 3));
   const float gss = (float)w_ssim;
+  float wv[11];
+#pragma unroll
+  for (int t = 0; t < 11; t++) wv[t] = c_win[t];
   for (int ch = 0; ch < 3; ch++) {
-    for (int e = tid; e < LH * LH; e += blockDim.x) {
-      const int r = e / LH, c = e % LH;
-      const int gr = r0 - HALO + r, gc = c0 - HALO + c;
-      const bool in = gr >= 0 && gr < H && gc >= 0 && gc < W;
-      const size_t pi = (size_t)gr * W + gc;
-      for (int k = 0; k < 3; k++) sm[k][r][c] = in ? dmaps[(size_t)(ch * 3 + k) * HW + pi] : 0.f;
+    for (int r = tid >> 5; r < LH; r += 8) {
+      const int gr = r0 - HALO + r;
+      const bool rin = gr >= 0 && gr < H;
+      for (int c = tid & 31; c < LH; c += 32) {
+        const int gc = c0 - HALO + c;
+        const bool in = rin && gc >= 0 && gc < W;
+        const size_t pi = (size_t)gr * W + gc;
+#pragma unroll
+        for (int k = 0; k < 3; k++) sm[k][r][c] = in ? dmaps[(size_t)(ch * 3 + k) * HW + pi] : 0.f;
+      }
     }
     __syncthreads();
-    for (int e = tid; e < LH * LT; e += blockDim.x) {
-      const int r = e / LT, c = e % LT;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+    if (tid < HITEMS) {
+      const int r = tid / (LT / HSEG), cs = (tid % (LT / HSEG)) * HSEG;
 #pragma unroll
-      for (int t = 0; t < 11; t++) {
-        const float w = c_win[t];
-        a0 += w * sm[0][r][c + t];
-        a1 += w * sm[1][r][c + t];
-        a2 += w * sm[2][r][c + t];
+      for (int k = 0; k < 3; k++) {
+        float xv[HSEG + 10];
+#pragma unroll
+        for (int j = 0; j < HSEG + 10; j++) xv[j] = sm[k][r][cs + j];
+#pragma unroll
+        for (int o = 0; o < HSEG; o++) {
+          float v = 0.f;
+#pragma unroll
+          for (int t = 0; t < 11; t++) v += wv[t] * xv[o + t];
+          hz[k][r][cs + o] = v;
+        }
       }
-      hz[0][r][c] = a0;
-      hz[1][r][c] = a1;
-      hz[2][r][c] = a2;
     }
     __syncthreads();
-    for (int e = tid; e < LT * LT; e += blockDim.x) {
-      const int r = e / LT, c = e % LT;
-      const int gr = r0 + r, gc = c0 + c;
-      if (gr >= H || gc >= W) continue;
-      float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    {
+      const int c = tid % LT, rs = (tid / LT) * VSEG;
+      float bm[3][VSEG];
 #pragma unroll
-      for (int t = 0; t < 11; t++) {
-        const float w = c_win[t];
-        b0 += w * hz[0][r + t][c];
-        b1 += w * hz[1][r + t][c];
-        b2 += w * hz[2][r + t][c];
+      for (int k = 0; k < 3; k++) {
+        float col[VSEG + 10];
+#pragma unroll
+        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[k][rs + j][c];
+#pragma unroll
+        for (int o = 0; o < VSEG; o++) {
+          float v = 0.f;
+#pragma unroll
+          for (int t = 0; t < 11; t++) v += wv[t] * col[o + t];
+          bm[k][o] = v;
+        }
       }
-      const size_t pi = (size_t)gr * W + gc;
-      const float x = img[pi * 3 + ch], y = tgt[pi * 3 + ch];
-      const float gs = b0 + 2.f * x * b1 + y * b2;  // d SSIM / d x
-      const float diff = x - y;
-      const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
-      d_image[pi * 3 + ch] = gl1 * sgn - gss * gs;
+#pragma unroll
+      for (int o = 0; o < VSEG; o++) {
+        const int gr = r0 + rs + o, gc = c0 + c;
+        if (gr >= H || gc >= W) continue;
+        const size_t pi = (size_t)gr * W + gc;
+        const float x = img[pi * 3 + ch], y = tgt[pi * 3 + ch];
+        const float gs = bm[0][o] + 2.f * x * bm[1][o] + y * bm[2][o];  // d SSIM / d x
+        const float diff = x - y;
+        const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+        d_image[pi * 3 + ch] = gl1 * sgn - gss * gs;
+      }
     }
     __syncthreads();
   }

@@ -6,14 +6,23 @@
 
 namespace ssr {
 
-// projection.py:69-162 + sh.py:114-132 -- one thread per field row.
-__global__ void __launch_bounds__(256) k_preprocess(Cam cam, int64_t n, int deg, int tiles_x, int tiles_y,
+// projection.py:69-162 + sh.py:114-132 -- one thread per field row.  Templated
+// on the SH degree so the basis stays in registers.
+template <int DEG>
+__global__ void __launch_bounds__(256) k_preprocess(Cam cam, int64_t n, int tiles_x, int tiles_y,
                                                     const float* __restrict__ pos, const float* __restrict__ rot,
                                                     const float* __restrict__ ls, const float* __restrict__ logit,
                                                     const float* __restrict__ sh, ssr_splats o) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int K = (deg + 1) * (deg + 1);
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  // start the row's SH coefficients on their way to L2 while the fp64
+  // projection runs (culled rows waste 3K floats of L2 fill, visible rows
+  // then read them at L2 latency)
+  {
+    const char* shp = reinterpret_cast<const char*>(sh + i * 3 * K);
+    for (int off = 0; off < 3 * K * 4; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
+  }
   Proj64 P;
   if (!project64(cam, pos + i * 3, rot + i * 4, ls + i * 3, tiles_x, tiles_y, P)) {
     o.tiles[i] = 0;
@@ -21,7 +30,7 @@ __global__ void __launch_bounds__(256) k_preprocess(Cam cam, int64_t n, int deg,
   }
   double dir[3], rs, basis[16], col[3];
   bool lo[3], hi[3];
-  sh_color64(cam, deg, pos + i * 3, sh + i * 3 * K, dir, &rs, basis, col, lo, hi);
+  sh_color64(cam, DEG, pos + i * 3, sh + i * 3 * K, dir, &rs, basis, col, lo, hi);
   const double opa = 1.0 / (1.0 + exp(-(double)logit[i]));
   reinterpret_cast<double2*>(o.mean)[i] = make_double2(P.u, P.v);
   // near-singular conics (1 - |b|/sqrt(ac) < 1e-3) are the only ones whose fp32
@@ -96,8 +105,18 @@ extern "C" int ssr_preprocess(const ssr_camera* cam, int64_t n, int32_t sh_degre
   tile_dims(cam, &tx, &ty);
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
-  k_preprocess<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-      to_cam(*cam), n, sh_degree, tx, ty, positions, rotations, log_scales, opacity_logits, sh, splats);
+  const Cam c = to_cam(*cam);
+  cudaStream_t st = (cudaStream_t)stream;
+#define SSR_PRE(D) \
+  k_preprocess<D><<<(unsigned)blocks, threads, 0, st>>>(c, n, tx, ty, positions, rotations, log_scales, opacity_logits, \
+                                                        sh, splats)
+  switch (sh_degree) {
+    case 0: SSR_PRE(0); break;
+    case 1: SSR_PRE(1); break;
+    case 2: SSR_PRE(2); break;
+    default: SSR_PRE(3); break;
+  }
+#undef SSR_PRE
   return check_launch("k_preprocess");
 }
 
