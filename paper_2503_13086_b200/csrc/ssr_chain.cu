@@ -418,7 +418,7 @@ constexpr int SH_ROWS = SH_THREADS / SH_LANES;
 // Lane q of a row owns coefficients k = q*KL + j (j < KL, k < K) of every
 // channel; at SH3 that is one float4 per channel, read and written directly.
 template <int DEG, bool FUSED>
-__global__ void __launch_bounds__(SH_THREADS) k_chain_sh(CamF cam, int64_t n, float* __restrict__ pos,
+__global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n, float* __restrict__ pos,
                                                          float* __restrict__ sh, const uint32_t* __restrict__ tiles,
                                                          const uint32_t* __restrict__ roff,
                                                          const float4* __restrict__ color,
@@ -456,33 +456,15 @@ __global__ void __launch_bounds__(SH_THREADS) k_chain_sh(CamF cam, int64_t n, fl
       }
     }
   }
-  // fused: the lane's moments (and lane 0's position moments) loaded up front
-  float mf[3][KL], vf[3][KL];
-  float mp[3] = {0.f, 0.f, 0.f}, vp[3] = {0.f, 0.f, 0.f};
+  // fused: start the lane's moments on their way to L2 now; they are loaded
+  // after the direction gradient, when the basis registers are free
   if (FUSED) {
-    const float* mrow = adam.m + 11 * ns + ii * W;
-    const float* vrow = adam.v + 11 * ns + ii * W;
-#pragma unroll
-    for (int ch = 0; ch < 3; ch++) {
-      if (VEC) {
-        const float4 a4 = *reinterpret_cast<const float4*>(mrow + ch * K + q * 4);
-        const float4 b4 = *reinterpret_cast<const float4*>(vrow + ch * K + q * 4);
-        mf[ch][0] = a4.x, mf[ch][1] = a4.y, mf[ch][2] = a4.z, mf[ch][3] = a4.w;
-        vf[ch][0] = b4.x, vf[ch][1] = b4.y, vf[ch][2] = b4.z, vf[ch][3] = b4.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < KL; j++) {
-          const int k = q * KL + j;
-          mf[ch][j] = k < K ? mrow[ch * K + k] : 0.f;
-          vf[ch][j] = k < K ? vrow[ch * K + k] : 0.f;
-        }
-      }
-    }
-    if (q == 0)
-      for (int d = 0; d < 3; d++) {
-        mp[d] = adam.m[ii * 3 + d];
-        vp[d] = adam.v[ii * 3 + d];
-      }
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + q * KL));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + q * KL));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + K + q * KL));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + K + q * KL));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + 2 * K + q * KL));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + 2 * K + q * KL));
   }
   // direction (sh.py:114-124), recomputed by each lane
   const float ox = pos[ii * 3] - cam.center[0], oy = pos[ii * 3 + 1] - cam.center[1],
@@ -531,6 +513,34 @@ __global__ void __launch_bounds__(SH_THREADS) k_chain_sh(CamF cam, int64_t n, fl
   const float radial = gd[0] * dx + gd[1] * dy + gd[2] * dz;
   const float dpos_sh[3] = {(gd[0] - radial * dx) * irs, (gd[1] - radial * dy) * irs, (gd[2] - radial * dz) * irs};
   if (!row_ok) return;
+  // fused: the lane's moments (and lane 0's position moments)
+  float mf[3][KL], vf[3][KL];
+  float mp[3] = {0.f, 0.f, 0.f}, vp[3] = {0.f, 0.f, 0.f};
+  if (FUSED) {
+    const float* mrow = adam.m + 11 * ns + ii * W;
+    const float* vrow = adam.v + 11 * ns + ii * W;
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+      if (VEC) {
+        const float4 a4 = *reinterpret_cast<const float4*>(mrow + ch * K + q * 4);
+        const float4 b4 = *reinterpret_cast<const float4*>(vrow + ch * K + q * 4);
+        mf[ch][0] = a4.x, mf[ch][1] = a4.y, mf[ch][2] = a4.z, mf[ch][3] = a4.w;
+        vf[ch][0] = b4.x, vf[ch][1] = b4.y, vf[ch][2] = b4.z, vf[ch][3] = b4.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < KL; j++) {
+          const int k = q * KL + j;
+          mf[ch][j] = k < K ? mrow[ch * K + k] : 0.f;
+          vf[ch][j] = k < K ? vrow[ch * K + k] : 0.f;
+        }
+      }
+    }
+    if (q == 0)
+      for (int d = 0; d < 3; d++) {
+        mp[d] = adam.m[ii * 3 + d];
+        vp[d] = adam.v[ii * 3 + d];
+      }
+  }
 
   if (FUSED) {
     // positions: geometric part from the geometry kernel + view-direction part

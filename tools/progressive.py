@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--t-i", type=int, default=200)
     ap.add_argument("--per-event", type=int, default=20_000)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--fused", type=int, default=1, help="chain + Adam in one pass (backward_and_step)")
     ap.add_argument("--paper-weights", action="store_true",
                     help="losses.py defaults (load 0.41) instead of BASELINE's L1 + 0.2 D-SSIM")
     args = ap.parse_args()
@@ -112,7 +113,7 @@ def main():
             if tgt is None:
                 tgt = targets[v]
             rate = 1.6e-4 * np.exp(-k / 200.0)
-            br = train_iteration(state, cams[int(tv)], tgt, rate)
+            br = train_iteration(state, cams[int(tv)], tgt, rate, fused=bool(args.fused))
             if args.trace and k % 100 == 99:
                 torch.cuda.synchronize()
                 o = render(state.field, cams[int(tv)])
