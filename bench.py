@@ -348,6 +348,24 @@ def main():
                                "(MEASURED_PEAKS.json has no fp32 figure)",
                 "work": f"{flops / 1e9:.2f} GFLOP per launch = {FLOP_BWD_PER_PAIR if 'backward' in dom else FLOP_FWD_PER_PAIR:.0f}"
                         f" flop x {P_mean / 1e6:.1f} M walked pairs"}
+    # HBM roofline of the streaming Adam pass (7 x S bytes per row: p, g, m, v
+    # read; p, m, v written) against the measured copy bandwidth
+    roofline_hbm = None
+    adam_ms = stage_ms.get("ssr_adam")
+    if adam_ms:
+        s_bytes = 4 * (11 + 3 * (field.sh_degree + 1) ** 2)
+        adam_bytes = 7.0 * s_bytes * len(state.field)
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        ach = adam_bytes / (adam_ms / 1e3) / 1e9
+        roofline_hbm = {"bound": "hbm", "kernel": "ssr_adam (k_adam)", "achieved": ach, "peak": hbm_peak,
+                        "unit": "GB/s", "frac": ach / hbm_peak,
+                        "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                        "work": f"{adam_bytes / 1e9:.3f} GB per launch = 7 x {s_bytes} B x {len(state.field):,} rows",
+                        "traffic": None}
+        try:
+            roofline_hbm["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("ssr_adam")
+        except Exception:
+            pass
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -365,6 +383,7 @@ def main():
                    "l2": "inputs larger than L2 (field + Adam moments 708 MB, per-step working set > 1 GB)",
                    "walked_pairs_per_view": P_mean},
         "roofline": roofline,
+        "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40},
         "gpu_launches": launches,

@@ -204,6 +204,16 @@ int ssr_knn(const double* pool, int64_t n_pool, const double* queries, int64_t n
             const double* grid, const int32_t* dims, double* out_dist, void* workspace,
             int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------- field snapshot */
+/* io/ply.py:29-124: the flat float32 parameter buffer <-> PLY vertex records,
+ * n x ssr_ply_properties(deg) doubles in property order x y z nx ny nz
+ * f_dc_0..2 f_rest_* (channel-major) opacity scale_0..2 rot_0..3.  Pack widens
+ * exactly (bit-exact round trip); unpack rounds to nearest float32.  Device
+ * pointers; the host writes / parses the header (paper_2503_13086_b200/ply.py). */
+int32_t ssr_ply_properties(int32_t sh_degree);
+int ssr_ply_pack(int64_t n, int32_t sh_degree, const float* params, double* records, void* stream);
+int ssr_ply_unpack(int64_t n, int32_t sh_degree, const double* records, float* params, void* stream);
+
 /* ---------------------------------------------------------- loss */
 /* losses.py:55-173: w_l1 * L1 + w_ssim * (1 - SSIM) + w_load * std(soft).
  * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,

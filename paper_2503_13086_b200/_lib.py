@@ -74,11 +74,15 @@ _SIGS = {
     "ssr_knn_workspace": [c_int64, c_int64, ctypes.POINTER(c_int64)],
     "ssr_knn": [c_void_p, c_int64, c_void_p, c_int64, c_int32, ctypes.POINTER(c_double),
                 ctypes.POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p],
+    "ssr_ply_properties": [c_int32],
+    "ssr_ply_pack": [c_int64, c_int32, c_void_p, c_void_p, c_void_p],
+    "ssr_ply_unpack": [c_int64, c_int32, c_void_p, c_void_p, c_void_p],
     "ssr_loss_workspace": [c_int32, c_int32, ctypes.POINTER(c_int64)],
     "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                  c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
 }
-_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_fix_list_ints": c_int64}
+_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_fix_list_ints": c_int64,
+             "ssr_ply_properties": c_int32}
 
 EXPORTS = tuple(_SIGS)
 

@@ -18,9 +18,9 @@ def pytest_configure(config):
 
 
 def golden_names():
-    """Rasterizer cases (the expansion fixture is tested separately)."""
+    """Rasterizer cases (the expansion and PLY fixtures are tested separately)."""
     names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
-    return sorted(n for n in names if n != "expansion")
+    return sorted(n for n in names if n != "expansion" and not n.startswith("ply_"))
 
 
 def load_golden(name):
