@@ -6,6 +6,6 @@ O=$1; shift
 mkdir -p $O
 for K in "$@"; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 1 -c 1 \
-    -o $O/full_$K python tools/profile_step.py > $O/ncu_full_$K.log 2>&1
-  echo "ncu_full_$K exit $?" >> $O/status.txt
+    -o $O/full_${K//[^A-Za-z0-9_]/} python tools/profile_step.py > $O/ncu_full_${K//[^A-Za-z0-9_]/}.log 2>&1
+  echo "ncu_full_${K//[^A-Za-z0-9_]/} exit $?" >> $O/status.txt
 done

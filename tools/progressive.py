@@ -28,6 +28,8 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--events", type=int, default=3)
+    ap.add_argument("--warmup-events", type=int, default=1,
+                    help="untimed events first (allocator, kNN grid and first-call warm-up)")
     ap.add_argument("--start", type=int, default=1_980_000, help="field size before the timed events")
     ap.add_argument("--t-i", type=int, default=200)
     ap.add_argument("--per-event", type=int, default=20_000)
@@ -59,7 +61,8 @@ def main():
     tp.positions += jr.normal(0.0, 0.01, tp.positions.shape).astype(np.float32)
     tp.sh[:, :, 0] += jr.normal(0.0, 0.3, tp.sh[:, :, 0].shape).astype(np.float32)
     tfield = GaussianField.from_host(tp)
-    first = n_views - args.events  # the timed events are the last ones of the 100-image sequence
+    n_ev = args.warmup_events + args.events
+    first = n_views - n_ev  # the timed events are the last ones of the 100-image sequence
     targets = {v: render(tfield, cams[v]).image.clone() for v in range(max(0, first - 10), n_views)}
     del tfield
     torch.cuda.synchronize()
@@ -78,7 +81,7 @@ def main():
                        weights=weights, scene_extent=extent, rng=np.random.default_rng(7), densify=dens)
     state.global_iteration = 1  # densify lands inside the timed events, not on their first iteration
     per_event = []
-    for e in range(args.events):
+    for e in range(n_ev):
         v = first + e
         cam = cams[v]
         torch.cuda.synchronize()
@@ -131,6 +134,8 @@ def main():
         after = psnr(render(state.field, cam).image, targets[v])
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if e < args.warmup_events:
+            continue
         per_event.append(dict(image=v, seconds=dt, field=len(state.field), psnr_before=before, psnr_after=after,
                               expand_s=t2 - t1, iterations_s=t3 - t2, ms_per_iteration=(t3 - t2) / len(plan) * 1e3,
                               psnr_renders_s=t_psnr0 + (time.perf_counter() - t3)))
