@@ -401,18 +401,18 @@ __device__ __forceinline__ float pair_alpha2(float opa, float power2) { return _
 // Soft count of the forward (kernels.py:83) is accumulated as
 //   n_small * S0 + sum(y * p(y)) + sum(sigmoid(alpha) for alpha >= 2.5e-3),
 // y = alpha / SOFT_TAU, S0 = sigmoid(-ALPHA_MIN / SOFT_TAU) in float64 and p a
-// degree-5 fit of (sigmoid(y - ALPHA_MIN/TAU) - S0) / y on [0, 0.25]
-// (max abs error 1e-11; 5e-9 after fp32 Horner).  Long walks (10^4 slots)
-// would otherwise accumulate the fp32 rounding of the same ~0.403 term.
+// degree-4 fit of (sigmoid(y - ALPHA_MIN/TAU) - S0) / y on [0, 0.25]
+// (max abs error of y p(y) 1.1e-10, below the ~5e-9 of its fp32 evaluation).
+// Long walks (10^4 slots) would otherwise accumulate the fp32 rounding of the
+// same ~0.403 term.
 constexpr double SOFT_S0 = 0.4031981879117929;
 constexpr float SOFT_Y0 = 0.25f;
 __device__ __forceinline__ float soft_dev_poly(float y) {
-  float p = 3.799443657e-04f;
-  p = __fmaf_rn(p, y, 1.492375741e-03f);
-  p = __fmaf_rn(p, y, -3.667983459e-03f);
-  p = __fmaf_rn(p, y, -1.779736020e-02f);
-  p = __fmaf_rn(p, y, 2.329335734e-02f);
-  p = __fmaf_rn(p, y, 2.406294048e-01f);
+  float p = 1.76897e-03f;
+  p = __fmaf_rn(p, y, -3.74327e-03f);
+  p = __fmaf_rn(p, y, -1.778797e-02f);
+  p = __fmaf_rn(p, y, 2.329284e-02f);
+  p = __fmaf_rn(p, y, 2.4062942e-01f);
   return __fmul_rn(y, p);
 }
 

@@ -67,6 +67,85 @@ __device__ __forceinline__ uint32_t inst_row(const RasterArgs& a, uint32_t g, in
 __device__ __forceinline__ size_t ckpt_base(int s0, int t) { return ((size_t)(s0 >> 5) + (size_t)t) * TILE_PX; }
 
 // ------------------------------------------------------------------ forward (fp32)
+// Per-pixel walk state of the fp32 forward.
+struct FwdState {
+  float T, c0, c1, c2, sdev;
+  double sbig;
+  // every walked slot is exactly one of: far or small-alpha (soft term S0 +
+  // deviation), skipped fragile (no term), or large-alpha (exact sigmoid), so
+  // the S0 count is n_walk - n_big and the common paths count nothing
+  int hard, nwk, nbig;
+  bool term, flag;
+};
+
+// kernels.py:68-95 over slots [j0, jend) of the staged batch (walk index
+// k0 + j).  FRAGILE: the batch holds a near-singular conic (negative staged
+// opacity), so the power > 0 guard band is tested; batches without one (the
+// common case) skip that test entirely.  Returns false once the pixel
+// terminated or was flagged.
+template <bool FRAGILE>
+__device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const float4* sA, const float4* sB, int j0,
+                                         int jend, int k0, float fpx, float fpy, float band, float band_t) {
+#pragma unroll 4
+  for (int j = j0; j < jend; j++) {
+    const float4 M = sM[j];
+    const float4 A = sA[j];
+    const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
+    const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+    float qpos;
+    const float p2 = pair_power2(dxx, dxy, dyy, A.x, A.y, A.z, qpos);
+    if (p2 < FAR_POWER2) continue;  // soft term S0, nothing else
+    if (FRAGILE && A.w < 0.f) {
+      // only near-singular conics can round to power > 0: flag near that decision
+      if (p2 > 1e-6f * qpos && qpos != 0.f) {
+        q.flag = true;
+        q.nwk = k0 + j;  // flagged: the slot of the ambiguous decision
+        return false;
+      }
+      if (p2 > 0.f) {
+        q.nbig++;  // skipped: no soft term (counted out of the S0 total)
+        continue;
+      }
+    }
+    float alpha = pair_alpha2(fabsf(A.w), p2);
+    // alpha < 2.5e-3 is below 1/255 and far from both guard bands: only its
+    // soft-count deviation
+    const float y = __fmul_rn(alpha, 100.f);
+    if (y < SOFT_Y0) {
+      q.sdev += soft_dev_poly(y);
+      continue;
+    }
+    if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
+      q.flag = true;
+      q.nwk = k0 + j;
+      return false;
+    }
+    alpha = fminf(alpha, ALPHA_CAP_F);
+    q.nbig++;
+    q.sbig += (double)soft_sigmoid_accurate(alpha);
+    if (alpha < ALPHA_MIN_F) continue;
+    const float test = __fmul_rn(q.T, __fsub_rn(1.f, alpha));
+    if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
+      q.flag = true;
+      q.nwk = k0 + j;
+      return false;
+    }
+    if (test < T_EPS_F) {
+      q.term = true;
+      q.nwk = k0 + j + 1;
+      return false;
+    }
+    const float w = __fmul_rn(alpha, q.T);
+    const float4 B = sB[j];
+    q.c0 = __fmaf_rn(B.x, w, q.c0);
+    q.c1 = __fmaf_rn(B.y, w, q.c1);
+    q.c2 = __fmaf_rn(B.z, w, q.c2);
+    q.hard++;
+    q.T = test;
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
@@ -76,7 +155,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const bool inside = px < a.width && py < a.height;
   const int2 rg = a.ranges[t];
   const int s0 = rg.x, s1 = rg.y;
-  float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
+  const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
   const float band = a.band, band_t = a.band_t;
 
   __shared__ float4 sM[TILE_PX];  // staged mean (x int, x frac, y int, y frac)
@@ -84,103 +163,57 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   __shared__ float4 sB[TILE_PX];  // r, g, b
   __shared__ int sMax[8];
 
-  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, sdev = 0.f;
-  double sbig = 0.0;
-  // every walked slot is exactly one of: far or small-alpha (soft term S0 +
-  // deviation), skipped fragile (no term), or large-alpha (exact sigmoid), so
-  // the S0 count is n_walk - n_big and the common paths count nothing
-  int hard = 0, nwk = s1 - s0, nbig = 0;
-  bool term = false, flag = false, done = !inside;
+  FwdState q;
+  q.T = 1.f;
+  q.c0 = q.c1 = q.c2 = q.sdev = 0.f;
+  q.sbig = 0.0;
+  q.hard = 0;
+  q.nwk = s1 - s0;
+  q.nbig = 0;
+  q.term = q.flag = false;
+  bool done = !inside;
   float4* ck = a.ckpt + ckpt_base(s0, t) + tid;
 
   for (int base = s0; base < s1; base += TILE_PX) {
     if (__syncthreads_count(done) == TILE_PX) break;
     const int s = base + tid;
+    bool fragile = false;
     if (s < s1) {
       const uint32_t g = a.inst[s];
       const double2 m = a.mean[g];
       const float4 co = a.conic_opa[g];
       const float4 col = a.color[g];
-      const StagedConic q = stage_conic(co.x, co.y, co.z);
+      const StagedConic sc = stage_conic(co.x, co.y, co.z);
       const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
       sM[tid] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
-      sA[tid] = make_float4(q.a2, q.b2, q.c2, co.w);  // opacity < 0 marks a fragile conic
+      sA[tid] = make_float4(sc.a2, sc.b2, sc.c2, co.w);  // opacity < 0 marks a fragile conic
       sB[tid] = col;
+      fragile = co.w < 0.f;
     }
-    __syncthreads();
+    const bool batch_fragile = __syncthreads_or(fragile);
     if (!done) {
       const int n = min(TILE_PX, s1 - base);
       const int k0 = base - s0;
       for (int j0 = 0; j0 < n; j0 += BUCKET) {
         if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
-          ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(T, c0, c1, c2);
-          sbig += (double)sdev;
-          sdev = 0.f;
+          ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
+          q.sbig += (double)q.sdev;
+          q.sdev = 0.f;
         }
         const int jend = min(j0 + BUCKET, n);
-#pragma unroll 4
-        for (int j = j0; j < jend; j++) {
-          const float4 M = sM[j];
-          const float4 A = sA[j];
-          const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
-          const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
-          float qpos;
-          const float p2 = pair_power2(dxx, dxy, dyy, A.x, A.y, A.z, qpos);
-          if (p2 < FAR_POWER2) continue;  // soft term S0, nothing else
-          // Only near-singular conics (negative staged opacity, warp-uniform)
-          // can round to power > 0: flag the pixel near that decision.
-          if (A.w < 0.f) {
-            if (p2 > 1e-6f * qpos && qpos != 0.f) {
-              flag = true;
-            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
-              break;
-            }
-            if (p2 > 0.f) {
-              nbig++;  // skipped: no soft term (counted out of the S0 total)
-              continue;
-            }
-          }
-          float alpha = pair_alpha2(fabsf(A.w), p2);
-          // common path: alpha < 2.5e-3 is below 1/255 and far from both guard
-          // bands, so it only adds its soft-count deviation
-          const float y = __fmul_rn(alpha, 100.f);
-          if (y < SOFT_Y0) {
-            sdev += soft_dev_poly(y);
-            continue;
-          }
-          if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
-            flag = true;
-            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
-            break;
-          }
-          alpha = fminf(alpha, ALPHA_CAP_F);
-          nbig++;
-          sbig += (double)soft_sigmoid_accurate(alpha);
-          if (alpha < ALPHA_MIN_F) continue;
-          const float test = __fmul_rn(T, __fsub_rn(1.f, alpha));
-          if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
-            flag = true;
-            nwk = k0 + j;  // flagged: the slot of the ambiguous decision
-            break;
-          }
-          if (test < T_EPS_F) {
-            term = true;
-            nwk = k0 + j + 1;
-            break;
-          }
-          const float w = __fmul_rn(alpha, T);
-          const float4 B = sB[j];
-          c0 = __fmaf_rn(B.x, w, c0);
-          c1 = __fmaf_rn(B.y, w, c1);
-          c2 = __fmaf_rn(B.z, w, c2);
-          hard++;
-          T = test;
+        const bool go = batch_fragile ? fwd_walk<true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                                      : fwd_walk<false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
+        if (!go) {
+          done = true;
+          break;
         }
-        if (flag || term) break;
       }
-      if (flag || term) done = true;
     }
   }
+  float T = q.T, c0 = q.c0, c1 = q.c1, c2 = q.c2, sdev = q.sdev;
+  double sbig = q.sbig;
+  int hard = q.hard, nwk = q.nwk, nbig = q.nbig;
+  const bool term = q.term, flag = q.flag;
   if (inside) {
     const size_t pix = (size_t)py * a.width + px;
     a.image[pix * 3 + 0] = c0 + a.bg[0] * T;
