@@ -83,11 +83,14 @@ struct FwdState {
 // opacity), so the power > 0 guard band is tested; batches without one (the
 // common case) skip that test entirely.  Returns false once the pixel
 // terminated or was flagged.
-template <bool FRAGILE>
+template <bool FRAGILE, bool FULL>
 __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const float4* sA, const float4* sB, int j0,
                                          int jend, int k0, float fpx, float fpy, float band, float band_t) {
-#pragma unroll 4
-  for (int j = j0; j < jend; j++) {
+  // FULL: a whole 32-slot bucket, constant trip count (no per-slot bound test)
+  const int nj = FULL ? BUCKET : jend - j0;
+#pragma unroll 8
+  for (int jj = 0; jj < nj; jj++) {
+    const int j = j0 + jj;
     const float4 M = sM[j];
     const float4 A = sA[j];
     const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
@@ -201,8 +204,13 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
           q.sdev = 0.f;
         }
         const int jend = min(j0 + BUCKET, n);
-        const bool go = batch_fragile ? fwd_walk<true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
-                                      : fwd_walk<false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
+        bool go;
+        if (jend - j0 == BUCKET)
+          go = batch_fragile ? fwd_walk<true, true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
+        else
+          go = batch_fragile ? fwd_walk<true, false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
         if (!go) {
           done = true;
           break;
