@@ -471,34 +471,33 @@ struct BwAcc {
 };
 
 // One bucket's stream.  SOFT = false: the tile carries no soft-count gradient,
-// so only blended pairs contribute; sPB.w holds the blend limit n_walk - term.
-// SOFT = true: sPB.w holds n_walk << 1 | terminated and every walked pair with
-// alpha below the cap adds its soft term.
+// so only blended pairs contribute; B.w holds the blend limit n_walk - term.
+// SOFT = true: B.w holds n_walk << 1 | terminated and every walked pair with
+// alpha below the cap adds its soft term.  The pixel list holds byte offsets
+// (p * 16) shared by both per-pixel arrays; the next step's records are
+// fetched one step ahead.
 template <bool SOFT>
-__device__ __forceinline__ void bw_stream(const float4* __restrict__ sPA, const float4* __restrict__ sPB,
+__device__ __forceinline__ void bw_stream(const char* __restrict__ sPAb, const char* __restrict__ sPBb,
                                           const uint16_t* __restrict__ list, const float2* __restrict__ seed,
                                           int n_live, int lane, int k, const BwSplat& s, BwAcc& g) {
   float T = 1.f, H = 0.f;
   const int n_steps = n_live + 31;
+  const bool lane0 = lane == 0;
   int jn = BW_PAD - lane;  // padded list index of step 0
-  int pn = list[jn];
-  float4 PBn = sPB[pn];
+  int on = list[jn];       // byte offset of the pixel's record in sPA / sPB
+  float4 PBn = *reinterpret_cast<const float4*>(sPBb + on), PAn = *reinterpret_cast<const float4*>(sPAb + on);
 #pragma unroll 2
   for (int i = 0; i < n_steps; i++) {
     float Tin = __shfl_up_sync(FULL, T, 1);
     float Hin = __shfl_up_sync(FULL, H, 1);
     const float2 sd = seed[i];  // broadcast read (garbage past n_live: sentinel steps)
-    if (lane == 0) {
-      Tin = sd.x;
-      Hin = sd.y;
-    }
-    T = Tin;
-    H = Hin;
-    const int p = pn;
-    const float4 PB = PBn;
+    T = lane0 ? sd.x : Tin;
+    H = lane0 ? sd.y : Hin;
+    const float4 PB = PBn, w = PAn;
     jn++;
-    pn = list[jn];
-    PBn = sPB[pn];
+    on = list[jn];
+    PBn = *reinterpret_cast<const float4*>(sPBb + on);
+    PAn = *reinterpret_cast<const float4*>(sPAb + on);
     const int lim = __float_as_int(PB.w);
     const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
     const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
@@ -508,7 +507,6 @@ __device__ __forceinline__ void bw_stream(const float4* __restrict__ sPA, const 
       const float araw = pair_alpha2(s.opa, p2);
       if (k < lim && p2 <= 0.f && p2 >= s.p2_min && araw >= ALPHA_MIN_F) {
         const float alpha = fminf(araw, ALPHA_CAP_F);
-        const float4 w = sPA[p];
         const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
         const float aT = alpha * T;
         g.g0 = fmaf(aT, w.x, g.g0);
@@ -536,7 +534,6 @@ __device__ __forceinline__ void bw_stream(const float4* __restrict__ sPA, const 
         const float alpha = capped ? ALPHA_CAP_F : araw;
         // the terminating slot (k == nw - 1 of a terminated walk) is never blended
         const bool blended = alpha >= ALPHA_MIN_F && k < nw - (lim & 1);
-        const float4 w = sPA[p];
         float dlda = 0.f;
         if (blended) {
           const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
@@ -579,10 +576,10 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
 
-  __shared__ float4 sPA[TILE_PX];      // dL/dr, dL/dg, dL/db, dL/dsoft
+  __shared__ float4 sPA[TILE_PX + 1];  // dL/dr, dL/dg, dL/db, dL/dsoft
   __shared__ float4 sPB[TILE_PX + 1];  // pixel x, y (tile-relative), w . image, walk limit; [256] = sentinel
   __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
-  __shared__ uint16_t sList[8][BW_LIST];     // per warp: live pixels of the current bucket, padded
+  __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
   bool soft_px = false;
   {
     const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
@@ -609,10 +606,13 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
     sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(lim));
     if (tid < 8)
       for (int e = 0; e < BW_PAD; e++) {
-        sList[tid][e] = TILE_PX;
-        sList[tid][BW_PAD + TILE_PX + e] = TILE_PX;
+        sList[tid][e] = TILE_PX * sizeof(float4);
+        sList[tid][BW_PAD + TILE_PX + e] = TILE_PX * sizeof(float4);
       }
-    if (tid == 0) sPB[TILE_PX] = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    if (tid == 0) {
+      sPA[TILE_PX] = make_float4(0.f, 0.f, 0.f, 0.f);
+      sPB[TILE_PX] = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    }
     soft_px = us;
   }
   __syncthreads();
@@ -633,14 +633,14 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       const int lim = __float_as_int(sPB[p].w);
       const bool lv = (use_soft ? (lim >> 1) : lim) > kb;
       const unsigned msk = __ballot_sync(FULL, lv);
-      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint16_t)p;
+      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint16_t)(p * sizeof(float4));
       n_live += __popc(msk);
     }
     // sentinels after the live pixels (the padding after 256 entries is fixed)
-    if (n_live + lane < TILE_PX) myList[n_live + lane] = TILE_PX;
+    if (n_live + lane < TILE_PX) myList[n_live + lane] = TILE_PX * sizeof(float4);
     __syncwarp();
     for (int j = lane; j < n_live; j += 32) {
-      const int p = myList[j];
+      const int p = myList[j] / sizeof(float4);
       float2 sd = make_float2(1.f, 0.f);
       if (b > 0) {
         const float4 c = ckt[(size_t)b * TILE_PX + p];
@@ -679,10 +679,12 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       s.p2_min = use_soft ? FAR_POWER2 : fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / s.opa));
     }
     BwAcc g = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const char* pab = reinterpret_cast<const char*>(sPA);
+    const char* pbb = reinterpret_cast<const char*>(sPB);
     if (use_soft)
-      bw_stream<true>(sPA, sPB, sList[warp], mySeed, n_live, lane, k, s, g);
+      bw_stream<true>(pab, pbb, sList[warp], mySeed, n_live, lane, k, s, g);
     else
-      bw_stream<false>(sPA, sPB, sList[warp], mySeed, n_live, lane, k, s, g);
+      bw_stream<false>(pab, pbb, sList[warp], mySeed, n_live, lane, k, s, g);
     if (live) {
       float* r = rows + (size_t)orow * 9;
       r[0] = g.g0;
