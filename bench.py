@@ -281,20 +281,55 @@ def main():
     value = world * args.steps / (ms / 1e3)
 
     # ---------------- end to end through the public API with host buffers
+    # Every step copies its target image from pinned host memory (H2D) and reads
+    # its loss terms back (D2H).  The H2D of step k+1 runs on a copy stream
+    # while step k computes (double-buffered, ordered by events); step k's
+    # loss read is consumed on the host one step later.
     pinned = [t.cpu().pin_memory() for t in targets]
-    dbuf = torch.empty_like(targets[0])
+    dbuf = [torch.empty_like(targets[0]) for _ in range(2)]
+    host_vals = [torch.empty(5, dtype=torch.float64).pin_memory() for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    main_stream = torch.cuda.current_stream()
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    read_done = [torch.cuda.Event() for _ in range(2)]
+    losses_seen = []
+
+    def view_of(k):
+        return ((args.warmup + args.steps + k) * world + rank) % len(cams)
+
+    def prefetch(k):
+        b = k % 2
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(consumed[b])  # the step that last read this buffer is done with it
+            dbuf[b].copy_(pinned[view_of(k)], non_blocking=True)
+            loaded[b].record(copy_stream)
+
     barrier()
     torch.cuda.synchronize()
+    for e in consumed:
+        e.record(main_stream)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
+    prefetch(0)
     for k in range(args.steps):
-        i = ((args.warmup + args.steps + k) * world + rank) % len(cams)
-        dbuf.copy_(pinned[i], non_blocking=True)
-        br = step(args.warmup + args.steps + k, target=dbuf)
-        _ = br.values.cpu()  # loss terms back to the host (40 bytes)
+        b = k % 2
+        main_stream.wait_event(loaded[b])
+        if k + 1 < args.steps:
+            prefetch(k + 1)
+        br = step(args.warmup + args.steps + k, target=dbuf[b])
+        consumed[b].record(main_stream)
+        host_vals[b].copy_(br.values, non_blocking=True)  # loss terms back to the host (40 bytes)
+        read_done[b].record(main_stream)
+        if k > 0:
+            read_done[1 - b].synchronize()
+            losses_seen.append(float(host_vals[1 - b][3]))
+    read_done[(args.steps - 1) % 2].synchronize()
+    losses_seen.append(float(host_vals[(args.steps - 1) % 2][3]))
     f1.record()
     torch.cuda.synchronize()
     barrier()
+    assert len(losses_seen) == args.steps and all(np.isfinite(losses_seen))
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
