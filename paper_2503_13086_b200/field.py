@@ -199,14 +199,29 @@ class GaussianField:
         existing centres and the new points (exact k-NN on the GPU grid index,
         spatial.py); identity rotation; logit(init_opacity); DC from colour.
         """
+        usable = [p for p in points if p.finite]
+        if not usable:
+            return 0
+        return self.insert_arrays(np.stack([p.position for p in usable]), np.stack([p.color for p in usable]),
+                                  init_opacity)
+
+    def insert_arrays(self, positions, colors, init_opacity: float = 0.1) -> int:
+        """insert_points for (n, 3) position / colour arrays (host or device);
+        rows with a non-finite value are skipped like non-finite SparsePoints."""
         from .spatial import mean_knn_scale
 
-        usable = [p for p in points if p.finite]
-        n_new = len(usable)
+        dev = self.device
+        as_t = lambda x: (x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x, dtype=np.float64))).to(
+            device=dev, dtype=torch.float64).reshape(-1, 3)
+        new_pos, cols = as_t(positions), as_t(colors)
+        if new_pos.shape[0] != cols.shape[0]:
+            raise InvalidParameter("positions and colors must have the same number of rows")
+        ok = torch.isfinite(new_pos).all(dim=1) & torch.isfinite(cols).all(dim=1)
+        if not bool(ok.all()):
+            new_pos, cols = new_pos[ok], cols[ok]
+        n_new = int(new_pos.shape[0])
         if n_new == 0:
             return 0
-        dev = self.device
-        new_pos = torch.tensor(np.stack([p.position for p in usable]), dtype=torch.float64, device=dev)
         # exact 3-NN over (existing centres + new points) on the GPU grid index
         mean_d = mean_knn_scale(self.positions.double() if self._n else None, new_pos)
         K = self.n_sh_coeffs
@@ -215,7 +230,6 @@ class GaussianField:
         rot[:, 0] = 1.0
         logit = torch.full((n_new,), math.log(init_opacity / (1.0 - init_opacity)), dtype=torch.float64, device=dev)
         sh = torch.zeros(n_new, 3, K, dtype=torch.float64, device=dev)
-        cols = torch.tensor(np.stack([p.color for p in usable]), dtype=torch.float64, device=dev)
         sh[:, :, 0] = (cols - 0.5) / SH_C0
         self._append([new_pos, rot, log_scales, logit, sh])
         self.generation += 1
@@ -223,16 +237,18 @@ class GaussianField:
         return n_new
 
     def _append(self, parts):
-        old = [getattr(self, k) for k in CLASSES] if self._n else None
+        """Grow the flat buffer by parts' rows (each class region copied once)."""
         n_add = parts[0].shape[0]
-        cat = []
-        for i, p in enumerate(parts):
-            p = p.to(dtype=torch.float32).reshape(n_add, -1)
-            if old is not None:
-                p = torch.cat([old[i].reshape(self._n, -1), p])
-            cat.append(p)
-        self._flat = pack_classes(cat, self._n + n_add, self.n_sh_coeffs, self.device)
-        self._n += n_add
+        n_old, k = self._n, self.n_sh_coeffs
+        n_tot = n_old + n_add
+        flat = torch.empty(flat_size(n_tot, k), dtype=torch.float32, device=self.device)
+        old_sl, new_sl = class_slices(n_old, k), class_slices(n_tot, k)
+        for (o_off, w), (n_off, _), part in zip(old_sl, new_sl, parts):
+            if n_old:
+                flat[n_off: n_off + w * n_old] = self._flat[o_off: o_off + w * n_old]
+            flat[n_off + w * n_old: n_off + w * n_tot] = part.reshape(-1).to(dtype=torch.float32)
+        self._flat = flat
+        self._n = n_tot
 
     def densify_and_prune(self, grad_stats, opts: DensifyOptions, rng, optimizer=None) -> DensifySummary:
         """Clone/split hot Gaussians and prune transparent ones (field.py:303-375).

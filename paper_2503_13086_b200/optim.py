@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from .errors import InvalidParameter, StaleFieldError
-from .field import CLASSES, class_slices, pack_classes
+from .field import CLASSES, class_slices, flat_size, pack_classes
 
 BETA1 = 0.9
 BETA2 = 0.999
@@ -58,7 +58,15 @@ class FieldOptimizer:
 
     def sync(self, fld, keep_mask, n_added):
         """Track a densify/prune: kept rows keep their moments, new rows start cold (optim.py:101-111)."""
-        keep = torch.as_tensor(np.asarray(keep_mask, dtype=bool), device=self.m.device)
+        keep_np = np.asarray(keep_mask, dtype=bool)
+        if keep_np.all():  # pure growth (field expansion): copy the regions, new rows start cold
+            self.m, self.v = self._grow(self.m, int(n_added)), self._grow(self.v, int(n_added))
+            self.n_rows += int(n_added)
+            self._generation = fld.generation
+            if self.n_rows != len(fld):
+                raise InvalidParameter(f"remap produced {self.n_rows} rows, field has {len(fld)}")
+            return
+        keep = torch.as_tensor(keep_np, device=self.m.device)
         n_new = int(keep.sum().item()) + int(n_added)
         newm, newv = [], []
         for name in CLASSES:
@@ -72,6 +80,13 @@ class FieldOptimizer:
         self._generation = fld.generation
         if self.n_rows != len(fld):
             raise InvalidParameter(f"remap produced {self.n_rows} rows, field has {len(fld)}")
+
+    def _grow(self, buf, n_added):
+        n, k = self.n_rows, (self.sh_degree + 1) ** 2
+        out = torch.zeros(flat_size(n + n_added, k), dtype=buf.dtype, device=buf.device)
+        for (o_off, w), (n_off, _) in zip(class_slices(n, k), class_slices(n + n_added, k)):
+            out[n_off: n_off + w * n] = buf[o_off: o_off + w * n]
+        return out
 
     def step(self, fld, grads, position_rate):
         """Apply one update; position_rate comes from the lr scheduler (optim.py:113-130)."""

@@ -94,10 +94,9 @@ def main():
         spread = rng.normal(0.0, 1.0, (args.per_event, 3)) * (0.35 * depth)[:, None]
         pos = cam.center[None, :] + depth[:, None] * fwd[None, :] + spread
         cols = rng.uniform(0.0, 1.0, (args.per_event, 3))
-        pts = [SparsePoint(p, c) for p, c in zip(pos, cols)]
         t1 = time.perf_counter()
         n_old = len(state.field)
-        state.field.insert_points(pts)
+        state.field.insert_arrays(pos, cols)
         keep = np.ones(n_old, dtype=bool)
         state.optimizer.sync(state.field, keep, len(state.field) - n_old)
         state.stats = torch.cat([state.stats[:n_old], torch.zeros(len(state.field) - n_old, device=state.stats.device),
