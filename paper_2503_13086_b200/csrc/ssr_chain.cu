@@ -60,36 +60,56 @@ __device__ __forceinline__ float adam_step(float p, float g, float& m, float& v,
 
 // ------------------------------------------------------------------ merge of large splats
 // Rows of Gaussians touching more than MERGE_BIG tiles (large splats, up to
-// thousands of tiles) are summed by a whole warp -- coalesced strided loads,
-// fixed-order tree reduction -- into the Gaussian's first row, so the chain's
-// per-thread merge stays bounded.  One warp per 32 rows.
+// thousands of tiles) are summed into the Gaussian's first row before the
+// chain, so the chain's per-thread merge stays bounded.  One CTA per 32 field
+// rows; each large row is summed by the whole CTA (threads striding the row
+// range, two rows in flight each, coalesced), reduced in a fixed order (warp
+// shuffles, then the warp partials in order): a splat covering much of the
+// image no longer serialises on one warp.
 constexpr uint32_t MERGE_BIG = 32;
+constexpr int MERGE_THREADS = 128;
 
-__global__ void __launch_bounds__(256) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
-                                                   const uint32_t* __restrict__ roff, float* __restrict__ rows) {
-  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
-  const int lane = threadIdx.x & 31;
-  if (g0 >= n) return;
+__global__ void __launch_bounds__(MERGE_THREADS) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
+                                                             const uint32_t* __restrict__ roff,
+                                                             float* __restrict__ rows) {
+  __shared__ float s_part[MERGE_THREADS / 32][9];
+  const int64_t g0 = (int64_t)blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gi = g0 + lane;
   const uint32_t mine = gi < n ? tiles[gi] : 0u;
-  unsigned big = __ballot_sync(FULLMASK, mine > MERGE_BIG);
+  unsigned big = __ballot_sync(FULLMASK, mine > MERGE_BIG);  // identical in every warp
   while (big) {
     const int l = __ffs(big) - 1;
     big &= big - 1;
     const uint32_t nt = __shfl_sync(FULLMASK, mine, l);
     float* rw = rows + (int64_t)roff[g0 + l] * 9;
     float acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t j = lane; j < nt; j += 32)
+    uint32_t j = threadIdx.x;
+    for (; j + MERGE_THREADS < nt; j += 2 * MERGE_THREADS) {
+      float v0[9], v1[9];
+#pragma unroll
+      for (int c = 0; c < 9; c++) {
+        v0[c] = rw[(int64_t)j * 9 + c];
+        v1[c] = rw[(int64_t)(j + MERGE_THREADS) * 9 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 9; c++) acc[c] += v0[c] + v1[c];
+    }
+    if (j < nt)
 #pragma unroll
       for (int c = 0; c < 9; c++) acc[c] += rw[(int64_t)j * 9 + c];
 #pragma unroll
-    for (int c = 0; c < 9; c++)
+    for (int c = 0; c < 9; c++) {
       for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(FULLMASK, acc[c], o);
-    __syncwarp();
-    if (lane == 0)
-#pragma unroll
-      for (int c = 0; c < 9; c++) rw[c] = acc[c];
-    __syncwarp();
+      if (lane == 0) s_part[warp][c] = acc[c];
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      float v = 0.f;
+      for (int w = 0; w < MERGE_THREADS / 32; w++) v += s_part[w][threadIdx.x];
+      rw[threadIdx.x] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -621,7 +641,7 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
                         int32_t accumulate, float* stats, const AdamArgsF& adam, cudaStream_t st) {
   const CamF c = to_camf(*cam);
   const int K = (sh_degree + 1) * (sh_degree + 1);
-  k_merge_big<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
+  k_merge_big<<<(unsigned)((n + 31) / 32), MERGE_THREADS, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
   SSR_TRY(check_launch("k_merge_big"));
   const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
   k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, 0, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
