@@ -64,6 +64,8 @@ typedef struct ssr_splats {
   uint32_t* offset;    /* N      first instance id: tiles scanned in (fp64 depth, row) order */
   uint32_t* row_offset; /* N     first gradient row: tiles scanned in field-row order, so a
                             block of consecutive rows owns one contiguous range of inst_rows */
+  uint32_t* depth_order; /* N    field row of the r-th Gaussian in (fp64 depth, row) order (culled
+                            rows last); written by ssr_scan_tiles, read by ssr_bin_tiles */
 } ssr_splats;
 
 /* Render-time per-pixel / per-tile state retained for the backward. */

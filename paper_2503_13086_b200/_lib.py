@@ -29,7 +29,7 @@ class SsrCamera(ctypes.Structure):
 
 class SsrSplats(ctypes.Structure):
     _fields_ = [(k, c_void_p) for k in ("mean", "conic_opa", "color", "conic_opa64", "color64", "depth",
-                                        "rect", "tiles", "offset", "row_offset")]
+                                        "rect", "tiles", "offset", "row_offset", "depth_order")]
 
 
 class SsrFrame(ctypes.Structure):

@@ -90,41 +90,78 @@ __global__ void k_zero_total(uint32_t* total) {
 }
 
 // Every field row writes its tiles at its depth-ordered offset; emission order
-// inside a row is ty-outer / tx-inner (projection.py:175-182).  Rows with at
-// most DUP_SMALL tiles are written by their own thread; larger rows (big
-// splats, up to thousands of tiles) by the whole warp, lane-strided and
-// coalesced, so one large splat no longer serialises its warp.
-constexpr uint32_t DUP_SMALL = 16;
+// inside a row is ty-outer / tx-inner (projection.py:175-182).  Two roles per
+// thread r:
+//  * small Gaussians (<= DUP_SMALL tiles) in depth order (depth_order[r]): a
+//    warp's 32 consecutive ranks own (up to the large ones among them) one
+//    contiguous output range, so the warp enumerates its small instances
+//    k = 0 .. sum-1 (lane-order prefix of the counts, 5-step shuffle search)
+//    and lanes write consecutive slots: coalesced stores;
+//  * large Gaussians in field-row order (row r): written by the whole warp,
+//    lane-strided over the Gaussian's own contiguous range.  Field order
+//    spreads adjacent-in-depth large splats over different warps.
+constexpr uint32_t DUP_SMALL = 32;
 
 __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const uint32_t* __restrict__ tiles,
                                                    const uint32_t* __restrict__ offset, const int4* __restrict__ rect,
-                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                   const uint32_t* __restrict__ order, uint32_t* __restrict__ keys,
+                                                   uint32_t* __restrict__ vals) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const uint32_t nt = i < n ? tiles[i] : 0u;
-  if (nt > 0 && nt <= DUP_SMALL) {
-    const int4 r = rect[i];
-    uint32_t o = offset[i];
-    for (int ty = r.y; ty < r.w; ty++) {
-      const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
-      for (int tx = r.x; tx < r.z; tx++) {
-        keys[o] = row + (uint32_t)tx;
-        vals[o] = (uint32_t)i;
-        o++;
+  const unsigned FULLM = 0xffffffffu;
+  // ---- small Gaussians, depth order
+  {
+    uint32_t g = 0, cnt = 0, off = 0;
+    int4 rc = make_int4(0, 0, 1, 1);
+    if (r < n) {
+      g = order[r];
+      cnt = tiles[g];
+      if (cnt > DUP_SMALL) cnt = 0;  // written by the field-order role
+      if (cnt) {
+        off = offset[g];
+        rc = rect[g];
+      }
+    }
+    uint32_t incl = cnt;  // inclusive prefix of the small counts in lane order
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(FULLM, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const uint32_t total = __shfl_sync(FULLM, incl, 31);
+    const uint32_t excl = incl - cnt;
+    const uint32_t w = (uint32_t)(rc.z - rc.x);
+    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      // last lane whose exclusive prefix <= k (for k < total that lane has a
+      // nonzero count: a zero-count lane shares its prefix with the next lane)
+      int src = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t e = __shfl_sync(FULLM, excl, src + step);
+        if (e <= k) src += step;
+      }
+      const uint32_t se = __shfl_sync(FULLM, excl, src), so = __shfl_sync(FULLM, off, src);
+      const uint32_t sw = __shfl_sync(FULLM, w, src), sg = __shfl_sync(FULLM, g, src);
+      const int sx = __shfl_sync(FULLM, rc.x, src), sy = __shfl_sync(FULLM, rc.y, src);
+      if (k < total) {
+        const uint32_t q = k - se;
+        keys[so + q] = ((uint32_t)sy + q / sw) * (uint32_t)tiles_x + (uint32_t)sx + q % sw;
+        vals[so + q] = sg;
       }
     }
   }
-  unsigned big = __ballot_sync(0xffffffffu, nt > DUP_SMALL);
+  // ---- large Gaussians, field-row order, warp-cooperative
+  const uint32_t nt = r < n ? tiles[r] : 0u;
+  unsigned big = __ballot_sync(FULLM, nt > DUP_SMALL);
   while (big) {
     const int l = __ffs(big) - 1;
     big &= big - 1;
-    const int64_t g = i - lane + l;
-    const int4 r = rect[g];
+    const int64_t g = r - lane + l;
+    const int4 rc = rect[g];
     const uint32_t o = offset[g];
-    const uint32_t w = (uint32_t)(r.z - r.x), cnt = __shfl_sync(0xffffffffu, nt, l);
+    const uint32_t w = (uint32_t)(rc.z - rc.x), cnt = __shfl_sync(FULLM, nt, l);
     for (uint32_t j = lane; j < cnt; j += 32) {
-      const uint32_t ty = (uint32_t)r.y + j / w, tx = (uint32_t)r.x + j % w;
-      keys[o + j] = ty * (uint32_t)tiles_x + tx;
+      keys[o + j] = ((uint32_t)rc.y + j / w) * (uint32_t)tiles_x + (uint32_t)rc.x + j % w;
       vals[o + j] = (uint32_t)g;
     }
   }
@@ -218,6 +255,9 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb, cnt, off_sorted, (int)n, st), "scan tiles"));
   k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev);
   SSR_TRY(check_launch("k_scatter_offsets"));
+  if (splats.depth_order)
+    SSR_TRY(check_cuda(cudaMemcpyAsync(splats.depth_order, order, 4 * n, cudaMemcpyDeviceToDevice, st),
+                       "depth order"));
   // gradient-row offsets in field-row order (contiguous per block of rows for the chain)
   size_t sb2 = scan_temp_bytes(n);
   return check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb2, splats.tiles, splats.row_offset, (int)n, st),
@@ -255,8 +295,13 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   uint32_t* vals_in = (uint32_t*)(w + 2 * a);
   const int bits = tile_bits(n_tiles);
   size_t temp = sort32_temp_bytes(m, bits);
+  if (!splats.depth_order) {
+    set_error("ssr_bin_tiles: splats.depth_order (from ssr_scan_tiles) is required");
+    return SSR_ERR_INVALID;
+  }
   k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, tiles_x, splats.tiles, splats.offset,
-                                                           (const int4*)splats.rect, keys_in, vals_in);
+                                                           (const int4*)splats.rect, splats.depth_order, keys_in,
+                                                           vals_in);
   SSR_TRY(check_launch("k_duplicate"));
   SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)(w + 3 * a), temp, keys_in, keys_out, vals_in, inst_gauss,
                                                      (int)m, 0, bits, st),

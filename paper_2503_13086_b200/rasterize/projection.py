@@ -44,7 +44,7 @@ class ProjectedSplats:
     def struct(self) -> _lib.SsrSplats:
         s = _lib.SsrSplats()
         for k in ("mean", "conic_opa", "color", "conic_opa64", "color64", "depth", "rect", "tiles", "offset",
-                  "row_offset"):
+                  "row_offset", "depth_order"):
             setattr(s, k, self.bufs[k].data_ptr() if self.bufs[k].numel() else None)
         return s
 
@@ -132,7 +132,7 @@ def _alloc_splats(n: int, dev) -> dict:
     return dict(mean=e(n, 2, dt=torch.float64), conic_opa=e(n, 4), color=e(n, 4),
                 conic_opa64=e(n, 4, dt=torch.float64), color64=e(n, 4, dt=torch.float64),
                 depth=e(n, dt=torch.float64), rect=e(n, 4, dt=torch.int32), tiles=e(n, dt=torch.int32),
-                offset=e(n, dt=torch.int32), row_offset=e(n, dt=torch.int32))
+                offset=e(n, dt=torch.int32), row_offset=e(n, dt=torch.int32), depth_order=e(n, dt=torch.int32))
 
 
 def project_field(field, cam: CameraFrame) -> ProjectedSplats:
