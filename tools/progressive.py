@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--per-event", type=int, default=20_000)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--fused", type=int, default=1, help="chain + Adam in one pass (backward_and_step)")
+    ap.add_argument("--profile", action="store_true",
+                    help="after the events, one more iteration inside cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off captures just that iteration)")
     ap.add_argument("--paper-weights", action="store_true",
                     help="losses.py defaults (load 0.41) instead of BASELINE's L1 + 0.2 D-SSIM")
     args = ap.parse_args()
@@ -139,6 +142,17 @@ def main():
                               expand_s=t2 - t1, iterations_s=t3 - t2, ms_per_iteration=(t3 - t2) / len(plan) * 1e3,
                               psnr_renders_s=t_psnr0 + (time.perf_counter() - t3)))
         print(json.dumps(per_event[-1]), flush=True)
+    if args.profile:
+        v = n_views - 1
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from bucket_stats import stats
+
+        print(json.dumps({"bucket_stats": stats(render(state.field, cams[v]))}), flush=True)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        train_iteration(state, cams[v], targets[v], 1.6e-4, fused=bool(args.fused))
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     print(json.dumps({"metric": "seconds per new image (config 3, final field size)",
                       "value": float(np.mean([p["seconds"] for p in per_event])), "unit": "s/image",
                       "events": len(per_event), "field_final": len(state.field),
