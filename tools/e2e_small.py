@@ -1,6 +1,6 @@
 """Small end-to-end run of every entry point: render, loss, both backward
 layouts, chain, Adam, fused chain+Adam, densify, PLY pack/unpack on config-0/1
-sized scenes.  compute-sanitizer --tool memcheck|racecheck python tools/sanitize.py"""
+sized scenes (a quick crash / error check: python tools/e2e_small.py)."""
 import os
 import sys
 import tempfile
