@@ -218,10 +218,12 @@ int ssr_ply_unpack(int64_t n, int32_t sh_degree, const double* records, float* p
 
 /* ---------------------------------------------------------- loss */
 /* losses.py:55-173: w_l1 * L1 + w_ssim * (1 - SSIM) + w_load * std(soft).
+ * target: H x W x 3 float32 in [0, 1], or 8-bit (target_u8 != 0; value / 255,
+ * like the reference's image loader io/images.py).
  * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,
  * total, hard_count_std) as float64 in device memory. */
 int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes);
-int ssr_loss(int32_t width, int32_t height, const float* image, const float* target,
+int ssr_loss(int32_t width, int32_t height, const float* image, const void* target, int32_t target_u8,
              const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim,
              double w_load, float* d_image, float* d_soft, double* out, void* workspace,
              int64_t workspace_bytes, void* stream);

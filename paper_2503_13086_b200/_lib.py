@@ -78,7 +78,7 @@ _SIGS = {
     "ssr_ply_pack": [c_int64, c_int32, c_void_p, c_void_p, c_void_p],
     "ssr_ply_unpack": [c_int64, c_int32, c_void_p, c_void_p, c_void_p],
     "ssr_loss_workspace": [c_int32, c_int32, ctypes.POINTER(c_int64)],
-    "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
+    "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_double, c_double, c_double,
                  c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
 }
 _RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_fix_list_ints": c_int64,

@@ -24,6 +24,16 @@ struct LossAcc {
 
 __constant__ float c_win[11];
 
+// Target pixels: float32 in [0, 1], or 8-bit (the reference's image files are
+// 8-bit; io/images.py divides by 255) converted on load.
+struct Target {
+  const void* p;
+  int u8;
+  __device__ __forceinline__ float operator[](size_t i) const {
+    return u8 ? (float)reinterpret_cast<const uint8_t*>(p)[i] * (1.f / 255.f) : reinterpret_cast<const float*>(p)[i];
+  }
+};
+
 __device__ __forceinline__ double block_sum64(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -46,7 +56,7 @@ constexpr int VSEG = 4;                 // vertical outputs per thread (32 x 8 =
 constexpr int HZS = LT + 1;             // padded row stride of the horizontal results
 
 __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
-                                                  const float* __restrict__ tgt, const double* __restrict__ soft,
+                                                  const Target tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
                                                   LossAcc* acc) {
   __shared__ float sx[LH][LH + 1], sy[LH][LH + 1];
@@ -198,7 +208,7 @@ __global__ void k_loss_finalize(int W, int H, double w_l1, double w_ssim, double
 }
 
 __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __restrict__ img,
-                                                  const float* __restrict__ tgt, const double* __restrict__ soft,
+                                                  const Target tgt, const double* __restrict__ soft,
                                                   const float* __restrict__ dmaps, const LossAcc* __restrict__ acc,
                                                   double w_l1, double w_ssim, double w_load,
                                                   float* __restrict__ d_image, float* __restrict__ d_soft) {
@@ -311,7 +321,7 @@ extern "C" int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes)
   return SSR_OK;
 }
 
-extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const float* target,
+extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const void* target, int32_t target_u8,
                         const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim, double w_load,
                         float* d_image, float* d_soft, double* out, void* workspace, int64_t workspace_bytes,
                         void* stream) {
@@ -331,11 +341,12 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   LossAcc* acc = (LossAcc*)((char*)workspace + align_up((int64_t)9 * width * height * 4, 256));
   SSR_TRY(check_cuda(cudaMemsetAsync(acc, 0, sizeof(LossAcc), st), "loss acc"));
   dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
-  k_ssim_fwd<<<grid, 256, 0, st>>>(width, height, image, target, soft_count, hard_count, dmaps, acc);
+  const Target tg{target, target_u8 ? 1 : 0};
+  k_ssim_fwd<<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
   SSR_TRY(check_launch("k_ssim_fwd"));
   k_loss_finalize<<<1, 32, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, acc, out);
   SSR_TRY(check_launch("k_loss_finalize"));
-  k_ssim_bwd<<<grid, 256, 0, st>>>(width, height, image, target, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
+  k_ssim_bwd<<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
                                    d_image, d_soft);
   return check_launch("k_ssim_bwd");
 }

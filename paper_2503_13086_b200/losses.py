@@ -63,7 +63,10 @@ class _Workspace:
 
 
 def total_loss(rendered, target, output, weights: LossWeights) -> LossBreakdown:
-    """Weighted objective over one rendered view (losses.py:147-173)."""
+    """Weighted objective over one rendered view (losses.py:147-173).
+
+    ``target`` is float in [0, 1] or uint8 (value / 255, as the reference's
+    io/images.py loads its 8-bit image files)."""
     rendered = torch.as_tensor(rendered)
     target = torch.as_tensor(target)
     if tuple(rendered.shape) != tuple(target.shape) or rendered.dim() != 3 or rendered.shape[2] != 3:
@@ -73,14 +76,17 @@ def total_loss(rendered, target, output, weights: LossWeights) -> LossBreakdown:
         raise InvalidParameter(f"image {h}x{w} smaller than the 11-tap SSIM window")
     dev = output.image.device
     x = rendered.to(device=dev, dtype=torch.float32).contiguous()
-    y = target.to(device=dev, dtype=torch.float32).contiguous()
+    # an 8-bit target (the reference's image files; value / 255) is read as is
+    u8 = target.dtype == torch.uint8
+    y = target.to(device=dev).contiguous() if u8 else target.to(device=dev, dtype=torch.float32).contiguous()
     soft = output.soft_count.to(dtype=torch.float64).contiguous()
     hard = output.hard_count.to(dtype=torch.int32).contiguous()
     d_image = torch.empty_like(x)
     d_soft = torch.empty(soft.shape, dtype=torch.float32, device=dev)
     vals = torch.empty(5, dtype=torch.float64, device=dev)
     ws = _Workspace.get(w, h, dev)
-    _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), soft.data_ptr(), hard.data_ptr(), float(weights.l1),
+    _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), 1 if u8 else 0, soft.data_ptr(), hard.data_ptr(),
+              float(weights.l1),
               float(weights.ssim), float(weights.load), d_image.data_ptr(), d_soft.data_ptr(), vals.data_ptr(),
               ws.data_ptr(), ws.numel(), _lib.stream_ptr())
     return LossBreakdown(vals, d_image, d_soft)

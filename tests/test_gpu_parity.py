@@ -235,3 +235,22 @@ def test_fused_chain_adam_matches_backward_then_step(deg, n):
         assert bad.mean() < 1e-3, (name, bad.mean())
         assert np.abs(pb - pa).max() <= 3 * step, name
     np.testing.assert_allclose(b.stats.cpu().numpy(), a.stats.cpu().numpy(), rtol=1e-5, atol=1e-8)
+
+
+@pytest.mark.gpu
+def test_loss_accepts_8bit_target():
+    """total_loss with a uint8 target == with the float target value/255 (io/images.py)."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.losses import LossWeights, total_loss
+    from paper_2503_13086_b200.rasterize import render
+
+    f = GaussianField.from_host(scenes.make_params(0, seed=2, n=3000))
+    out = render(f, scenes.camera(0, view=1, width=72, height=56))
+    t8 = torch.randint(0, 256, (56, 72, 3), dtype=torch.uint8, device="cuda")
+    tf = t8.float() * torch.tensor(1.0 / 255.0, dtype=torch.float32, device="cuda")
+    for w in (LossWeights(), LossWeights(l1=1.0, ssim=0.2, load=0.0)):
+        a, b = total_loss(out.image, t8, out, w), total_loss(out.image, tf, out, w)
+        assert a.total == pytest.approx(b.total, rel=1e-6)
+        assert float((a.d_image - b.d_image).abs().max()) <= 1e-6 * float(b.d_image.abs().max()) + 1e-12
