@@ -254,3 +254,37 @@ def test_loss_accepts_8bit_target():
         a, b = total_loss(out.image, t8, out, w), total_loss(out.image, tf, out, w)
         assert a.total == pytest.approx(b.total, rel=1e-6)
         assert float((a.d_image - b.d_image).abs().max()) <= 1e-6 * float(b.d_image.abs().max()) + 1e-12
+
+
+def test_insert_arrays_matches_insert_points_and_skips_nonfinite():
+    from paper_2503_13086_b200 import SparsePoint
+
+    g = load_golden("expansion")
+    pos, col = g["exp_cand_pos"], g["exp_cand_col"]
+    f1, f2 = _field(g), _field(g)
+    n1 = f1.insert_points([SparsePoint(p, c) for p, c in zip(pos, col)])
+    bad_pos = np.concatenate([pos, [[np.nan, 0.0, 0.0]]])
+    bad_col = np.concatenate([col, [[0.5, 0.5, 0.5]]])
+    n2 = f2.insert_arrays(bad_pos, bad_col)
+    assert n1 == n2 == len(pos)
+    assert f1.checksum() == f2.checksum() and f1.generation == f2.generation
+
+
+def test_optimizer_growth_keeps_moments_and_cold_starts_new_rows():
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.field import CLASSES
+    from paper_2503_13086_b200.optim import FieldOptimizer
+
+    f = GaussianField.from_host(scenes.make_params(1, seed=4, n=777))
+    opt = FieldOptimizer(f, 2.0)
+    opt.m.copy_(torch.rand_like(opt.m))
+    opt.v.copy_(torch.rand_like(opt.v))
+    before = {k: [t.clone() for t in opt.moments(k)] for k in CLASSES}
+    n_add = f.insert_arrays(np.random.default_rng(1).normal(size=(13, 3)), np.full((13, 3), 0.5))
+    opt.sync(f, np.ones(777, dtype=bool), n_add)
+    assert opt.n_rows == len(f) == 790
+    for k in CLASSES:
+        for old, new in zip(before[k], opt.moments(k)):
+            assert bool((new[:777] == old).all()) and bool((new[777:] == 0).all()), k
