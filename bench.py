@@ -66,7 +66,7 @@ def _views(args):
 class ClockSampler:
     """nvidia-smi equivalent via NVML, sampled during the timed region."""
 
-    def __init__(self, dev_index=0, period=0.1):
+    def __init__(self, dev_index=0, period=0.01):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period, self._stop, self._t = period, threading.Event(), None
         try:
