@@ -142,6 +142,13 @@ def test_full_config_vs_oracle(cfg, oracle_lib):
     gr = backward(f, out, d_img, d_soft)
     r = grads_report(gr, ref_g)
     assert grads_ok(r), r
+    # the training configuration's path: no soft-count gradient (load weight 0,
+    # d_soft all zero), where the backward skips pairs below 1/255
+    ref_g0 = oracle_lib.backward(P, ref_out, d_img.astype(np.float64), np.zeros((cam.height, cam.width)))
+    r0 = grads_report(backward(f, out, d_img, np.zeros((cam.height, cam.width), np.float32)), ref_g0)
+    assert grads_ok(r0), r0
+    r1 = grads_report(backward(f, out, d_img, None), ref_g0)
+    assert grads_ok(r1), r1
 
 
 # ---------------------------------------------------------------- field expansion
