@@ -43,7 +43,8 @@ def _args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fused", type=int, default=0, help="1: chain + Adam in one pass (backward_and_step)")
+    ap.add_argument("--fused", type=int, default=1,
+                    help="1 (default): chain + Adam in one pass (backward_and_step); 0: backward() + optimizer.step()")
     ap.add_argument("--e2e-target", default="u8", choices=["u8", "f32"],
                     help="e2e upload of each step's target image: 8-bit like the reference's image files "
                          "(io/images.py; read natively by the loss kernels) or float32")
@@ -358,10 +359,12 @@ def main():
     if rank != 0:
         return
     # ---------------- roofline of the dominant kernel
-    P = 0
+    P = M = 0
     for c in cams:
-        P += int(render(state.field, c).n_walk.sum().item())
-    P_mean = P / len(cams)
+        o = render(state.field, c)
+        P += int(o.n_walk.sum().item())
+        M += o.splats.n_instances
+    P_mean, M_mean = P / len(cams), M / len(cams)
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks = {}
     try:
@@ -391,20 +394,33 @@ def main():
                         f" flop x {P_mean / 1e6:.1f} M walked pairs"}
     # HBM roofline of the streaming Adam pass (7 x S bytes per row: p, g, m, v
     # read; p, m, v written) against the measured copy bandwidth
+    # HBM roofline of the streaming optimizer pass against the measured copy
+    # bandwidth: k_adam moves 7 x S bytes per row (p, g, m, v read; p, m, v
+    # written); the fused chain+Adam 6 x S bytes per row plus the 36-byte
+    # instance rows it merges
     roofline_hbm = None
-    adam_ms = stage_ms.get("ssr_adam")
-    if adam_ms:
-        s_bytes = 4 * (11 + 3 * (field.sh_degree + 1) ** 2)
-        adam_bytes = 7.0 * s_bytes * len(state.field)
+    s_bytes = 4 * (11 + 3 * (field.sh_degree + 1) ** 2)
+    n_rows = len(state.field)
+    if stage_ms.get("ssr_adam"):
+        kname, kms = "ssr_adam (k_adam)", stage_ms["ssr_adam"]
+        kbytes = 7.0 * s_bytes * n_rows
+        work = f"7 x {s_bytes} B x {n_rows:,} rows"
+    elif stage_ms.get("ssr_chain_adam"):
+        kname, kms = "ssr_chain_adam (k_merge_big + k_chain_geo + k_chain_sh, fused Adam)", stage_ms["ssr_chain_adam"]
+        kbytes = 6.0 * s_bytes * n_rows + 36.0 * M_mean
+        work = f"6 x {s_bytes} B x {n_rows:,} rows + 36 B x {M_mean:,.0f} instance rows"
+    else:
+        kms = None
+    if kms:
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        ach = adam_bytes / (adam_ms / 1e3) / 1e9
-        roofline_hbm = {"bound": "hbm", "kernel": "ssr_adam (k_adam)", "achieved": ach, "peak": hbm_peak,
-                        "unit": "GB/s", "frac": ach / hbm_peak,
-                        "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
-                        "work": f"{adam_bytes / 1e9:.3f} GB per launch = 7 x {s_bytes} B x {len(state.field):,} rows",
-                        "traffic": None}
+        ach = kbytes / (kms / 1e3) / 1e9
+        roofline_hbm = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": ach / hbm_peak, "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                        "work": f"{kbytes / 1e9:.3f} GB per launch = {work}", "traffic": None}
         try:
-            roofline_hbm["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("ssr_adam")
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            roofline_hbm["traffic"] = tr.get("ssr_adam") if "k_adam" in kname else (
+                (tr.get("ssr_chain_sh_fused") or 0) + (tr.get("ssr_chain_geo_fused") or 0) or None)
         except Exception:
             pass
     cpu = None

@@ -59,13 +59,14 @@ def densify(state: TrainState) -> None:
 
 
 def train_iteration(state: TrainState, cam, target, position_rate: float, bg=(0.0, 0.0, 0.0),
-                    fused: bool = False) -> LossBreakdown:
+                    fused: bool = True) -> LossBreakdown:
     """One iteration of the hot path on one view (pipeline.py:185-206).
 
-    Goes through FieldGrads exactly like the reference's backward + step calls.
-    ``fused=True`` uses backward_and_step (one chain+Adam pass, no gradient
-    buffer); it is verified equal but not yet faster (its TMA staging is not
-    double-buffered), so it is off by default.
+    ``fused=True`` (default) runs backward_and_step: the chain applies the
+    dense Adam step in the same pass, without materialising FieldGrads (same
+    math as the reference's backward + step calls; tests/test_gpu_parity.py
+    checks the two agree).  ``fused=False`` goes through FieldGrads exactly like
+    the reference's backward + step calls.
     """
     out = render(state.field, cam, bg=bg)
     br = total_loss(out.image, target, out, state.weights)
