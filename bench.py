@@ -43,6 +43,9 @@ def _args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--progressive-events", type=int, default=2,
+                    help="also time the progressive loop (config 3, seconds per new image) over this many "
+                         "events after one warm-up event; 0 skips it (single GPU only)")
     ap.add_argument("--fused", type=int, default=1,
                     help="1 (default): chain + Adam in one pass (backward_and_step); 0: backward() + optimizer.step()")
     ap.add_argument("--e2e-target", default="u8", choices=["u8", "f32"],
@@ -429,6 +432,28 @@ def main():
             cpu = cpu_baseline(cfg, views)
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "error": str(ex)}
+    # ---------------- seconds per new image (BASELINE metric, second half): config 3
+    progressive = None
+    if world == 1 and args.progressive_events > 0:
+        try:
+            import contextlib
+            import io
+
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import progressive as prog
+
+            del state, targets
+            torch.cuda.empty_cache()
+            with contextlib.redirect_stdout(io.StringIO()):
+                summ = prog.main(["--events", str(args.progressive_events), "--warmup-events", "1"])
+            progressive = {"metric": "seconds per new image", "value": summ["value"], "unit": "s/image",
+                           "higher_is_better": False, "events": summ["events"],
+                           "ms_per_iteration": summ["ms_per_iteration"], "field": summ["field_final"],
+                           "config": "config 3: 1297x840, +20k Gaussians per image, 200 iterations per image "
+                                     "(Local & Semi-Global plan stand-in), expansion + 2 PSNR renders included, "
+                                     "wall clock"}
+        except Exception as ex:  # pragma: no cover
+            progressive = {"error": str(ex)}
     h2d = int(pinned[0].numel() * pinned[0].element_size())
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -445,6 +470,7 @@ def main():
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40,
                 "target": f"{args.e2e_target} image uploaded every step (copy stream, overlapped); loss read back"},
         "gpu_launches": launches,
+        "progressive": progressive,
         "clocks": clk.summary(),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if not k.endswith("workspace")},
     }

@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--events", type=int, default=3)
     ap.add_argument("--warmup-events", type=int, default=1,
@@ -40,7 +40,12 @@ def main():
                          "(ncu --profile-from-start off captures just that iteration)")
     ap.add_argument("--paper-weights", action="store_true",
                     help="losses.py defaults (load 0.41) instead of BASELINE's L1 + 0.2 D-SSIM")
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main(argv=None):
+    """Run the events; prints one JSON line per event and a summary line, returns the summary."""
+    args = parse_args(argv)
     import torch
 
     from paper_2503_13086_b200 import GaussianField, SparsePoint, scenes
@@ -153,10 +158,13 @@ def main():
         train_iteration(state, cams[v], targets[v], 1.6e-4, fused=bool(args.fused))
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-    print(json.dumps({"metric": "seconds per new image (config 3, final field size)",
-                      "value": float(np.mean([p["seconds"] for p in per_event])), "unit": "s/image",
-                      "events": len(per_event), "field_final": len(state.field),
-                      "width": cams[0].width, "height": cams[0].height, "t_i": args.t_i}), flush=True)
+    summary = {"metric": "seconds per new image (config 3, final field size)",
+               "value": float(np.mean([p["seconds"] for p in per_event])), "unit": "s/image",
+               "events": len(per_event), "field_final": len(state.field),
+               "width": cams[0].width, "height": cams[0].height, "t_i": args.t_i,
+               "ms_per_iteration": float(np.mean([p["ms_per_iteration"] for p in per_event]))}
+    print(json.dumps(summary), flush=True)
+    return summary
 
 
 if __name__ == "__main__":
