@@ -262,7 +262,8 @@ __device__ __forceinline__ bool project64(const Cam& cam, const float* pos, cons
   o.txc = tx < -limx ? -limx : (tx > limx ? limx : tx);
   o.tyc = ty < -limy ? -limy : (ty > limy ? limy : ty);
   // field.py:71-75  Sigma = M M^T, M = R(q) diag(exp(s))
-  double q[4] = {(double)quat[0], (double)quat[1], (double)quat[2], (double)quat[3]};
+  const float4 q4 = *reinterpret_cast<const float4*>(quat);  // rotation rows are 16-byte aligned
+  double q[4] = {(double)q4.x, (double)q4.y, (double)q4.z, (double)q4.w};
   quat_rotmat64(q, o.rot, o.qn, &o.qnorm);
   double m[9], cw[9];
   for (int j = 0; j < 3; j++) o.sc[j] = exp((double)ls[j]);
@@ -322,9 +323,22 @@ __device__ __forceinline__ void sh_color64(const Cam& cam, int deg, const float*
   *rs = r > 1e-12 ? r : 1e-12;
   for (int j = 0; j < 3; j++) dir[j] = off[j] / *rs;
   sh_basis64(deg, dir, basis);
+  // degree 3: the row's 48 coefficients as 12 aligned float4 loads (rows are
+  // 192 B, class regions 16-byte aligned), issued together
+  float cf[48];
+  if (K == 16) {
+#pragma unroll
+    for (int q = 0; q < 12; q++) {
+      const float4 v = reinterpret_cast<const float4*>(shrow)[q];
+      cf[4 * q] = v.x;
+      cf[4 * q + 1] = v.y;
+      cf[4 * q + 2] = v.z;
+      cf[4 * q + 3] = v.w;
+    }
+  }
   for (int c = 0; c < 3; c++) {
     double acc = 0.0;
-    for (int k = 0; k < K; k++) acc += (double)shrow[c * K + k] * basis[k];
+    for (int k = 0; k < K; k++) acc += (double)(K == 16 ? cf[c * 16 + k] : shrow[c * K + k]) * basis[k];
     double raw = acc + 0.5;
     lo[c] = raw < 0.0;
     hi[c] = raw > 1.0;
