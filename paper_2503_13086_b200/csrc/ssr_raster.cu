@@ -505,7 +505,9 @@ __device__ __forceinline__ void bw_stream(const char* __restrict__ sPAb, const c
     const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
     if (!SOFT) {
       const float araw = pair_alpha2(s.opa, p2);
-      if (k < lim && p2 <= 0.f && p2 >= s.p2_min && araw >= ALPHA_MIN_F) {
+      // (araw >= 1/255 implies p2 >= p2_min: no separate far test here; lanes
+      // past the walks have opacity 0)
+      if (k < lim && p2 <= 0.f && araw >= ALPHA_MIN_F) {
         const float alpha = fminf(araw, ALPHA_CAP_F);
         const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
         const float aT = alpha * T;
