@@ -295,3 +295,44 @@ def test_optimizer_growth_keeps_moments_and_cold_starts_new_rows():
     for k in CLASSES:
         for old, new in zip(before[k], opt.moments(k)):
             assert bool((new[:777] == old).all()) and bool((new[777:] == 0).all()), k
+
+
+@pytest.mark.parametrize("case", ["deep_lists", "opaque_big", "low_opacity_deep"])
+def test_stress_cases_vs_oracle(case, oracle_lib):
+    """Long tile lists (many 256-splat batches, dozens of 32-slot buckets and
+    checkpoints), large opaque splats (early termination, huge rect merges) and
+    very low opacities (walks through whole lists): GPU vs the float64 oracle."""
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.camera import CameraFrame, look_at
+    from paper_2503_13086_b200.rasterize import backward, render
+
+    rng = np.random.default_rng({"deep_lists": 11, "opaque_big": 12, "low_opacity_deep": 13}[case])
+    n = 6000
+    hp = scenes.make_params(1, seed=5, n=n)
+    hp.positions[:] = rng.uniform(-0.6, 0.6, (n, 3)).astype(np.float32)
+    if case == "deep_lists":
+        hp.log_scales[:] = rng.normal(-1.6, 0.3, (n, 3)).astype(np.float32)
+        hp.opacity_logits[:] = rng.normal(-3.0, 1.0, n).astype(np.float32)
+    elif case == "opaque_big":
+        hp.log_scales[:] = rng.normal(-1.0, 0.3, (n, 3)).astype(np.float32)
+        hp.opacity_logits[:] = rng.normal(4.0, 1.0, n).astype(np.float32)
+    else:
+        hp.log_scales[:] = rng.normal(-1.3, 0.2, (n, 3)).astype(np.float32)
+        hp.opacity_logits[:] = np.full(n, -6.5, np.float32)
+    rot, tr = look_at(np.array([0.3, -0.2, -3.0]), np.zeros(3))
+    cam = CameraFrame(1, 96, 80, 90.0, 90.0, 48.0, 40.0, rot, tr)
+    P = oracle_lib.Params(*(getattr(hp, k).astype(np.float64) for k in GRAD_CLASSES))
+    ref = oracle_lib.render(P, cam)
+    f = GaussianField.from_host(hp)
+    out = render(f, cam)
+    assert all(v for k, v in projection_report(out.splats, ref["splats"]).items() if k.endswith("_equal"))
+    fr = forward_report(out, ref)
+    assert forward_ok(fr), fr
+    assert int(out.n_walk.max()) > 300, "case does not produce deep walks"
+    d_img = (rng.standard_normal((80, 96, 3)) * 1e-3).astype(np.float32)
+    for d_soft in (None, (rng.standard_normal((80, 96)) * 1e-4).astype(np.float32)):
+        ds = np.zeros((80, 96)) if d_soft is None else d_soft.astype(np.float64)
+        ref_g = oracle_lib.backward(P, ref, d_img.astype(np.float64), ds)
+        for layout in ("splat", "pixel"):
+            r = grads_report(backward(f, out, d_img, d_soft, layout=layout), ref_g)
+            assert grads_ok(r), (layout, d_soft is None, r)
