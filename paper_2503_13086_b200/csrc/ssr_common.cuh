@@ -421,13 +421,14 @@ __device__ __forceinline__ float pair_alpha2(float opa, float power2) { return _
 // same ~0.403 term.
 constexpr double SOFT_S0 = 0.4031981879117929;
 constexpr float SOFT_Y0 = 0.25f;
-__device__ __forceinline__ float soft_dev_poly(float y) {
+// Accumulates y p(y) into acc with one final FMA (acc += y * p(y)).
+__device__ __forceinline__ float soft_dev_acc(float y, float acc) {
   float p = 1.76897e-03f;
   p = __fmaf_rn(p, y, -3.74327e-03f);
   p = __fmaf_rn(p, y, -1.778797e-02f);
   p = __fmaf_rn(p, y, 2.329284e-02f);
   p = __fmaf_rn(p, y, 2.4062942e-01f);
-  return __fmul_rn(y, p);
+  return __fmaf_rn(y, p, acc);
 }
 
 __device__ __forceinline__ float soft_sigmoid_accurate(float alpha) {

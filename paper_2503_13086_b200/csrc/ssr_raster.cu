@@ -115,7 +115,7 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
     // soft-count deviation
     const float y = __fmul_rn(alpha, 100.f);
     if (y < SOFT_Y0) {
-      q.sdev += soft_dev_poly(y);
+      q.sdev = soft_dev_acc(y, q.sdev);
       continue;
     }
     if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
