@@ -9,7 +9,7 @@ timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?
 timeout 600 python bench.py --fused 0 --no-cpu-baseline > $O/bench_unfused.json 2> $O/bench_unfused.err; echo "bench_unfused exit $?" >> $O/status.txt
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "bench_ref exit $?" >> $O/status.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/ncu_bench.log 2>&1; echo "ncu_launch_bench exit $?" >> $O/status.txt
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --progressive-events 0 > $O/ncu_bench.log 2>&1; echo "ncu_launch_bench exit $?" >> $O/status.txt
 SSR_CFG=3 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
   python tools/profile_step.py > $O/ncu_c3.log 2>&1; echo "ncu_launch_c3 exit $?" >> $O/status.txt
 bash tools/ncu_kernels.sh $O "k_forward$" k_backward_splat k_adam k_chain_geo k_chain_sh k_preprocess k_ssim_fwd k_backward_fixup k_forward_fixup
