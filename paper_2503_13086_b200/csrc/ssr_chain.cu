@@ -18,8 +18,12 @@
 //    channel's coefficients, read and written as coalesced float4 streams
 //    straight from HBM (no shared-memory transpose); channel sums and the
 //    direction gradient are reduced over the four lanes with shuffles.
-// FUSED (ssr_chain_adam) applies the dense Adam step in place instead of
-// writing FieldGrads: the gradient buffer's write and read disappear.
+// Fused (ssr_chain_adam): the dense Adam step is applied in place instead of
+// writing FieldGrads, so the gradient buffer's write and read disappear.  The
+// geometry kernel then also stages its CTA's rotation / log-scale / logit rows
+// and their moments by TMA, and k_chain_sh_adam (same lane layout as
+// k_chain_sh) stages the SH, position and moment rows: every Adam stream is
+// a few large bulk copies per CTA instead of per-thread loads.
 #include "ssr_common.cuh"
 
 namespace ssr {
@@ -140,12 +144,28 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   const int pad = (int)((b0 - a0) >> 2);
   const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
   const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
+  const int64_t ns = row_stride(n);
+  // fused: the CTA's rotation / log-scale / logit rows and their moments come
+  // in by TMA bulk copies next to the instance rows ([param | m | v] x
+  // [rot 4 | log-scale 3 | logit 1] x CHAIN_ROWS, dynamic shared memory)
+  extern __shared__ __align__(16) float s_adam[];
   if (threadIdx.x == 0) mbar_init(&mbar, 1);
   __syncthreads();
-  if (staged) {
+  if (staged || FUSED) {
     if (threadIdx.x == 0) {
-      mbar_expect_tx(&mbar, (uint32_t)bytes);
-      bulk_g2s(s_rows, reinterpret_cast<const char*>(rows) + a0, (uint32_t)bytes, &mbar);
+      const uint32_t rows4 = (uint32_t)min((int64_t)CHAIN_ROWS, ns - i0);
+      mbar_expect_tx(&mbar, (staged ? (uint32_t)bytes : 0u) + (FUSED ? 3u * 32u * rows4 : 0u));
+      if (staged) bulk_g2s(s_rows, reinterpret_cast<const char*>(rows) + a0, (uint32_t)bytes, &mbar);
+      if (FUSED) {
+        const float* src[3] = {rot, adam.m + 3 * ns, adam.v + 3 * ns};
+        for (int t = 0; t < 3; t++) {
+          const float* base = src[t];  // rotation region; log-scales at +4ns, logits at +7ns
+          float* d = s_adam + t * 8 * CHAIN_ROWS;
+          bulk_g2s(d, base + i0 * 4, rows4 * 16, &mbar);
+          bulk_g2s(d + 4 * CHAIN_ROWS, base + 4 * ns + i0 * 3, rows4 * 12, &mbar);
+          bulk_g2s(d + 7 * CHAIN_ROWS, base + 7 * ns + i0, rows4 * 4, &mbar);
+        }
+      }
     }
     mbar_wait(&mbar, 0);
   }
@@ -161,27 +181,18 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
 #pragma unroll
       for (int c = 0; c < 9; c++) pr[c] += rw[j * 9 + c];
   }
-  const int64_t ns = row_stride(n);
   float* g_pos = grads;
   float* g_rot = grads + 3 * ns;
   float* g_ls = grads + 7 * ns;
   float* g_logit = grads + 10 * ns;
   float* g_screen = grads + (int64_t)S * ns;
   float* g_vis = grads + (int64_t)(S + 1) * ns;
-  const float4 q4 = *reinterpret_cast<const float4*>(rot + i * 4);
-  // fused: the rows' moments are loaded up front so their latency overlaps the chain
-  float4 m_rot, v_rot;
-  float m_ls[3], v_ls[3], m_lo = 0.f, v_lo = 0.f;
-  if (FUSED) {
-    m_rot = *reinterpret_cast<const float4*>(adam.m + 3 * ns + i * 4);
-    v_rot = *reinterpret_cast<const float4*>(adam.v + 3 * ns + i * 4);
-    for (int j = 0; j < 3; j++) {
-      m_ls[j] = adam.m[7 * ns + i * 3 + j];
-      v_ls[j] = adam.v[7 * ns + i * 3 + j];
-    }
-    m_lo = adam.m[10 * ns + i];
-    v_lo = adam.v[10 * ns + i];
-  }
+  const int tr = threadIdx.x;
+  const float* s_p = s_adam;
+  const float* s_m = s_adam + 8 * CHAIN_ROWS;
+  const float* s_v = s_adam + 16 * CHAIN_ROWS;
+  const float4 q4 = FUSED ? *reinterpret_cast<const float4*>(s_p + tr * 4)
+                          : *reinterpret_cast<const float4*>(rot + i * 4);
   float grot[4] = {0.f, 0.f, 0.f, 0.f}, dls[3] = {0.f, 0.f, 0.f}, dpos[3] = {0.f, 0.f, 0.f}, screen = 0.f;
   float* dst = rows + (int64_t)roff[i] * 9;
   if (nt > 0) {
@@ -216,7 +227,8 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
     rm[6] = 2.f * (qx * qz - qw * qy);
     rm[7] = 2.f * (qy * qz + qw * qx);
     rm[8] = 1.f - 2.f * (qx * qx + qy * qy);
-    const float sc[3] = {__expf(ls[i * 3]), __expf(ls[i * 3 + 1]), __expf(ls[i * 3 + 2])};
+    const float* lsr = FUSED ? s_p + 4 * CHAIN_ROWS + tr * 3 : ls + i * 3;
+    const float sc[3] = {__expf(lsr[0]), __expf(lsr[1]), __expf(lsr[2])};
     float m[9], cw[9], tmp[9], cc[9];
 #pragma unroll
     for (int a = 0; a < 3; a++)
@@ -325,6 +337,8 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   const bool vis = nt > 0;
   if (FUSED) {
     // dense Adam: invisible rows step with a zero gradient like the reference
+    float4 m_rot = *reinterpret_cast<const float4*>(s_m + tr * 4);
+    float4 v_rot = *reinterpret_cast<const float4*>(s_v + tr * 4);
     float4 qn;
     qn.x = adam_step(q4.x, grot[0], m_rot.x, v_rot.x, adam.c[1]);
     qn.y = adam_step(q4.y, grot[1], m_rot.y, v_rot.y, adam.c[1]);
@@ -333,12 +347,15 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
     *reinterpret_cast<float4*>(rot + i * 4) = qn;
     *reinterpret_cast<float4*>(adam.m + 3 * ns + i * 4) = m_rot;
     *reinterpret_cast<float4*>(adam.v + 3 * ns + i * 4) = v_rot;
+#pragma unroll
     for (int j = 0; j < 3; j++) {
-      ls[i * 3 + j] = adam_step(ls[i * 3 + j], dls[j], m_ls[j], v_ls[j], adam.c[2]);
-      adam.m[7 * ns + i * 3 + j] = m_ls[j];
-      adam.v[7 * ns + i * 3 + j] = v_ls[j];
+      float mj = s_m[4 * CHAIN_ROWS + tr * 3 + j], vj = s_v[4 * CHAIN_ROWS + tr * 3 + j];
+      ls[i * 3 + j] = adam_step(s_p[4 * CHAIN_ROWS + tr * 3 + j], dls[j], mj, vj, adam.c[2]);
+      adam.m[7 * ns + i * 3 + j] = mj;
+      adam.v[7 * ns + i * 3 + j] = vj;
     }
-    logit_p[i] = adam_step(logit_p[i], pr[3], m_lo, v_lo, adam.c[3]);
+    float m_lo = s_m[7 * CHAIN_ROWS + tr], v_lo = s_v[7 * CHAIN_ROWS + tr];
+    logit_p[i] = adam_step(s_p[7 * CHAIN_ROWS + tr], pr[3], m_lo, v_lo, adam.c[3]);
     adam.m[10 * ns + i] = m_lo;
     adam.v[10 * ns + i] = v_lo;
     if (vis) {
@@ -437,13 +454,13 @@ constexpr int SH_ROWS = SH_THREADS / SH_LANES;
 
 // Lane q of a row owns coefficients k = q*KL + j (j < KL, k < K) of every
 // channel; at SH3 that is one float4 per channel, read and written directly.
-template <int DEG, bool FUSED>
+template <int DEG>
 __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n, float* __restrict__ pos,
                                                          float* __restrict__ sh, const uint32_t* __restrict__ tiles,
                                                          const uint32_t* __restrict__ roff,
                                                          const float4* __restrict__ color,
                                                          const float* __restrict__ rows, float* __restrict__ grads,
-                                                         int accumulate, AdamArgsF adam) {
+                                                         int accumulate) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
   constexpr int KL = (K + 3) / 4;
@@ -456,7 +473,7 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   const bool vis = row_ok && tiles[ii] != 0;
   const float* rw = rows + (vis ? (int64_t)roff[ii] * 9 : 0);
   float* shrow = sh + ii * W;
-  float* grow = FUSED ? nullptr : grads + 11 * ns + ii * W;
+  float* grow = grads + 11 * ns + ii * W;
 
   // the lane's coefficients: c[ch][j] = sh[ch*K + q*KL + j]
   float cf[3][KL];
@@ -475,16 +492,6 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
         cf[ch][j] = k < K ? shrow[ch * K + k] : 0.f;
       }
     }
-  }
-  // fused: start the lane's moments on their way to L2 now; they are loaded
-  // after the direction gradient, when the basis registers are free
-  if (FUSED) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + q * KL));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + q * KL));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + K + q * KL));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + K + q * KL));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.m + 11 * ns + ii * W + 2 * K + q * KL));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(adam.v + 11 * ns + ii * W + 2 * K + q * KL));
   }
   // direction (sh.py:114-124), recomputed by each lane
   const float ox = pos[ii * 3] - cam.center[0], oy = pos[ii * 3 + 1] - cam.center[1],
@@ -533,73 +540,6 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   const float radial = gd[0] * dx + gd[1] * dy + gd[2] * dz;
   const float dpos_sh[3] = {(gd[0] - radial * dx) * irs, (gd[1] - radial * dy) * irs, (gd[2] - radial * dz) * irs};
   if (!row_ok) return;
-  // fused: the lane's moments (and lane 0's position moments)
-  float mf[3][KL], vf[3][KL];
-  float mp[3] = {0.f, 0.f, 0.f}, vp[3] = {0.f, 0.f, 0.f};
-  if (FUSED) {
-    const float* mrow = adam.m + 11 * ns + ii * W;
-    const float* vrow = adam.v + 11 * ns + ii * W;
-#pragma unroll
-    for (int ch = 0; ch < 3; ch++) {
-      if (VEC) {
-        const float4 a4 = *reinterpret_cast<const float4*>(mrow + ch * K + q * 4);
-        const float4 b4 = *reinterpret_cast<const float4*>(vrow + ch * K + q * 4);
-        mf[ch][0] = a4.x, mf[ch][1] = a4.y, mf[ch][2] = a4.z, mf[ch][3] = a4.w;
-        vf[ch][0] = b4.x, vf[ch][1] = b4.y, vf[ch][2] = b4.z, vf[ch][3] = b4.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < KL; j++) {
-          const int k = q * KL + j;
-          mf[ch][j] = k < K ? mrow[ch * K + k] : 0.f;
-          vf[ch][j] = k < K ? vrow[ch * K + k] : 0.f;
-        }
-      }
-    }
-    if (q == 0)
-      for (int d = 0; d < 3; d++) {
-        mp[d] = adam.m[ii * 3 + d];
-        vp[d] = adam.v[ii * 3 + d];
-      }
-  }
-
-  if (FUSED) {
-    // positions: geometric part from the geometry kernel + view-direction part
-    if (q == 0) {
-      for (int d = 0; d < 3; d++) {
-        const float g = vis ? rw[3 + d] + dpos_sh[d] : 0.f;
-        const int64_t e = i * 3 + d;
-        pos[e] = adam_step(pos[e], g, mp[d], vp[d], adam.c[0]);
-        adam.m[e] = mp[d];
-        adam.v[e] = vp[d];
-      }
-    }
-    float* mrow = adam.m + 11 * ns + i * W;
-    float* vrow = adam.v + 11 * ns + i * W;
-    const AdamClassF c_dc = adam.c[4], c_rest = adam.c[5];
-#pragma unroll
-    for (int ch = 0; ch < 3; ch++) {
-      float pn[KL];
-#pragma unroll
-      for (int j = 0; j < KL; j++)
-        pn[j] = adam_step(cf[ch][j], dcol[ch] * bown[j], mf[ch][j], vf[ch][j], (q * KL + j == 0) ? c_dc : c_rest);
-      if (VEC) {
-        *reinterpret_cast<float4*>(shrow + ch * K + q * 4) = make_float4(pn[0], pn[1], pn[2], pn[3]);
-        *reinterpret_cast<float4*>(mrow + ch * K + q * 4) = make_float4(mf[ch][0], mf[ch][1], mf[ch][2], mf[ch][3]);
-        *reinterpret_cast<float4*>(vrow + ch * K + q * 4) = make_float4(vf[ch][0], vf[ch][1], vf[ch][2], vf[ch][3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < KL; j++) {
-          const int k = q * KL + j;
-          if (k < K) {
-            shrow[ch * K + k] = pn[j];
-            mrow[ch * K + k] = mf[ch][j];
-            vrow[ch * K + k] = vf[ch][j];
-          }
-        }
-      }
-    }
-    return;
-  }
   if (q == 0 && vis) {
     float* g_pos = grads + i * 3;
 #pragma unroll
@@ -631,6 +571,181 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   }
 }
 
+// Fused SH chain + Adam with the CTA's parameter, first- and second-moment
+// rows (and the position rows) staged by TMA bulk copies issued at entry: six
+// contiguous ranges per CTA, ~39 KB in flight per CTA at SH3, so the dense
+// Adam stream is not bounded by per-thread load latency.  The per-row gathers
+// of the chain (tile count, merged colour / position gradient, clamp bits)
+// overlap the copies.  Results are stored straight to global memory.
+constexpr int SHA_ROWS = 64;  // 4 lanes per row, 256 threads
+
+template <int DEG>
+__global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh_adam(CamF cam, int64_t n, float* __restrict__ pos,
+                                                              float* __restrict__ sh,
+                                                              const uint32_t* __restrict__ tiles,
+                                                              const uint32_t* __restrict__ roff,
+                                                              const float4* __restrict__ color,
+                                                              const float* __restrict__ rows, AdamArgsF adam) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int W = 3 * K;
+  constexpr int KL = (K + 3) / 4;
+  constexpr bool VEC = (K == 16);
+  extern __shared__ __align__(16) float s_st[];  // sh | m | v  (SHA_ROWS*W each), pos | mpos | vpos (SHA_ROWS*3)
+  __shared__ uint64_t mbar;
+  float* s_sh = s_st;
+  float* s_m = s_st + SHA_ROWS * W;
+  float* s_v = s_st + 2 * SHA_ROWS * W;
+  float* s_p = s_st + 3 * SHA_ROWS * W;
+  float* s_mp = s_p + SHA_ROWS * 3;
+  float* s_vp = s_p + 2 * SHA_ROWS * 3;
+  const int64_t i0 = (int64_t)blockIdx.x * SHA_ROWS;
+  const int64_t ns = row_stride(n);
+  // rows rounded up to 4: the class regions are padded to 4-row strides, so the
+  // byte counts stay multiples of 16 and the copies stay inside each region
+  const int rows4 = (int)min((int64_t)SHA_ROWS, ns - i0);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    const uint32_t bw = (uint32_t)rows4 * W * 4, bp = (uint32_t)rows4 * 12;
+    mbar_expect_tx(&mbar, 3 * bw + 3 * bp);
+    bulk_g2s(s_sh, sh + i0 * W, bw, &mbar);
+    bulk_g2s(s_m, adam.m + 11 * ns + i0 * W, bw, &mbar);
+    bulk_g2s(s_v, adam.v + 11 * ns + i0 * W, bw, &mbar);
+    bulk_g2s(s_p, pos + i0 * 3, bp, &mbar);
+    bulk_g2s(s_mp, adam.m + i0 * 3, bp, &mbar);
+    bulk_g2s(s_vp, adam.v + i0 * 3, bp, &mbar);
+  }
+  const int rl = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int64_t i = i0 + rl;
+  const bool row_ok = i < n;
+  const int64_t ii = row_ok ? i : n - 1;  // out-of-range lanes shadow the last row (shuffles need them)
+  const bool vis = row_ok && tiles[ii] != 0;
+  const float* rw = rows + (vis ? (int64_t)roff[ii] * 9 : 0);
+  // colour gradient through the clamp (sh.py:128-131), masks from the fp64 preprocess
+  float dcol[3] = {0.f, 0.f, 0.f}, gp_geo = 0.f;
+  if (vis) {
+    const int pass = __float_as_int(color[ii].w);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) dcol[ch] = (pass >> ch) & 1 ? rw[ch] : 0.f;
+    if (q < 3) gp_geo = rw[3 + q];
+  }
+  __syncthreads();  // barrier init visible before anyone waits on it
+  mbar_wait(&mbar, 0);
+  const float* srow = s_sh + rl * W;
+  float cf[3][KL];
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    if (VEC) {
+      const float4 v4 = *reinterpret_cast<const float4*>(srow + ch * K + q * 4);
+      cf[ch][0] = v4.x;
+      cf[ch][1] = v4.y;
+      cf[ch][2] = v4.z;
+      cf[ch][3] = v4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < KL; j++) {
+        const int k = q * KL + j;
+        cf[ch][j] = k < K ? srow[ch * K + k] : 0.f;
+      }
+    }
+  }
+  // direction (sh.py:114-124)
+  const float px = s_p[rl * 3], py = s_p[rl * 3 + 1], pz = s_p[rl * 3 + 2];
+  const float ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
+  const float r = sqrtf(ox * ox + oy * oy + oz * oz);
+  const float rs = fmaxf(r, 1e-12f);
+  const float irs = 1.f / rs;
+  const float dx = ox * irs, dy = oy * irs, dz = oz * irs;
+  float basis[16];
+  sh_basis32<DEG>(dx, dy, dz, basis);
+  float bown[KL];
+#pragma unroll
+  for (int j = 0; j < KL; j++) {
+    float b = 0.f;
+#pragma unroll
+    for (int qq = 0; qq < 4; qq++)
+      if (qq * KL + j < K) b = (q == qq) ? basis[qq * KL + j] : b;
+    bown[j] = (q * KL + j < K) ? b : 0.f;
+  }
+  float vfull[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) vfull[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const int qq = k / KL, j = k % KL;
+    const float vk = dcol[0] * cf[0][j] + dcol[1] * cf[1][j] + dcol[2] * cf[2][j];
+    vfull[k] = (q == qq) ? vk : 0.f;
+  }
+  float gd[3];
+  sh_dir_grad32<DEG>(vfull, dx, dy, dz, gd);
+#pragma unroll
+  for (int d = 0; d < 3; d++) {
+    gd[d] += __shfl_xor_sync(FULLMASK, gd[d], 1);
+    gd[d] += __shfl_xor_sync(FULLMASK, gd[d], 2);
+  }
+  if (!row_ok) return;
+  const float radial = gd[0] * dx + gd[1] * dy + gd[2] * dz;
+  // positions: lane q < 3 owns coordinate q (geometric part from k_chain_geo
+  // plus the view-direction part)
+  if (q < 3) {
+    const float gq = q == 0 ? gd[0] : (q == 1 ? gd[1] : gd[2]);
+    const float dq = q == 0 ? dx : (q == 1 ? dy : dz);
+    const float g = vis ? gp_geo + (gq - radial * dq) * irs : 0.f;
+    float mq = s_mp[rl * 3 + q], vq = s_vp[rl * 3 + q];
+    const float pq = q == 0 ? px : (q == 1 ? py : pz);
+    const int64_t e = i * 3 + q;
+    pos[e] = adam_step(pq, g, mq, vq, adam.c[0]);
+    adam.m[e] = mq;
+    adam.v[e] = vq;
+  }
+  float* shrow = sh + i * W;
+  float* mrow = adam.m + 11 * ns + i * W;
+  float* vrow = adam.v + 11 * ns + i * W;
+  const float* smr = s_m + rl * W;
+  const float* svr = s_v + rl * W;
+  const AdamClassF c_dc = adam.c[4], c_rest = adam.c[5];
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    float mf[KL], vf[KL], pn[KL];
+    if (VEC) {
+      const float4 a4 = *reinterpret_cast<const float4*>(smr + ch * K + q * 4);
+      const float4 b4 = *reinterpret_cast<const float4*>(svr + ch * K + q * 4);
+      mf[0] = a4.x, mf[1] = a4.y, mf[2] = a4.z, mf[3] = a4.w;
+      vf[0] = b4.x, vf[1] = b4.y, vf[2] = b4.z, vf[3] = b4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < KL; j++) {
+        const int k = q * KL + j;
+        mf[j] = k < K ? smr[ch * K + k] : 0.f;
+        vf[j] = k < K ? svr[ch * K + k] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KL; j++)
+      pn[j] = adam_step(cf[ch][j], dcol[ch] * bown[j], mf[j], vf[j], (q * KL + j == 0) ? c_dc : c_rest);
+    if (VEC) {
+      *reinterpret_cast<float4*>(shrow + ch * K + q * 4) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+      *reinterpret_cast<float4*>(mrow + ch * K + q * 4) = make_float4(mf[0], mf[1], mf[2], mf[3]);
+      *reinterpret_cast<float4*>(vrow + ch * K + q * 4) = make_float4(vf[0], vf[1], vf[2], vf[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KL; j++) {
+        const int k = q * KL + j;
+        if (k < K) {
+          shrow[ch * K + k] = pn[j];
+          mrow[ch * K + k] = mf[j];
+          vrow[ch * K + k] = vf[j];
+        }
+      }
+    }
+  }
+}
+
+template <int DEG>
+static size_t sh_adam_smem() {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  return (size_t)(3 * SHA_ROWS * 3 * K + 3 * SHA_ROWS * 3) * sizeof(float);
+}
+
 }  // namespace ssr
 
 using namespace ssr;
@@ -644,14 +759,48 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
   k_merge_big<<<(unsigned)((n + 31) / 32), MERGE_THREADS, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
   SSR_TRY(check_launch("k_merge_big"));
   const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
-  k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, 0, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
-                                                    splats.row_offset, rows, grads, 11 + 3 * K, accumulate, stats,
-                                                    adam);
+  const size_t geo_smem = FUSED ? 3 * 8 * CHAIN_ROWS * sizeof(float) : 0;
+  if (FUSED) {
+    static bool attr = false;
+    if (!attr) {
+      SSR_TRY(check_cuda(cudaFuncSetAttribute(k_chain_geo<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)geo_smem),
+                         "k_chain_geo smem"));
+      attr = true;
+    }
+  }
+  k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, geo_smem, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
+                                                           splats.row_offset, rows, grads, 11 + 3 * K, accumulate,
+                                                           stats, adam);
   SSR_TRY(check_launch("k_chain_geo"));
+  if (FUSED) {
+    const unsigned ablocks = (unsigned)((n + SHA_ROWS - 1) / SHA_ROWS);
+#define SSR_SHA(D)                                                                                                \
+  do {                                                                                                            \
+    const size_t sm = sh_adam_smem<D>();                                                                          \
+    static bool attr = false;                                                                                     \
+    if (!attr) {                                                                                                  \
+      SSR_TRY(check_cuda(cudaFuncSetAttribute(k_chain_sh_adam<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                              (int)sm),                                                           \
+                         "k_chain_sh_adam smem"));                                                                \
+      attr = true;                                                                                                \
+    }                                                                                                             \
+    k_chain_sh_adam<D><<<ablocks, SH_THREADS, sm, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset,     \
+                                                        (const float4*)splats.color, rows, adam);                 \
+  } while (0)
+    switch (sh_degree) {
+      case 0: SSR_SHA(0); break;
+      case 1: SSR_SHA(1); break;
+      case 2: SSR_SHA(2); break;
+      default: SSR_SHA(3); break;
+    }
+#undef SSR_SHA
+    return check_launch("k_chain_sh_adam");
+  }
   const unsigned sblocks = (unsigned)((n + SH_ROWS - 1) / SH_ROWS);
 #define SSR_SH(D)                                                                                       \
-  k_chain_sh<D, FUSED><<<sblocks, SH_THREADS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, \
-                                                        (const float4*)splats.color, rows, grads, accumulate, adam)
+  k_chain_sh<D><<<sblocks, SH_THREADS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, \
+                                                 (const float4*)splats.color, rows, grads, accumulate)
   switch (sh_degree) {
     case 0: SSR_SH(0); break;
     case 1: SSR_SH(1); break;

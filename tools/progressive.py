@@ -38,6 +38,8 @@ def parse_args(argv=None):
     ap.add_argument("--profile", action="store_true",
                     help="after the events, one more iteration inside cudaProfilerStart/Stop "
                          "(ncu --profile-from-start off captures just that iteration)")
+    ap.add_argument("--gaps", action="store_true",
+                    help="torch.profiler timeline of the last event's iterations: device busy vs idle")
     ap.add_argument("--paper-weights", action="store_true",
                     help="losses.py defaults (load 0.41) instead of BASELINE's L1 + 0.2 D-SSIM")
     return ap.parse_args(argv)
@@ -118,6 +120,12 @@ def main(argv=None):
         from paper_2503_13086_b200 import _lib
 
         _lib.enable_timers(args.trace)
+        prof = None
+        if args.gaps and e == n_ev - 1:
+            from torch.profiler import ProfilerActivity, profile
+
+            prof = profile(activities=[ProfilerActivity.CUDA])
+            prof.__enter__()
         for k, tv in enumerate(plan):
             tgt = targets.get(int(tv))
             if tgt is None:
@@ -132,6 +140,12 @@ def main(argv=None):
                                   "flagged": int(o.flagged.sum()), "loss": br.total}), flush=True)
         torch.cuda.synchronize()
         t3 = time.perf_counter()
+        if prof is not None:
+            prof.__exit__(None, None, None)
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from gap_profile import analyse
+
+            analyse(prof, len(plan))
         if args.trace:
             st_ms = _lib.timer_ms()
             _lib.enable_timers(False)
