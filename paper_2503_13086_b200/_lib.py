@@ -15,7 +15,7 @@ import torch
 from .errors import ExtensionMissing, InvalidParameter, NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssr.so")
+LIB_PATH = os.environ.get("SSR_LIB") or os.path.join(_HERE, "libssr.so")
 
 c_void_p, c_int32, c_int64, c_double, c_float = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                                   ctypes.c_double, ctypes.c_float)

@@ -24,6 +24,8 @@
 // and their moments by TMA, and k_chain_sh_adam (same lane layout as
 // k_chain_sh) stages the SH, position and moment rows: every Adam stream is
 // a few large bulk copies per CTA instead of per-thread loads.
+#include <climits>
+
 #include "ssr_common.cuh"
 
 namespace ssr {
@@ -64,56 +66,118 @@ __device__ __forceinline__ float adam_step(float p, float g, float& m, float& v,
 
 // ------------------------------------------------------------------ merge of large splats
 // Rows of Gaussians touching more than MERGE_BIG tiles (large splats, up to
-// thousands of tiles) are summed into the Gaussian's first row before the
-// chain, so the chain's per-thread merge stays bounded.  One CTA per 32 field
-// rows; each large row is summed by the whole CTA (threads striding the row
-// range, two rows in flight each, coalesced), reduced in a fixed order (warp
-// shuffles, then the warp partials in order): a splat covering much of the
-// image no longer serialises on one warp.
+// the whole image) are pre-summed before the chain, load-balanced over the
+// instance rows: the rows (field-row order, contiguous per Gaussian) are cut
+// into MERGE_CHUNK-row chunks and every warp takes a contiguous run of chunks.
+// Each large Gaussian's rows inside one chunk are summed by the warp (fixed
+// order: flat coalesced loads, then a shuffle tree) into the first of those
+// rows -- the Gaussian's first row or a chunk boundary.  The geometry kernel
+// adds those heads in ascending order, so the merge is deterministic and no
+// warp waits on another.
 constexpr uint32_t MERGE_BIG = 32;
-constexpr int MERGE_THREADS = 128;
+constexpr uint32_t MERGE_CHUNK = 256;
+constexpr int MERGE_WARPS = 8;
 
-__global__ void __launch_bounds__(MERGE_THREADS) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
-                                                             const uint32_t* __restrict__ roff,
-                                                             float* __restrict__ rows) {
-  __shared__ float s_part[MERGE_THREADS / 32][9];
-  const int64_t g0 = (int64_t)blockIdx.x * 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gi = g0 + lane;
-  const uint32_t mine = gi < n ? tiles[gi] : 0u;
-  unsigned big = __ballot_sync(FULLMASK, mine > MERGE_BIG);  // identical in every warp
-  while (big) {
-    const int l = __ffs(big) - 1;
-    big &= big - 1;
-    const uint32_t nt = __shfl_sync(FULLMASK, mine, l);
-    float* rw = rows + (int64_t)roff[g0 + l] * 9;
-    float acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t j = threadIdx.x;
-    for (; j + MERGE_THREADS < nt; j += 2 * MERGE_THREADS) {
-      float v0[9], v1[9];
+// Sum of nr contiguous instance rows (9 floats each) over a warp: lane l
+// reads rows l, l + 32, ... (two rows, 18 loads, in flight), then a
+// reduce-scatter butterfly over 16 zero-padded channels (16 shuffles instead
+// of 9 x 5).  Lanes 2c and 2c + 1 of the bit-reversed lane order end up with
+// channel c; the return value is the lane's channel sum, *ch its channel.
+__device__ __forceinline__ float merge_rows_warp(const float* __restrict__ rw, uint32_t nr, int lane, int* ch) {
+  float acc[16];
 #pragma unroll
-      for (int c = 0; c < 9; c++) {
-        v0[c] = rw[(int64_t)j * 9 + c];
-        v1[c] = rw[(int64_t)(j + MERGE_THREADS) * 9 + c];
-      }
-#pragma unroll
-      for (int c = 0; c < 9; c++) acc[c] += v0[c] + v1[c];
-    }
-    if (j < nt)
-#pragma unroll
-      for (int c = 0; c < 9; c++) acc[c] += rw[(int64_t)j * 9 + c];
+  for (int c = 0; c < 16; c++) acc[c] = 0.f;
+  uint32_t j = lane;
+  for (; j + 32 < nr; j += 64) {
+    float v0[9], v1[9];
 #pragma unroll
     for (int c = 0; c < 9; c++) {
-      for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(FULLMASK, acc[c], o);
-      if (lane == 0) s_part[warp][c] = acc[c];
+      v0[c] = rw[(int64_t)j * 9 + c];
+      v1[c] = rw[(int64_t)(j + 32) * 9 + c];
     }
-    __syncthreads();
-    if (threadIdx.x < 9) {
-      float v = 0.f;
-      for (int w = 0; w < MERGE_THREADS / 32; w++) v += s_part[w][threadIdx.x];
-      rw[threadIdx.x] = v;
+#pragma unroll
+    for (int c = 0; c < 9; c++) acc[c] += v0[c] + v1[c];
+  }
+  if (j < nr)
+#pragma unroll
+    for (int c = 0; c < 9; c++) acc[c] += rw[(int64_t)j * 9 + c];
+  // level xor 16: keep half 8 channels, receive the partner's copy of them
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+    const bool hi = lane & (2 * w);
+#pragma unroll
+    for (int k = 0; k < w; k++) {
+      const float keep = hi ? acc[w + k] : acc[k];
+      const float give = hi ? acc[k] : acc[w + k];
+      acc[k] = keep + __shfl_xor_sync(FULLMASK, give, 2 * w);
     }
-    __syncthreads();
+  }
+  *ch = ((lane >> 4) & 1) << 3 | ((lane >> 3) & 1) << 2 | ((lane >> 2) & 1) << 1 | ((lane >> 1) & 1);
+  return acc[0] + __shfl_xor_sync(FULLMASK, acc[0], 1);
+}
+
+// First Gaussian whose rows end after instance row `lo` (ends = roff + tiles
+// are non-decreasing): 32-ary warp search, warp-uniform result.
+__device__ __forceinline__ int64_t merge_find(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ roff,
+                                              int64_t n, uint32_t lo, int lane) {
+  int64_t a = 0, b = n - 1;  // the answer is in [a, b]; rows end after lo at b
+  while (b - a >= 32) {
+    const int64_t step = (b - a + 31) / 32;
+    const int64_t p = min(a + (int64_t)lane * step, b);
+    const unsigned m = __ballot_sync(FULLMASK, roff[p] + tiles[p] > lo);
+    if (m & 1u) return a;
+    if (m == 0u) {
+      a = min(a + 31 * step, b) + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      b = min(a + (int64_t)f * step, b);
+      a = a + (int64_t)(f - 1) * step + 1;
+    }
+  }
+  const int64_t p = a + lane;
+  const unsigned m = __ballot_sync(FULLMASK, p <= b && roff[p] + tiles[p] > lo);
+  return a + (__ffs(m) - 1);
+}
+
+__global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
+                                                                const uint32_t* __restrict__ roff,
+                                                                float* __restrict__ rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (int64_t)gridDim.x * MERGE_WARPS;
+  const int64_t w = (int64_t)blockIdx.x * MERGE_WARPS + (threadIdx.x >> 5);
+  const uint32_t m_rows = roff[n - 1] + tiles[n - 1];
+  const int64_t n_chunks = (m_rows + MERGE_CHUNK - 1) / MERGE_CHUNK;
+  const int64_t c0 = w * n_chunks / n_warps, c1 = (w + 1) * n_chunks / n_warps;
+  if (c0 >= c1) return;
+  const uint32_t lo0 = (uint32_t)(c0 * MERGE_CHUNK), hi1 = (uint32_t)min((int64_t)m_rows, c1 * MERGE_CHUNK);
+  int64_t g = merge_find(tiles, roff, n, lo0, lane);
+  while (g < n) {
+    const int64_t gl = g + lane;
+    uint32_t s = UINT32_MAX, nt = 0;
+    if (gl < n) {
+      s = roff[gl];
+      nt = tiles[gl];
+    }
+    const bool in = gl < n && s < hi1;
+    unsigned big = __ballot_sync(FULLMASK, in && nt > MERGE_BIG);
+    while (big) {
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t sl = __shfl_sync(FULLMASK, s, l), el = sl + __shfl_sync(FULLMASK, nt, l);
+      // the Gaussian's rows inside this warp's range, one portion per chunk
+      uint32_t p0 = max(sl, lo0);
+      while (p0 < min(el, hi1)) {
+        const uint32_t p1 = min(min(el, hi1), (p0 / MERGE_CHUNK + 1) * MERGE_CHUNK);
+        float* rw = rows + (int64_t)p0 * 9;
+        int ch;
+        const float v = merge_rows_warp(rw, p1 - p0, lane, &ch);
+        __syncwarp();  // every lane's reads of the head row are done before it is overwritten
+        if (!(lane & 1) && ch < 9) rw[ch] = v;
+        p0 = p1;
+      }
+    }
+    if (__ballot_sync(FULLMASK, in) != FULLMASK) break;
+    g += 32;
   }
 }
 
@@ -175,11 +239,21 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   // more than MERGE_BIG rows were reduced into their first row by k_merge_big
   float pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (nt > 0) {
-    const float* rw = staged ? s_rows + pad + (int64_t)(roff[i] - r_begin) * 9 : rows + (int64_t)roff[i] * 9;
-    const uint32_t nr = nt > MERGE_BIG ? 1u : nt;
-    for (uint32_t j = 0; j < nr; j++)
+    const uint32_t s0 = roff[i];
+    const float* rw = staged ? s_rows + pad + (int64_t)(s0 - r_begin) * 9 : rows + (int64_t)s0 * 9;
+    if (nt <= MERGE_BIG) {
+      for (uint32_t j = 0; j < nt; j++)
 #pragma unroll
-      for (int c = 0; c < 9; c++) pr[c] += rw[j * 9 + c];
+        for (int c = 0; c < 9; c++) pr[c] += rw[j * 9 + c];
+    } else {
+      // k_merge_big left one partial sum per chunk the rows span: the first
+      // row and every chunk boundary inside the range
+#pragma unroll
+      for (int c = 0; c < 9; c++) pr[c] = rw[c];
+      for (uint32_t h = (s0 / MERGE_CHUNK + 1) * MERGE_CHUNK; h < s0 + nt; h += MERGE_CHUNK)
+#pragma unroll
+        for (int c = 0; c < 9; c++) pr[c] += rw[(int64_t)(h - s0) * 9 + c];
+    }
   }
   float* g_pos = grads;
   float* g_rot = grads + 3 * ns;
@@ -756,7 +830,16 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
                         int32_t accumulate, float* stats, const AdamArgsF& adam, cudaStream_t st) {
   const CamF c = to_camf(*cam);
   const int K = (sh_degree + 1) * (sh_degree + 1);
-  k_merge_big<<<(unsigned)((n + 31) / 32), MERGE_THREADS, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
+  static int merge_blocks = 0;
+  if (!merge_blocks) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_merge_big, MERGE_WARPS * 32, 0);
+    merge_blocks = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 4);  // one resident wave
+  }
+  k_merge_big<<<merge_blocks, MERGE_WARPS * 32, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
   SSR_TRY(check_launch("k_merge_big"));
   const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
   const size_t geo_smem = FUSED ? 3 * 8 * CHAIN_ROWS * sizeof(float) : 0;

@@ -8,29 +8,66 @@ namespace ssr {
 
 // projection.py:69-162 + sh.py:114-132 -- one thread per field row.  Templated
 // on the SH degree so the basis stays in registers.
+//
+// STAGED: the CTA's position, rotation, log-scale and SH rows arrive by TMA
+// bulk copies issued at entry (~30 KB per CTA at SH3), so the fp64 math reads
+// shared memory instead of waiting on per-thread loads; used when the class
+// arrays are 16-byte aligned (the flat field layout always is), for every
+// full CTA (the last, partial one reads global memory directly).
+constexpr int PRE_ROWS = 128;
+
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess(Cam cam, int64_t n, int tiles_x, int tiles_y,
-                                                    const float* __restrict__ pos, const float* __restrict__ rot,
-                                                    const float* __restrict__ ls, const float* __restrict__ logit,
-                                                    const float* __restrict__ sh, ssr_splats o) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__host__ __device__ constexpr int pre_stage_floats() {
+  return PRE_ROWS * (3 + 4 + 3 + 3 * (DEG + 1) * (DEG + 1));
+}
+
+template <int DEG, bool STAGED>
+__global__ void __launch_bounds__(PRE_ROWS, 7) k_preprocess(Cam cam, int64_t n, int tiles_x, int tiles_y,
+                                                         const float* __restrict__ pos, const float* __restrict__ rot,
+                                                         const float* __restrict__ ls,
+                                                         const float* __restrict__ logit,
+                                                         const float* __restrict__ sh, ssr_splats o) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  // start the row's SH coefficients on their way to L2 while the fp64
-  // projection runs (culled rows waste 3K floats of L2 fill, visible rows
-  // then read them at L2 latency)
-  {
-    const char* shp = reinterpret_cast<const char*>(sh + i * 3 * K);
-    for (int off = 0; off < 3 * K * 4; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
+  constexpr int W = 3 * K;
+  extern __shared__ __align__(16) float s_pre[];  // rot 4R | pos 3R | log-scale 3R | sh W R
+  __shared__ uint64_t mbar;
+  const int64_t i0 = (int64_t)blockIdx.x * PRE_ROWS;
+  const int64_t i = i0 + threadIdx.x;
+  const bool staged = STAGED && i0 + PRE_ROWS <= n;
+  if (staged) {
+    if (threadIdx.x == 0) {
+      mbar_init(&mbar, 1);
+      constexpr uint32_t bytes = (uint32_t)pre_stage_floats<DEG>() * 4;
+      mbar_expect_tx(&mbar, bytes);
+      bulk_g2s(s_pre, rot + i0 * 4, PRE_ROWS * 16, &mbar);
+      bulk_g2s(s_pre + 4 * PRE_ROWS, pos + i0 * 3, PRE_ROWS * 12, &mbar);
+      bulk_g2s(s_pre + 7 * PRE_ROWS, ls + i0 * 3, PRE_ROWS * 12, &mbar);
+      bulk_g2s(s_pre + 10 * PRE_ROWS, sh + i0 * W, PRE_ROWS * W * 4, &mbar);
+    }
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+  }
+  if (i >= n) return;
+  const int r = threadIdx.x;
+  const float* prow = staged ? s_pre + 4 * PRE_ROWS + r * 3 : pos + i * 3;
+  const float* qrow = staged ? s_pre + r * 4 : rot + i * 4;
+  const float* lrow = staged ? s_pre + 7 * PRE_ROWS + r * 3 : ls + i * 3;
+  const float* shrow = staged ? s_pre + 10 * PRE_ROWS + r * W : sh + i * W;
+  if (!staged) {
+    // start the row's SH coefficients on their way to L2 while the fp64
+    // projection runs (culled rows waste 3K floats of L2 fill, visible rows
+    // then read them at L2 latency)
+    const char* shp = reinterpret_cast<const char*>(shrow);
+    for (int off = 0; off < W * 4; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
   }
   Proj64 P;
-  if (!project64(cam, pos + i * 3, rot + i * 4, ls + i * 3, tiles_x, tiles_y, P)) {
+  if (!project64(cam, prow, qrow, lrow, tiles_x, tiles_y, P)) {
     o.tiles[i] = 0;
     return;
   }
   double dir[3], rs, basis[16], col[3];
   bool lo[3], hi[3];
-  sh_color64(cam, DEG, pos + i * 3, sh + i * 3 * K, dir, &rs, basis, col, lo, hi);
+  sh_color64(cam, DEG, prow, shrow, dir, &rs, basis, col, lo, hi);
   const double opa = 1.0 / (1.0 + exp(-(double)logit[i]));
   reinterpret_cast<double2*>(o.mean)[i] = make_double2(P.u, P.v);
   // near-singular conics (1 - |b|/sqrt(ac) < 1e-3) are the only ones whose fp32
@@ -103,13 +140,29 @@ extern "C" int ssr_preprocess(const ssr_camera* cam, int64_t n, int32_t sh_degre
   if (n == 0) return SSR_OK;
   int tx, ty;
   tile_dims(cam, &tx, &ty);
-  const int threads = 256;
-  const int64_t blocks = (n + threads - 1) / threads;
+  const int64_t blocks = (n + PRE_ROWS - 1) / PRE_ROWS;
   const Cam c = to_cam(*cam);
   cudaStream_t st = (cudaStream_t)stream;
-#define SSR_PRE(D) \
-  k_preprocess<D><<<(unsigned)blocks, threads, 0, st>>>(c, n, tx, ty, positions, rotations, log_scales, opacity_logits, \
-                                                        sh, splats)
+  auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
+  const bool staged = al16(positions) && al16(rotations) && al16(log_scales) && al16(sh);
+#define SSR_PRE(D)                                                                                                 \
+  do {                                                                                                             \
+    if (staged) {                                                                                                  \
+      constexpr size_t sm = (size_t)pre_stage_floats<D>() * sizeof(float);                                        \
+      static bool attr = false;                                                                                    \
+      if (!attr) {                                                                                                 \
+        SSR_TRY(check_cuda(                                                                                        \
+            cudaFuncSetAttribute(k_preprocess<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),     \
+            "k_preprocess smem"));                                                                                 \
+        attr = true;                                                                                               \
+      }                                                                                                            \
+      k_preprocess<D, true><<<(unsigned)blocks, PRE_ROWS, sm, st>>>(c, n, tx, ty, positions, rotations,           \
+                                                                    log_scales, opacity_logits, sh, splats);       \
+    } else {                                                                                                       \
+      k_preprocess<D, false><<<(unsigned)blocks, PRE_ROWS, 0, st>>>(c, n, tx, ty, positions, rotations,           \
+                                                                    log_scales, opacity_logits, sh, splats);       \
+    }                                                                                                              \
+  } while (0)
   switch (sh_degree) {
     case 0: SSR_PRE(0); break;
     case 1: SSR_PRE(1); break;

@@ -166,7 +166,12 @@ def main(argv=None):
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         from bucket_stats import stats
 
-        print(json.dumps({"bucket_stats": stats(render(state.field, cams[v]))}), flush=True)
+        o = render(state.field, cams[v])
+        tl = o.splats.bufs["tiles"][: len(state.field)].long()
+        big = tl[tl > 32]
+        print(json.dumps({"bucket_stats": stats(o), "instances": int(tl.sum()), "visible": int((tl > 0).sum()),
+                          "big_splats": int(big.numel()), "big_rows": int(big.sum()),
+                          "max_tiles": int(tl.max())}), flush=True)
         torch.cuda.synchronize()
         torch.cuda.profiler.start()
         train_iteration(state, cams[v], targets[v], 1.6e-4, fused=bool(args.fused))
