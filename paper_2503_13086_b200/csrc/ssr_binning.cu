@@ -45,15 +45,20 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const uint32_t* _
 }
 
 // Runs of equal fp32 depth keys: insertion sort by fp64 depth (stable, so
-// equal fp64 depths keep field-row order).  Also gathers tiles in depth order.
+// equal fp64 depths keep field-row order).  Also gathers the tile counts in
+// depth order (cnt[s] = tiles[order[s]]) once each position's entry is final:
+// a run's head writes the whole run after sorting it.
 __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t* __restrict__ keys,
-                                                      uint32_t* __restrict__ order, const double* __restrict__ depth) {
+                                                      uint32_t* __restrict__ order, const double* __restrict__ depth,
+                                                      const uint32_t* __restrict__ tiles, uint32_t* __restrict__ cnt) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t key = keys[s];
-  if (key == DEPTH_KEY_CULLED) return;
   const bool head = (s == 0) || (keys[s - 1] != key);
-  if (!head || s + 1 >= n || keys[s + 1] != key) return;
+  if (key == DEPTH_KEY_CULLED || !head || s + 1 >= n || keys[s + 1] != key) {
+    if (key == DEPTH_KEY_CULLED || head) cnt[s] = tiles[order[s]];  // culled or a run of one
+    return;
+  }
   int64_t e = s + 1;
   while (e < n && keys[e] == key) e++;
   for (int64_t a = s + 1; a < e; a++) {
@@ -66,22 +71,19 @@ __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t*
     }
     order[b + 1] = v;
   }
-}
-
-__global__ void __launch_bounds__(256) k_gather_counts(int64_t n, const uint32_t* __restrict__ order,
-                                                       const uint32_t* __restrict__ tiles,
-                                                       uint32_t* __restrict__ cnt) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) cnt[r] = tiles[order[r]];
+  for (int64_t a = s; a < e; a++) cnt[a] = tiles[order[a]];
 }
 
 __global__ void __launch_bounds__(256) k_scatter_offsets(int64_t n, const uint32_t* __restrict__ order,
                                                          const uint32_t* __restrict__ cnt,
                                                          const uint32_t* __restrict__ off_sorted,
-                                                         uint32_t* __restrict__ offset, uint32_t* __restrict__ total) {
+                                                         uint32_t* __restrict__ offset, uint32_t* __restrict__ total,
+                                                         uint32_t* __restrict__ depth_order) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
-  offset[order[r]] = off_sorted[r];
+  const uint32_t g = order[r];
+  offset[g] = off_sorted[r];
+  if (depth_order) depth_order[r] = g;
   if (r == n - 1) *total = off_sorted[r] + cnt[r];
 }
 
@@ -167,20 +169,32 @@ __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const
   }
 }
 
-// searchsorted(left/right) for every tile id from the sorted tile keys.
+// searchsorted(left/right) for every tile id from the sorted tile keys;
+// RANGE_KEYS consecutive keys per thread.
+constexpr int RANGE_KEYS = 8;
+
 __global__ void __launch_bounds__(256) k_ranges(int64_t m, int n_tiles, const uint32_t* __restrict__ keys,
                                                 int32_t* __restrict__ ranges) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= m) return;
-  const int tile = (int)keys[s];
-  const int prev = s > 0 ? (int)keys[s - 1] : -1;
-  if (tile != prev) {
-    for (int t = prev + 1; t <= tile; t++) ranges[2 * t] = (int32_t)s;
-    for (int t = prev < 0 ? 0 : prev; t < tile; t++) ranges[2 * t + 1] = (int32_t)s;
-  }
-  if (s == m - 1) {
-    for (int t = tile + 1; t < n_tiles; t++) ranges[2 * t] = (int32_t)m;
-    for (int t = tile; t < n_tiles; t++) ranges[2 * t + 1] = (int32_t)m;
+  const int64_t s0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RANGE_KEYS;
+  if (s0 >= m) return;
+  int prev = s0 > 0 ? (int)keys[s0 - 1] : -1;
+  uint32_t kk[RANGE_KEYS];
+#pragma unroll
+  for (int j = 0; j < RANGE_KEYS; j++) kk[j] = s0 + j < m ? keys[s0 + j] : 0u;
+#pragma unroll
+  for (int j = 0; j < RANGE_KEYS; j++) {
+    const int64_t s = s0 + j;
+    if (s >= m) break;
+    const int tile = (int)kk[j];
+    if (tile != prev) {
+      for (int t = prev + 1; t <= tile; t++) ranges[2 * t] = (int32_t)s;
+      for (int t = prev < 0 ? 0 : prev; t < tile; t++) ranges[2 * t + 1] = (int32_t)s;
+    }
+    if (s == m - 1) {
+      for (int t = tile + 1; t < n_tiles; t++) ranges[2 * t] = (int32_t)m;
+      for (int t = tile; t < n_tiles; t++) ranges[2 * t + 1] = (int32_t)m;
+    }
+    prev = tile;
   }
 }
 
@@ -247,17 +261,13 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)temp, tb, keys_in, keys_out, vals_in, order, (int)n, 0,
                                                      DEPTH_KEY_BITS, st),
                      "depth sort"));
-  k_depth_tiefix<<<blocks, 256, 0, st>>>(n, keys_out, order, splats.depth);
+  k_depth_tiefix<<<blocks, 256, 0, st>>>(n, keys_out, order, splats.depth, splats.tiles, cnt);
   SSR_TRY(check_launch("k_depth_tiefix"));
-  k_gather_counts<<<blocks, 256, 0, st>>>(n, order, splats.tiles, cnt);
-  SSR_TRY(check_launch("k_gather_counts"));
   size_t sb = scan_temp_bytes(n);
   SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb, cnt, off_sorted, (int)n, st), "scan tiles"));
-  k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev);
+  k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev,
+                                            splats.depth_order);
   SSR_TRY(check_launch("k_scatter_offsets"));
-  if (splats.depth_order)
-    SSR_TRY(check_cuda(cudaMemcpyAsync(splats.depth_order, order, 4 * n, cudaMemcpyDeviceToDevice, st),
-                       "depth order"));
   // gradient-row offsets in field-row order (contiguous per block of rows for the chain)
   size_t sb2 = scan_temp_bytes(n);
   return check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb2, splats.tiles, splats.row_offset, (int)n, st),
@@ -306,7 +316,8 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)(w + 3 * a), temp, keys_in, keys_out, vals_in, inst_gauss,
                                                      (int)m, 0, bits, st),
                      "tile sort"));
-  k_ranges<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, n_tiles, keys_out, tile_ranges);
+  const int64_t rthreads = (m + RANGE_KEYS - 1) / RANGE_KEYS;
+  k_ranges<<<(unsigned)((rthreads + 255) / 256), 256, 0, st>>>(m, n_tiles, keys_out, tile_ranges);
   return check_launch("k_ranges");
 }
 

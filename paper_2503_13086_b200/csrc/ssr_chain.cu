@@ -183,10 +183,16 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, co
 
 // ------------------------------------------------------------------ geometry chain
 constexpr int CHAIN_ROWS = 128;
-constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
+#ifndef GEO_ROWS_STAGE
+#define GEO_ROWS_STAGE 1
+#endif
+constexpr int CHAIN_STAGE_FLOATS = GEO_ROWS_STAGE ? 9 * 1024 : 4;
 
 template <bool FUSED>
-__global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
+#ifndef GEO_MINB
+#define GEO_MINB 1
+#endif
+__global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
                                                           float* __restrict__ rot, float* __restrict__ ls,
                                                           float* __restrict__ logit_p,
                                                           const uint32_t* __restrict__ tiles,
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
   const int pad = (int)((b0 - a0) >> 2);
   const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
-  const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
+  const bool staged = GEO_ROWS_STAGE && n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
   const int64_t ns = row_stride(n);
   // fused: the CTA's rotation / log-scale / logit rows and their moments come
   // in by TMA bulk copies next to the instance rows ([param | m | v] x
