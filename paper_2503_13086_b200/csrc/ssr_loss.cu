@@ -25,14 +25,17 @@ struct LossAcc {
 __constant__ float c_win[11];
 
 // Target pixels: float32 in [0, 1], or 8-bit (the reference's image files are
-// 8-bit; io/images.py divides by 255) converted on load.
+// 8-bit; io/images.py divides by 255) converted on load.  The kernels are
+// templated on the format, so the per-element test is resolved at compile time.
 struct Target {
   const void* p;
   int u8;
-  __device__ __forceinline__ float operator[](size_t i) const {
-    return u8 ? (float)reinterpret_cast<const uint8_t*>(p)[i] * (1.f / 255.f) : reinterpret_cast<const float*>(p)[i];
-  }
 };
+
+template <bool U8>
+__device__ __forceinline__ float tgt_at(const Target& t, int i) {
+  return U8 ? (float)reinterpret_cast<const uint8_t*>(t.p)[i] * (1.f / 255.f) : reinterpret_cast<const float*>(t.p)[i];
+}
 
 __device__ __forceinline__ double block_sum64(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -55,6 +58,7 @@ constexpr int HITEMS = LH * (LT / HSEG);  // 168
 constexpr int VSEG = 4;                 // vertical outputs per thread (32 x 8 = 256 items)
 constexpr int HZS = LT + 1;             // padded row stride of the horizontal results
 
+template <bool U8>
 __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
                                                   const Target tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
@@ -72,17 +76,39 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
 #pragma unroll
   for (int t = 0; t < 11; t++) wv[t] = c_win[t];
   double l1 = 0.0, ss = 0.0;
+  // the thread's halo columns (lane and lane + 32 < LH), fixed for every row
+  const int ca = tid & 31, cb = ca + 32;
+  const int gca = c0 - HALO + ca, gcb = c0 - HALO + cb;
+  const bool ina = gca >= 0 && gca < W, inb = cb < LH && gcb >= 0 && gcb < W;
   for (int ch = 0; ch < 3; ch++) {
-    // 8 rows x 32 columns per pass, no div/mod per element
-    for (int r = tid >> 5; r < LH; r += 8) {
-      const int gr = r0 - HALO + r;
-      const bool rin = gr >= 0 && gr < H;
-      for (int c = tid & 31; c < LH; c += 32) {
-        const int gc = c0 - HALO + c;
-        const bool in = rin && gc >= 0 && gc < W;
-        const size_t pi = (size_t)gr * W + gc;
-        sx[r][c] = in ? img[pi * 3 + ch] : 0.f;
-        sy[r][c] = in ? tgt[pi * 3 + ch] : 0.f;
+    const float* imc = img + ch;
+    float* dm0 = dmaps + (size_t)(ch * 3 + 0) * HW;
+    float* dm1 = dmaps + (size_t)(ch * 3 + 1) * HW;
+    float* dm2 = dmaps + (size_t)(ch * 3 + 2) * HW;
+    // two rows per pass, all eight loads issued before the stores
+    for (int r = tid >> 5; r < LH; r += 16) {
+      float v[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int rr = r + 8 * u;
+        const int gr = r0 - HALO + rr;
+        const bool rin = rr < LH && gr >= 0 && gr < H;
+        const int row = gr * W;
+        v[u][0] = rin && ina ? imc[3 * (row + gca)] : 0.f;
+        v[u][1] = rin && ina ? tgt_at<U8>(tgt, 3 * (row + gca) + ch) : 0.f;
+        v[u][2] = rin && inb ? imc[3 * (row + gcb)] : 0.f;
+        v[u][3] = rin && inb ? tgt_at<U8>(tgt, 3 * (row + gcb) + ch) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int rr = r + 8 * u;
+        if (rr >= LH) break;
+        sx[rr][ca] = v[u][0];
+        sy[rr][ca] = v[u][1];
+        if (cb < LH) {
+          sx[rr][cb] = v[u][2];
+          sy[rr][cb] = v[u][3];
+        }
       }
     }
     __syncthreads();
@@ -128,6 +154,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
           mom[k][o] = v;
         }
       }
+      float l1f = 0.f, ssf = 0.f;  // <= 4 terms per channel: fp32 partials, fp64 from here on
 #pragma unroll
       for (int o = 0; o < VSEG; o++) {
         const int r = rs + o;
@@ -137,22 +164,25 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
         const float vx = gx2 - mx * mx, vy = gy2 - my * my, cv = gxy - mx * my;
         const float a1 = 2.f * mx * my + C1, a2 = 2.f * cv + C2;
         const float b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
-        const float smap = (a1 * a2) / (b1 * b2);
+        const float i1 = __frcp_rn(b1), i2 = __frcp_rn(b2), i12 = i1 * i2;
+        const float smap = (a1 * a2) * i12;
         const bool crop = gr >= HALO && gr < H - HALO && gc >= HALO && gc < W - HALO;
-        const size_t pi = (size_t)gr * W + gc;
+        const int pi = gr * W + gc;
         float dmu = 0.f, dg2 = 0.f, dxy = 0.f;
         if (crop) {
-          ss += (double)smap;
+          ssf += smap;
           const float m = (float)mw;
-          dmu = m * (2.f * my * (a2 - a1) / (b1 * b2) - 2.f * mx * smap * (1.f / b1 - 1.f / b2));
-          dg2 = m * (-smap / b2);
-          dxy = m * (2.f * a1 / (b1 * b2));
+          dmu = m * (2.f * my * (a2 - a1) * i12 - 2.f * mx * smap * (i1 - i2));
+          dg2 = m * (-smap * i2);
+          dxy = m * (2.f * a1 * i12);
         }
-        dmaps[(size_t)(ch * 3 + 0) * HW + pi] = dmu;
-        dmaps[(size_t)(ch * 3 + 1) * HW + pi] = dg2;
-        dmaps[(size_t)(ch * 3 + 2) * HW + pi] = dxy;
-        l1 += (double)fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
+        dm0[pi] = dmu;
+        dm1[pi] = dg2;
+        dm2[pi] = dxy;
+        l1f += fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
       }
+      l1 += (double)l1f;
+      ss += (double)ssf;
     }
     __syncthreads();
   }
@@ -207,6 +237,7 @@ __global__ void k_loss_finalize(int W, int H, double w_l1, double w_ssim, double
   out[4] = varh > 0.0 ? sqrt(varh) : 0.0;
 }
 
+template <bool U8>
 __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __restrict__ img,
                                                   const Target tgt, const double* __restrict__ soft,
                                                   const float* __restrict__ dmaps, const LossAcc* __restrict__ acc,
@@ -222,16 +253,36 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
   float wv[11];
 #pragma unroll
   for (int t = 0; t < 11; t++) wv[t] = c_win[t];
+  const int ca = tid & 31, cb = ca + 32;
+  const int gca = c0 - HALO + ca, gcb = c0 - HALO + cb;
+  const bool ina = gca >= 0 && gca < W, inb = cb < LH && gcb >= 0 && gcb < W;
   for (int ch = 0; ch < 3; ch++) {
-    for (int r = tid >> 5; r < LH; r += 8) {
-      const int gr = r0 - HALO + r;
-      const bool rin = gr >= 0 && gr < H;
-      for (int c = tid & 31; c < LH; c += 32) {
-        const int gc = c0 - HALO + c;
-        const bool in = rin && gc >= 0 && gc < W;
-        const size_t pi = (size_t)gr * W + gc;
+    const float* dm[3] = {dmaps + (size_t)(ch * 3 + 0) * HW, dmaps + (size_t)(ch * 3 + 1) * HW,
+                          dmaps + (size_t)(ch * 3 + 2) * HW};
+    // two rows per pass, all twelve loads issued before the stores
+    for (int r = tid >> 5; r < LH; r += 16) {
+      float v[2][3][2];
 #pragma unroll
-        for (int k = 0; k < 3; k++) sm[k][r][c] = in ? dmaps[(size_t)(ch * 3 + k) * HW + pi] : 0.f;
+      for (int u = 0; u < 2; u++) {
+        const int rr = r + 8 * u;
+        const int gr = r0 - HALO + rr;
+        const bool rin = rr < LH && gr >= 0 && gr < H;
+        const int row = gr * W;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          v[u][k][0] = rin && ina ? dm[k][row + gca] : 0.f;
+          v[u][k][1] = rin && inb ? dm[k][row + gcb] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int rr = r + 8 * u;
+        if (rr >= LH) break;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          sm[k][rr][ca] = v[u][k][0];
+          if (cb < LH) sm[k][rr][cb] = v[u][k][1];
+        }
       }
     }
     __syncthreads();
@@ -272,8 +323,8 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
       for (int o = 0; o < VSEG; o++) {
         const int gr = r0 + rs + o, gc = c0 + c;
         if (gr >= H || gc >= W) continue;
-        const size_t pi = (size_t)gr * W + gc;
-        const float x = img[pi * 3 + ch], y = tgt[pi * 3 + ch];
+        const int pi = gr * W + gc;
+        const float x = img[pi * 3 + ch], y = tgt_at<U8>(tgt, pi * 3 + ch);
         const float gs = bm[0][o] + 2.f * x * bm[1][o] + y * bm[2][o];  // d SSIM / d x
         const float diff = x - y;
         const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
@@ -329,6 +380,10 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
     set_error("ssr_loss: image smaller than the 11-tap SSIM window");
     return SSR_ERR_INVALID;
   }
+  if ((int64_t)width * height * 3 > INT32_MAX) {
+    set_error("ssr_loss: image larger than 715 megapixels (32-bit pixel indexing)");
+    return SSR_ERR_INVALID;
+  }
   int64_t need = 0;
   ssr_loss_workspace(width, height, &need);
   if (workspace_bytes < need) {
@@ -342,11 +397,18 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   SSR_TRY(check_cuda(cudaMemsetAsync(acc, 0, sizeof(LossAcc), st), "loss acc"));
   dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
   const Target tg{target, target_u8 ? 1 : 0};
-  k_ssim_fwd<<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
+  if (tg.u8)
+    k_ssim_fwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
+  else
+    k_ssim_fwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
   SSR_TRY(check_launch("k_ssim_fwd"));
   k_loss_finalize<<<1, 32, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, acc, out);
   SSR_TRY(check_launch("k_loss_finalize"));
-  k_ssim_bwd<<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
-                                   d_image, d_soft);
+  if (tg.u8)
+    k_ssim_bwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
+                                           d_image, d_soft);
+  else
+    k_ssim_bwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
+                                            d_image, d_soft);
   return check_launch("k_ssim_bwd");
 }
