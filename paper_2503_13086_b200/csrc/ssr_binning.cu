@@ -30,35 +30,50 @@ constexpr int DEPTH_KEY_BITS = 24;
 constexpr int DEPTH_KEY_SHIFT = 4;
 constexpr uint32_t DEPTH_KEY_CULLED = (1u << DEPTH_KEY_BITS) - 1u;
 
-__global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const uint32_t* __restrict__ tiles,
-                                                    const double* __restrict__ depth, uint32_t* __restrict__ keys,
-                                                    uint32_t* __restrict__ vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t key = DEPTH_KEY_CULLED;
-  if (tiles[i]) {
-    const uint32_t b = __float_as_uint(__double2float_rn(depth[i])) - __float_as_uint((float)ZNEAR);
-    key = min(b >> DEPTH_KEY_SHIFT, DEPTH_KEY_CULLED - 1u);
+// The per-Gaussian passes below handle BIN_PER elements per thread, block-
+// strided (each step coalesced across the warp), so several independent
+// loads are in flight per thread.
+constexpr int BIN_PER = 4;
+constexpr int BIN_THREADS = 256;
+
+__global__ void __launch_bounds__(BIN_THREADS) k_depth_keys(int64_t n, const uint32_t* __restrict__ tiles,
+                                                            const double* __restrict__ depth,
+                                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t base = (int64_t)blockIdx.x * BIN_THREADS * BIN_PER + threadIdx.x;
+  uint32_t t[BIN_PER];
+  double d[BIN_PER];
+#pragma unroll
+  for (int k = 0; k < BIN_PER; k++) {
+    const int64_t i = base + k * BIN_THREADS;
+    t[k] = i < n ? tiles[i] : 0u;
+    d[k] = i < n ? depth[i] : 0.0;
   }
-  keys[i] = key;
-  vals[i] = (uint32_t)i;
+#pragma unroll
+  for (int k = 0; k < BIN_PER; k++) {
+    const int64_t i = base + k * BIN_THREADS;
+    if (i >= n) break;
+    uint32_t key = DEPTH_KEY_CULLED;
+    if (t[k]) {
+      const uint32_t b = __float_as_uint(__double2float_rn(d[k])) - __float_as_uint((float)ZNEAR);
+      key = min(b >> DEPTH_KEY_SHIFT, DEPTH_KEY_CULLED - 1u);
+    }
+    keys[i] = key;
+    vals[i] = (uint32_t)i;
+  }
 }
 
-// Runs of equal fp32 depth keys: insertion sort by fp64 depth (stable, so
-// equal fp64 depths keep field-row order).  Also gathers the tile counts in
-// depth order (cnt[s] = tiles[order[s]]) once each position's entry is final:
-// a run's head writes the whole run after sorting it.
-__global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t* __restrict__ keys,
-                                                      uint32_t* __restrict__ order, const double* __restrict__ depth,
-                                                      const uint32_t* __restrict__ tiles, uint32_t* __restrict__ cnt) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const uint32_t key = keys[s];
-  const bool head = (s == 0) || (keys[s - 1] != key);
-  if (key == DEPTH_KEY_CULLED || !head || s + 1 >= n || keys[s + 1] != key) {
-    if (key == DEPTH_KEY_CULLED || head) cnt[s] = tiles[order[s]];  // culled or a run of one
-    return;
-  }
+// Runs of equal fp32 depth keys: re-ordered by fp64 depth (stable, so equal
+// fp64 depths keep field-row order).  Also gathers the tile counts in depth
+// order (cnt[s] = tiles[order[s]]) once each position's entry is final: a
+// run's head writes the whole run after sorting it.  Runs of up to TIE_MAX
+// (nearly all) are loaded with independent loads and sorted in registers
+// (stable bubble network); longer ones fall back to an insertion sort in
+// place.
+constexpr int TIE_MAX = 8;
+
+__device__ __noinline__ void tiefix_long_run(int64_t s, int64_t n, uint32_t key, const uint32_t* __restrict__ keys,
+                                             uint32_t* __restrict__ order, const double* __restrict__ depth,
+                                             const uint32_t* __restrict__ tiles, uint32_t* __restrict__ cnt) {
   int64_t e = s + 1;
   while (e < n && keys[e] == key) e++;
   for (int64_t a = s + 1; a < e; a++) {
@@ -72,6 +87,58 @@ __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t*
     order[b + 1] = v;
   }
   for (int64_t a = s; a < e; a++) cnt[a] = tiles[order[a]];
+}
+
+__global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t* __restrict__ keys,
+                                                      uint32_t* __restrict__ order, const double* __restrict__ depth,
+                                                      const uint32_t* __restrict__ tiles, uint32_t* __restrict__ cnt) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t key = keys[s];
+  const bool head = (s == 0) || (keys[s - 1] != key);
+  if (key == DEPTH_KEY_CULLED || !head || s + 1 >= n || keys[s + 1] != key) {
+    if (key == DEPTH_KEY_CULLED || head) cnt[s] = tiles[order[s]];  // culled or a run of one
+    return;
+  }
+  // run length (>= 2): the next TIE_MAX keys at once
+  uint32_t kk[TIE_MAX];
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++) kk[j] = s + 1 + j < n ? keys[s + 1 + j] : UINT32_MAX;
+  int len = 1;
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++)
+    if (len == j + 1 && kk[j] == key) len++;
+  if (len > TIE_MAX) {
+    tiefix_long_run(s, n, key, keys, order, depth, tiles, cnt);
+    return;
+  }
+  uint32_t o[TIE_MAX];
+  double d[TIE_MAX];
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++) o[j] = j < len ? order[s + j] : 0u;
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++) d[j] = j < len ? depth[o[j]] : __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+  for (int i = 0; i < TIE_MAX - 1; i++)
+#pragma unroll
+    for (int j = 0; j < TIE_MAX - 1 - i; j++)
+      if (d[j] > d[j + 1]) {
+        const double td = d[j];
+        d[j] = d[j + 1];
+        d[j + 1] = td;
+        const uint32_t to = o[j];
+        o[j] = o[j + 1];
+        o[j + 1] = to;
+      }
+  uint32_t tc[TIE_MAX];
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++) tc[j] = j < len ? tiles[o[j]] : 0u;
+#pragma unroll
+  for (int j = 0; j < TIE_MAX; j++)
+    if (j < len) {
+      order[s + j] = o[j];
+      cnt[s + j] = tc[j];
+    }
 }
 
 __global__ void __launch_bounds__(256) k_scatter_offsets(int64_t n, const uint32_t* __restrict__ order,
@@ -254,18 +321,19 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   uint32_t* cnt = (uint32_t*)(w + 4 * a);
   uint32_t* off_sorted = (uint32_t*)(w + 5 * a);
   char* temp = w + 6 * a;
-  const unsigned blocks = (unsigned)((n + 255) / 256);
-  k_depth_keys<<<blocks, 256, 0, st>>>(n, splats.tiles, splats.depth, keys_in, vals_in);
+  const unsigned blocks = (unsigned)((n + BIN_THREADS * BIN_PER - 1) / (BIN_THREADS * BIN_PER));
+  k_depth_keys<<<blocks, BIN_THREADS, 0, st>>>(n, splats.tiles, splats.depth, keys_in, vals_in);
   SSR_TRY(check_launch("k_depth_keys"));
   size_t tb = sort32_temp_bytes(n, DEPTH_KEY_BITS);
   SSR_TRY(check_cuda(cub::DeviceRadixSort::SortPairs((void*)temp, tb, keys_in, keys_out, vals_in, order, (int)n, 0,
                                                      DEPTH_KEY_BITS, st),
                      "depth sort"));
-  k_depth_tiefix<<<blocks, 256, 0, st>>>(n, keys_out, order, splats.depth, splats.tiles, cnt);
+  const unsigned blocks1 = (unsigned)((n + 255) / 256);
+  k_depth_tiefix<<<blocks1, 256, 0, st>>>(n, keys_out, order, splats.depth, splats.tiles, cnt);
   SSR_TRY(check_launch("k_depth_tiefix"));
   size_t sb = scan_temp_bytes(n);
   SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, sb, cnt, off_sorted, (int)n, st), "scan tiles"));
-  k_scatter_offsets<<<blocks, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev,
+  k_scatter_offsets<<<blocks1, 256, 0, st>>>(n, order, cnt, off_sorted, splats.offset, total_dev,
                                             splats.depth_order);
   SSR_TRY(check_launch("k_scatter_offsets"));
   // gradient-row offsets in field-row order (contiguous per block of rows for the chain)
