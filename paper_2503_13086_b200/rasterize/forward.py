@@ -10,7 +10,7 @@ import torch
 from .. import _lib
 from ..camera import CameraFrame
 from ..errors import InvalidParameter
-from .projection import ProjectedSplats, project_field
+from .projection import ProjectedSplats, project_begin, project_end, project_field  # noqa: F401
 
 # Relative guard bands of the fp32 walk's discrete decisions; pixels inside
 # either are re-walked in float64.  GUARD_BAND covers the
@@ -65,19 +65,24 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
     band = GUARD_BAND if band is None else float(band)
     band_t = GUARD_BAND_T if band_t is None else float(band_t)
     bg = np.asarray(bg, dtype=np.float64).reshape(3)
-    splats = project_field(field, cam)
+    splats, ctx = project_begin(field, cam)
+    # the outputs do not depend on the instance count: allocated while the
+    # device runs the preprocess, before the host waits for that count
     dev = splats.tile_ranges.device
     h, w = cam.height, cam.width
     n_tiles = splats.tiles_x * splats.tiles_y
-    m = splats.n_instances
     e = lambda *s, dt=torch.float32: torch.empty(s, dtype=dt, device=dev)
+    image, t_final, n_walk = e(h, w, 3), e(h, w), e(h, w, dt=torch.int32)
+    terminated, hard, soft = e(h, w, dt=torch.uint8), e(h, w, dt=torch.int32), e(h, w, dt=torch.float64)
+    flagged, tile_info = e(h, w, dt=torch.uint8), e(n_tiles, 4, dt=torch.int32)
+    fix_list = e(int(_lib.load().ssr_fix_list_ints(w, h, n_tiles)), dt=torch.int32)
+    project_end(splats, ctx, field)
+    m = splats.n_instances
     out = RenderOutput(
-        image=e(h, w, 3), t_final=e(h, w), n_walk=e(h, w, dt=torch.int32), terminated=e(h, w, dt=torch.uint8),
-        hard_count=e(h, w, dt=torch.int32), soft_count=e(h, w, dt=torch.float64), splats=splats, cam=cam, bg=bg,
-        generation=field.generation, workers=workers, flagged=e(h, w, dt=torch.uint8),
-        tile_info=e(n_tiles, 4, dt=torch.int32),
-        ckpt=e(int(_lib.load().ssr_ckpt_floats(m, n_tiles))),
-        fix_list=e(int(_lib.load().ssr_fix_list_ints(w, h, n_tiles)), dt=torch.int32),
+        image=image, t_final=t_final, n_walk=n_walk, terminated=terminated, hard_count=hard, soft_count=soft,
+        splats=splats, cam=cam, bg=bg, generation=field.generation, workers=workers, flagged=flagged,
+        tile_info=tile_info, ckpt=e(int(_lib.load().ssr_ckpt_floats(max(m, splats._cap), n_tiles))),
+        fix_list=fix_list,
     )
     _lib.call("ssr_forward", m, splats.struct(), splats.inst_gauss.data_ptr() if m else None,
               splats.tile_ranges.data_ptr(), out.frame_struct(), band, band_t, _lib.stream_ptr())

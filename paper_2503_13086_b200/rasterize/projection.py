@@ -39,6 +39,7 @@ class ProjectedSplats:
     tile_ranges: torch.Tensor  # (n_tiles, 2) int32 (start, end)
     cam: CameraFrame
     _src: tuple = dc_field(default=None, repr=False)  # (flat params, n, K) for aux
+    _cap: int = dc_field(default=0, repr=False)  # instance capacity of the buffers sized by M
     _cache: dict = dc_field(default_factory=dict, repr=False)
 
     def struct(self) -> _lib.SsrSplats:
@@ -137,6 +138,19 @@ def _alloc_splats(n: int, dev) -> dict:
 
 def project_field(field, cam: CameraFrame) -> ProjectedSplats:
     """Project every Gaussian, cull, bin into tiles and depth-sort (projection.py:69-191)."""
+    sp, ctx = project_begin(field, cam)
+    project_end(sp, ctx, field)
+    return sp
+
+
+def project_begin(field, cam: CameraFrame):
+    """Launch the preprocess and the per-Gaussian scans; returns (splats, ctx).
+
+    Nothing here waits for the device.  The instance buffers are allocated
+    speculatively from the field's last instance count (``_m_hint``), so that
+    after the one host synchronisation of the path (the instance total M, in
+    ``project_end``) the binning launches without further host work.
+    """
     from ..field import class_slices
 
     dev = _lib.require_cuda()
@@ -147,11 +161,13 @@ def project_field(field, cam: CameraFrame) -> ProjectedSplats:
     n_tiles = tiles_x * tiles_y
     st = _lib.stream_ptr()
     bufs = _alloc_splats(n, dev)
+    # every tile's range is written by ssr_bin_tiles (empty tiles included)
     sp = ProjectedSplats(n, field.sh_degree, tiles_x, tiles_y, bufs,
                          torch.empty(0, dtype=torch.int32, device=dev),
-                         torch.zeros(n_tiles, 2, dtype=torch.int32, device=dev), cam, (field.flat, n, k))
+                         torch.empty(n_tiles, 2, dtype=torch.int32, device=dev), cam, (field.flat, n, k))
     if n == 0:
-        return sp
+        sp.tile_ranges.zero_()
+        return sp, None
     flat = field.flat
     sl = class_slices(n, k)
     cstruct = _lib.camera_struct(cam)
@@ -161,11 +177,36 @@ def project_field(field, cam: CameraFrame) -> ProjectedSplats:
     ws = torch.empty(_lib.query("ssr_scan_workspace", n), dtype=torch.uint8, device=dev)
     total = torch.empty(1, dtype=torch.int32, device=dev)
     _lib.call("ssr_scan_tiles", n, s, ws.data_ptr(), ws.numel(), total.data_ptr(), st)
+    cap = int(getattr(field, "_m_hint", 0) or 0)
+    inst_cap = ws_cap = None
+    if cap > 0:
+        inst_cap = torch.empty(cap, dtype=torch.int32, device=dev)
+        ws_cap = torch.empty(_lib.query("ssr_bin_workspace", cap, n_tiles), dtype=torch.uint8, device=dev)
+    return sp, (total, cap, inst_cap, ws_cap, s, st, ws)
+
+
+def project_end(sp: ProjectedSplats, ctx, field=None) -> ProjectedSplats:
+    """Read the instance total (the path's one host synchronisation) and bin."""
+    if ctx is None:
+        return sp
+    total, cap, inst_cap, ws_cap, s, st, _ = ctx
+    dev = total.device
+    n_tiles = sp.tiles_x * sp.tiles_y
     m = int(total.item())  # host needs M to size the instance buffers
     if m < 0:
         raise InvalidParameter("instance count overflow")
-    sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
-    ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
-    _lib.call("ssr_bin_tiles", n, m, tiles_x, tiles_y, s, sp.inst_gauss.data_ptr() if m else None,
+    if 0 < m <= cap:
+        sp.inst_gauss = inst_cap[:m]
+        ws = ws_cap
+        sp._cap = cap
+    else:
+        sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
+        ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
+        sp._cap = m
+    if field is not None and m > cap:
+        # capacity for the next renders: grows in 1 Mi-instance steps (+6%), so the
+        # buffer sizes repeat and the caching allocator reuses its blocks
+        field._m_hint = ((m + m // 16 + (1 << 20)) >> 20) << 20
+    _lib.call("ssr_bin_tiles", sp.n, m, sp.tiles_x, sp.tiles_y, s, sp.inst_gauss.data_ptr() if m else None,
               sp.tile_ranges.data_ptr(), ws.data_ptr(), ws.numel(), st)
     return sp

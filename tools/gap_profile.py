@@ -64,6 +64,11 @@ def analyse(prof, iters):
 
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     iv = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev)
+    # drop the first iteration (profiler start-up): analyse from the second preprocess on
+    starts = [i for i, x in enumerate(iv) if "k_preprocess" in x[2]]
+    if len(starts) > 1:
+        iv = iv[starts[1]:]
+        iters = len(starts) - 1
     if not iv:
         print(json.dumps({"error": "no device events"}))
         return None
