@@ -127,6 +127,17 @@ int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tiles_y, ssr_sp
                   uint32_t* inst_gauss, int32_t* tile_ranges, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* ssr_bin_tiles with the instance count read here: copies *total_dev (from
+ * ssr_scan_tiles) to the host, synchronises the stream, stores M in *m_out and,
+ * when M <= capacity, bins into inst_gauss / workspace sized for `capacity`
+ * instances (ssr_bin_workspace(capacity, ...)).  Returns SSR_ERR_CAPACITY
+ * without launching when M > capacity (the caller then sizes the buffers for
+ * *m_out and calls ssr_bin_tiles).  Lets the binning start without a round
+ * trip through the host language after the path's one synchronisation. */
+int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y, ssr_splats splats,
+                           const uint32_t* total_dev, int64_t* m_out, uint32_t* inst_gauss, int32_t* tile_ranges,
+                           void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Floats needed for the checkpoint buffer of a frame with M instances. */
 int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles);
 

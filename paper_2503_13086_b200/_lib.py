@@ -54,6 +54,8 @@ _SIGS = {
     "ssr_bin_workspace": [c_int64, c_int32, ctypes.POINTER(c_int64)],
     "ssr_bin_tiles": [c_int64, c_int64, c_int32, c_int32, SsrSplats, c_void_p, c_void_p, c_void_p, c_int64,
                       c_void_p],
+    "ssr_bin_tiles_capacity": [c_int64, c_int64, c_int32, c_int32, SsrSplats, c_void_p, ctypes.POINTER(c_int64),
+                               c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "ssr_ckpt_floats": [c_int64, c_int32],
     "ssr_fix_list_ints": [c_int32, c_int32, c_int32],
     "ssr_forward": [c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_float, c_float, c_void_p],
@@ -126,7 +128,16 @@ def timer_ms() -> dict:
     return {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in _timers.items()}
 
 
-def call(name: str, *args) -> None:
+def raise_last(name: str, rc: int) -> None:
+    """Raise the Python error of a failed entry point's return code."""
+    msg = (load().ssr_last_error() or b"").decode(errors="replace")
+    if rc in (1, 3):
+        raise InvalidParameter(f"{name}: {msg}")
+    raise NativeError(f"{name} failed ({rc}): {msg}")
+
+
+def call_rc(name: str, *args) -> int:
+    """Call an entry point (timed when timers are on) and return its code."""
     if _timers is not None:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev0.record()
@@ -135,11 +146,13 @@ def call(name: str, *args) -> None:
         ev1 = torch.cuda.Event(enable_timing=True)
         ev1.record()
         _timers.setdefault(name, []).append((ev0, ev1))
+    return rc
+
+
+def call(name: str, *args) -> None:
+    rc = call_rc(name, *args)
     if rc != 0:
-        msg = (load().ssr_last_error() or b"").decode(errors="replace")
-        if rc in (1, 3):
-            raise InvalidParameter(f"{name}: {msg}")
-        raise NativeError(f"{name} failed ({rc}): {msg}")
+        raise_last(name, rc)
 
 
 def require_cuda() -> torch.device:

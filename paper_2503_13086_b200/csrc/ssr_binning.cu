@@ -389,6 +389,31 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   return check_launch("k_ranges");
 }
 
+extern "C" int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y,
+                                      ssr_splats splats, const uint32_t* total_dev, int64_t* m_out,
+                                      uint32_t* inst_gauss, int32_t* tile_ranges, void* workspace,
+                                      int64_t workspace_bytes, void* stream) {
+  if (!total_dev || !m_out) {
+    set_error("ssr_bin_tiles_capacity: total_dev and m_out are required");
+    return SSR_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // one pinned word per host thread for the instance total
+  static thread_local uint32_t* host_total = nullptr;
+  if (!host_total) SSR_TRY(check_cuda(cudaMallocHost(&host_total, sizeof(uint32_t)), "pinned total"));
+  SSR_TRY(check_cuda(cudaMemcpyAsync(host_total, total_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
+                     "instance total"));
+  SSR_TRY(check_cuda(cudaStreamSynchronize(st), "instance total"));
+  const int64_t m = (int64_t)*host_total;
+  *m_out = m;
+  if (m > capacity) {
+    set_error("ssr_bin_tiles_capacity: instance count exceeds the capacity");
+    return SSR_ERR_CAPACITY;
+  }
+  return ssr_bin_tiles(n, m, tiles_x, tiles_y, splats, m ? inst_gauss : nullptr, tile_ranges, workspace,
+                       workspace_bytes, stream);
+}
+
 extern "C" int64_t ssr_ckpt_floats(int64_t m, int32_t n_tiles) {
   return (m / BUCKET + (int64_t)n_tiles + 1) * TILE_PX * 4;
 }

@@ -8,6 +8,7 @@ itself only touches the N-indexed device arrays and the sorted instance list.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field as dc_field
 
 import torch
@@ -192,21 +193,33 @@ def project_end(sp: ProjectedSplats, ctx, field=None) -> ProjectedSplats:
     total, cap, inst_cap, ws_cap, s, st, _ = ctx
     dev = total.device
     n_tiles = sp.tiles_x * sp.tiles_y
-    m = int(total.item())  # host needs M to size the instance buffers
+    m = -1
+    if cap > 0:
+        # read M and launch the binning in one native call (no host-language
+        # work between the synchronisation and the first binning kernel)
+        m_out = ctypes.c_int64(0)
+        rc = _lib.call_rc("ssr_bin_tiles_capacity", sp.n, cap, sp.tiles_x, sp.tiles_y, s, total.data_ptr(),
+                          ctypes.byref(m_out), inst_cap.data_ptr(), sp.tile_ranges.data_ptr(), ws_cap.data_ptr(),
+                          ws_cap.numel(), st)
+        m = int(m_out.value)
+        if rc == 0:
+            sp.inst_gauss = inst_cap[:m]
+            sp._cap = cap
+            return sp
+        if rc != 3 or m <= cap:
+            _lib.raise_last("ssr_bin_tiles_capacity", rc)
+    if m < 0:
+        m = int(total.item())  # host needs M to size the instance buffers
     if m < 0:
         raise InvalidParameter("instance count overflow")
-    if 0 < m <= cap:
-        sp.inst_gauss = inst_cap[:m]
-        ws = ws_cap
-        sp._cap = cap
-    else:
-        sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
-        ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
-        sp._cap = m
-    if field is not None and m > cap:
-        # capacity for the next renders: grows in 1 Mi-instance steps (+6%), so the
-        # buffer sizes repeat and the caching allocator reuses its blocks
-        field._m_hint = ((m + m // 16 + (1 << 20)) >> 20) << 20
+    sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
+    ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
+    sp._cap = m
+    if field is not None:
+        # capacity for the next renders: M + 6%, rounded up to 1/16 of M's leading
+        # power of two, so the buffer sizes repeat and the allocator reuses its blocks
+        step = 1 << max(12, m.bit_length() - 4)
+        field._m_hint = (m + m // 16 + step) // step * step
     _lib.call("ssr_bin_tiles", sp.n, m, sp.tiles_x, sp.tiles_y, s, sp.inst_gauss.data_ptr() if m else None,
               sp.tile_ranges.data_ptr(), ws.data_ptr(), ws.numel(), st)
     return sp

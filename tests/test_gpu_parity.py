@@ -336,3 +336,37 @@ def test_stress_cases_vs_oracle(case, oracle_lib):
         for layout in ("splat", "pixel"):
             r = grads_report(backward(f, out, d_img, d_soft, layout=layout), ref_g)
             assert grads_ok(r), (layout, d_soft is None, r)
+
+
+def test_instance_capacity_reuse_and_growth():
+    """Renders through the capacity path (buffers sized from the field's last
+    instance count, ssr_bin_tiles_capacity) equal renders of a fresh field,
+    both when M fits the capacity and when it outgrows it (fallback)."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.rasterize import render
+
+    hp = scenes.make_params(1, seed=3, n=6000)
+    small = scenes.camera(1, view=2, width=64, height=48)
+    big = scenes.camera(1, view=2, width=320, height=240)
+
+    def fields_equal(a, b):
+        for k in ("image", "t_final", "n_walk", "terminated", "hard_count", "soft_count"):
+            assert torch.equal(getattr(a, k), getattr(b, k)), k
+        assert torch.equal(a.splats.inst_gauss, b.splats.inst_gauss)
+        assert torch.equal(a.splats.tile_ranges, b.splats.tile_ranges)
+
+    f = GaussianField.from_host(hp)
+    r_small = render(f, small)  # sets the capacity hint
+    assert getattr(f, "_m_hint", 0) >= r_small.splats.n_instances
+    r_big = render(f, big)  # M outgrows the capacity: exact-size fallback
+    r_big2 = render(f, big)  # now within the (grown) capacity
+    ref_big = render(GaussianField.from_host(hp), big)
+    ref_small = render(GaussianField.from_host(hp), small)
+    r_small2 = render(f, small)  # capacity larger than M
+    torch.cuda.synchronize()
+    assert r_big.splats.n_instances > r_small.splats.n_instances
+    fields_equal(r_big, ref_big)
+    fields_equal(r_big2, ref_big)
+    fields_equal(r_small2, ref_small)
