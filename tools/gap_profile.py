@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--view", type=int, default=99)
     ap.add_argument("--trace-out", default="")
+    ap.add_argument("--u8", action="store_true", help="8-bit target image (as the e2e bench uploads)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -42,6 +43,8 @@ def main():
     cam = scenes.camera(cfg, view=args.view)
     tp = scenes.make_params(cfg, seed=1, n=n) if n else scenes.make_params(cfg, seed=1)
     target = render(GaussianField.from_host(tp), cam).image.clone()
+    if args.u8:
+        target = (target * 255.0).round().clamp(0, 255).to(torch.uint8)
     state = TrainState(field=field, optimizer=FieldOptimizer(field, scene_extent=6.6),
                        weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), scene_extent=6.6,
                        rng=np.random.default_rng(7))
