@@ -183,16 +183,10 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, co
 
 // ------------------------------------------------------------------ geometry chain
 constexpr int CHAIN_ROWS = 128;
-#ifndef GEO_ROWS_STAGE
-#define GEO_ROWS_STAGE 1
-#endif
-constexpr int CHAIN_STAGE_FLOATS = GEO_ROWS_STAGE ? 9 * 1024 : 4;
+constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
 
 template <bool FUSED>
-#ifndef GEO_MINB
-#define GEO_MINB 1
-#endif
-__global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
+__global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
                                                           float* __restrict__ rot, float* __restrict__ ls,
                                                           float* __restrict__ logit_p,
                                                           const uint32_t* __restrict__ tiles,
@@ -213,7 +207,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, in
   const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
   const int pad = (int)((b0 - a0) >> 2);
   const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
-  const bool staged = GEO_ROWS_STAGE && n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
+  const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
   const int64_t ns = row_stride(n);
   // fused: the CTA's rotation / log-scale / logit rows and their moments come
   // in by TMA bulk copies next to the instance rows ([param | m | v] x
@@ -237,15 +231,27 @@ __global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, in
         }
       }
     }
-    mbar_wait(&mbar, 0);
   }
+  // the row's own global reads are issued before waiting for the bulk copies
+  uint32_t nt = 0, s0 = 0;
+  float px = 0.f, py = 0.f, pz = 0.f, st0 = 0.f, st1 = 0.f;
+  if (mine) {
+    nt = tiles[i];
+    s0 = roff[i];
+    px = pos[i * 3];
+    py = pos[i * 3 + 1];
+    pz = pos[i * 3 + 2];
+    if (stats) {
+      st0 = stats[i];
+      st1 = stats[n + i];
+    }
+  }
+  if (staged || FUSED) mbar_wait(&mbar, 0);
   if (!mine) return;
-  const uint32_t nt = tiles[i];
   // bincount merge (backward.py:110-118): ascending tile order; Gaussians with
   // more than MERGE_BIG rows were reduced into their first row by k_merge_big
   float pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (nt > 0) {
-    const uint32_t s0 = roff[i];
     const float* rw = staged ? s_rows + pad + (int64_t)(s0 - r_begin) * 9 : rows + (int64_t)s0 * 9;
     if (nt <= MERGE_BIG) {
       for (uint32_t j = 0; j < nt; j++)
@@ -281,7 +287,6 @@ __global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, in
     dst[2] = pr[2];
 
     // ---- forward quantities of projection.py:76-128 (float32 restatement)
-    const float px = pos[i * 3], py = pos[i * 3 + 1], pz = pos[i * 3 + 2];
     const float* R = cam.R;
     const float x = R[0] * px + R[1] * py + R[2] * pz + cam.t[0];
     const float y = R[3] * px + R[4] * py + R[5] * pz + cam.t[1];
@@ -461,8 +466,8 @@ __global__ void __launch_bounds__(CHAIN_ROWS, GEO_MINB) k_chain_geo(CamF cam, in
     g_vis[i] = vis ? 1.f : 0.f;
   }
   if (stats && vis) {
-    stats[i] += screen;
-    stats[n + i] += 1.f;
+    stats[i] = st0 + screen;
+    stats[n + i] = st1 + 1.f;
   }
 }
 
