@@ -1,7 +1,7 @@
 // Stages 3 and 4: 16x16-tile alpha-blend forward and the two backward layouts
 // (rasterize/kernels.py:31-353), plus the float64 guard-band fix-up.
 //
-// Forward: one CTA per tile, one thread per pixel, splat batches staged in
+// Forward: one CTA per tile, one thread per pixel, 512-splat batches staged in
 // shared memory, block-wide early exit on transmittance.  Every 32 walked
 // slots each live pixel checkpoints (T, C_front) so the splat-parallel
 // backward can start any 32-splat bucket without replaying the tile.
@@ -149,6 +149,9 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
   return true;
 }
 
+// Splats staged per batch: two per thread (half the barriers of one per thread).
+constexpr int FWD_BATCH = 2 * TILE_PX;
+
 __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
@@ -161,9 +164,9 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
   const float band = a.band, band_t = a.band_t;
 
-  __shared__ float4 sM[TILE_PX];  // staged mean (x int, x frac, y int, y frac)
-  __shared__ float4 sA[TILE_PX];  // staged conic a2, b2, c2; opacity
-  __shared__ float4 sB[TILE_PX];  // r, g, b
+  __shared__ float4 sM[FWD_BATCH];  // staged mean (x int, x frac, y int, y frac)
+  __shared__ float4 sA[FWD_BATCH];  // staged conic a2, b2, c2; opacity
+  __shared__ float4 sB[FWD_BATCH];  // r, g, b
   __shared__ int sMax[8];
 
   FwdState q;
@@ -177,25 +180,29 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   bool done = !inside;
   float4* ck = a.ckpt + ckpt_base(s0, t) + tid;
 
-  for (int base = s0; base < s1; base += TILE_PX) {
+  for (int base = s0; base < s1; base += FWD_BATCH) {
     if (__syncthreads_count(done) == TILE_PX) break;
-    const int s = base + tid;
     bool fragile = false;
-    if (s < s1) {
-      const uint32_t g = a.inst[s];
-      const double2 m = a.mean[g];
-      const float4 co = a.conic_opa[g];
-      const float4 col = a.color[g];
-      const StagedConic sc = stage_conic(co.x, co.y, co.z);
-      const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
-      sM[tid] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
-      sA[tid] = make_float4(sc.a2, sc.b2, sc.c2, co.w);  // opacity < 0 marks a fragile conic
-      sB[tid] = col;
-      fragile = co.w < 0.f;
+#pragma unroll
+    for (int u = 0; u < FWD_BATCH / TILE_PX; u++) {
+      const int e = u * TILE_PX + tid;
+      const int s = base + e;
+      if (s < s1) {
+        const uint32_t g = a.inst[s];
+        const double2 m = a.mean[g];
+        const float4 co = a.conic_opa[g];
+        const float4 col = a.color[g];
+        const StagedConic sc = stage_conic(co.x, co.y, co.z);
+        const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
+        sM[e] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
+        sA[e] = make_float4(sc.a2, sc.b2, sc.c2, co.w);  // opacity < 0 marks a fragile conic
+        sB[e] = col;
+        fragile |= co.w < 0.f;
+      }
     }
     const bool batch_fragile = __syncthreads_or(fragile);
     if (!done) {
-      const int n = min(TILE_PX, s1 - base);
+      const int n = min(FWD_BATCH, s1 - base);
       const int k0 = base - s0;
       for (int j0 = 0; j0 < n; j0 += BUCKET) {
         if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
