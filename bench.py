@@ -124,7 +124,12 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # SSR_DIST_BACKEND / SSR_FORCE_DEVICE0: functional checks of the N > 1 path
+        # on a one-GPU box (gloo, every rank on cuda:0) -- never a measurement
+        backend = os.environ.get("SSR_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
+    if os.environ.get("SSR_FORCE_DEVICE0"):
+        local = 0
     return rank, world, local
 
 
@@ -156,6 +161,7 @@ def _cpu_setup(cfg, views):
 
 def cpu_baseline(cfg, views, budget_s=25.0, min_iters=1, max_iters=3):
     orc, P, opt, cams, targets = _cpu_setup(cfg, views)
+    orc.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
     n, t0 = 0, time.perf_counter()
     while n < max_iters and (n < min_iters or time.perf_counter() - t0 < budget_s / 2):
@@ -173,6 +179,9 @@ def run_reference(args):
         return
     views = _views(args)
     orc, P, opt, cams, targets = _cpu_setup(args.config, views)
+    # every host core: torchrun sets OMP_NUM_THREADS=1 for its workers, which
+    # would understate the reference arm at N > 1
+    orc.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
     for i in range(args.warmup and 1):  # one warm-up iteration is enough for the C port
         _oracle_iteration(orc, P, opt, cams[i % 2], targets[i % 2], w)
@@ -231,14 +240,20 @@ def main():
     rate = 1.6e-4
     n = len(field)
 
+    grads_buf = [None]
+
     def step(k, target=None):
         cam_i = (k * world + rank) % len(cams)
         cam = cams[cam_i]
         out = render(state.field, cam)
         br = total_loss(out.image, targets[cam_i] if target is None else target, out, state.weights)
         if world > 1:
-            grads = FieldGrads.zeros(n, field.sh_degree, dev)
-            backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=True)
+            # one view per rank: the chain writes every row (accumulate=False), so
+            # the buffer needs no zero fill; the flat buffer is the all-reduce unit
+            if grads_buf[0] is None:
+                grads_buf[0] = FieldGrads.zeros(n, field.sh_degree, dev)
+            grads = grads_buf[0]
+            backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=False)
             allreduce_grads(grads.flat)
             state.stats[:n] += grads.screen_norms
             state.stats[n:] += grads.visible_count
