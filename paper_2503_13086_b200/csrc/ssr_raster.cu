@@ -483,8 +483,17 @@ struct BwAcc {
 // alpha below the cap adds its soft term.  The pixel list holds byte offsets
 // (p * 16) shared by both per-pixel arrays; the next step's records are
 // fetched one step ahead.
+// Per-pixel records of the tile being differentiated (k_backward_splat), at
+// file scope so the stream addresses them as list offset + constant base.
+// sPA: dL/dr, dL/dg, dL/db, dL/dsoft; sPB: pixel x, y (tile-relative),
+// w . image, walk limit; entry [256] = sentinel.  One array, so a pixel's two
+// records sit at one register address plus an immediate offset.
+__shared__ float4 sPix[2 * (TILE_PX + 1)];
+#define sPA (sPix)
+#define sPB (sPix + TILE_PX + 1)
+
 template <bool SOFT>
-__device__ __forceinline__ void bw_stream(const char* __restrict__ sPAb, const char* __restrict__ sPBb,
+__device__ __forceinline__ void bw_stream(
                                           const uint16_t* __restrict__ list, const float2* __restrict__ seed,
                                           int n_live, int lane, int k, const BwSplat& s, BwAcc& g) {
   float T = 1.f, H = 0.f;
@@ -492,7 +501,9 @@ __device__ __forceinline__ void bw_stream(const char* __restrict__ sPAb, const c
   const bool lane0 = lane == 0;
   int jn = BW_PAD - lane;  // padded list index of step 0
   int on = list[jn];       // byte offset of the pixel's record in sPA / sPB
-  float4 PBn = *reinterpret_cast<const float4*>(sPBb + on), PAn = *reinterpret_cast<const float4*>(sPAb + on);
+  const char* sPixb = reinterpret_cast<const char*>(sPix);
+  constexpr int B_OFF = (TILE_PX + 1) * sizeof(float4);
+  float4 PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF), PAn = *reinterpret_cast<const float4*>(sPixb + on);
 #pragma unroll 2
   for (int i = 0; i < n_steps; i++) {
     float Tin = __shfl_up_sync(FULL, T, 1);
@@ -503,8 +514,8 @@ __device__ __forceinline__ void bw_stream(const char* __restrict__ sPAb, const c
     const float4 PB = PBn, w = PAn;
     jn++;
     on = list[jn];
-    PBn = *reinterpret_cast<const float4*>(sPBb + on);
-    PAn = *reinterpret_cast<const float4*>(sPAb + on);
+    PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF);
+    PAn = *reinterpret_cast<const float4*>(sPixb + on);
     const int lim = __float_as_int(PB.w);
     const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
     const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
@@ -585,8 +596,6 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
 
-  __shared__ float4 sPA[TILE_PX + 1];  // dL/dr, dL/dg, dL/db, dL/dsoft
-  __shared__ float4 sPB[TILE_PX + 1];  // pixel x, y (tile-relative), w . image, walk limit; [256] = sentinel
   __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
   __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
   bool soft_px = false;
@@ -688,12 +697,10 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       s.p2_min = use_soft ? FAR_POWER2 : fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / s.opa));
     }
     BwAcc g = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const char* pab = reinterpret_cast<const char*>(sPA);
-    const char* pbb = reinterpret_cast<const char*>(sPB);
     if (use_soft)
-      bw_stream<true>(pab, pbb, sList[warp], mySeed, n_live, lane, k, s, g);
+      bw_stream<true>(sList[warp], mySeed, n_live, lane, k, s, g);
     else
-      bw_stream<false>(pab, pbb, sList[warp], mySeed, n_live, lane, k, s, g);
+      bw_stream<false>(sList[warp], mySeed, n_live, lane, k, s, g);
     if (live) {
       float* r = rows + (size_t)orow * 9;
       r[0] = g.g0;
