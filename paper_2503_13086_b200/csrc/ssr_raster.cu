@@ -524,28 +524,29 @@ __device__ __forceinline__ void bw_stream(
     if (!SOFT) {
       const float araw = pair_alpha2(s.opa, p2);
       // (araw >= 1/255 implies p2 >= p2_min: no separate far test here; lanes
-      // past the walks have opacity 0)
-      if (k < lim && p2 <= 0.f && araw >= ALPHA_MIN_F) {
-        const float alpha = fminf(araw, ALPHA_CAP_F);
-        const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
-        const float aT = alpha * T;
-        g.g0 = fmaf(aT, w.x, g.g0);
-        g.g1 = fmaf(aT, w.y, g.g1);
-        g.g2 = fmaf(aT, w.z, g.g2);
-        const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
-        const float awc = aT * wc;
-        const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
-        const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
-        H += awc;
-        T = __fmul_rn(T, one_m);
-        const float gp = araw > ALPHA_CAP_F ? 0.f : dlda * alpha;  // capped: no opacity/geometry path
-        g.g3 += gp;
-        g.sx = fmaf(gp, dx, g.sx);
-        g.sy = fmaf(gp, dy, g.sy);
-        g.g6 = fmaf(gp, dxx, g.g6);
-        g.g7 = fmaf(gp, dxy, g.g7);
-        g.g8 = fmaf(gp, dyy, g.g8);
-      }
+      // past the walks have opacity 0).  Branch-free: some lane of the warp
+      // nearly always contributes, so the block runs anyway; a lane that does
+      // not contributes exactly zero (alpha = 0: T, H and every sum unchanged).
+      const bool c = (k < lim) & (p2 <= 0.f) & (araw >= ALPHA_MIN_F);
+      const float alpha = c ? fminf(araw, ALPHA_CAP_F) : 0.f;
+      const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+      const float aT = alpha * T;
+      g.g0 = fmaf(aT, w.x, g.g0);
+      g.g1 = fmaf(aT, w.y, g.g1);
+      g.g2 = fmaf(aT, w.z, g.g2);
+      const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
+      const float awc = aT * wc;
+      const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
+      const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
+      H = c ? H + awc : H;
+      T = __fmul_rn(T, one_m);
+      const float gp = (c & (araw <= ALPHA_CAP_F)) ? dlda * alpha : 0.f;  // capped: no opacity/geometry path
+      g.g3 += gp;
+      g.sx = fmaf(gp, dx, g.sx);
+      g.sy = fmaf(gp, dy, g.sy);
+      g.g6 = fmaf(gp, dxx, g.g6);
+      g.g7 = fmaf(gp, dxy, g.g7);
+      g.g8 = fmaf(gp, dyy, g.g8);
     } else {
       const int nw = lim >> 1;
       if (k < nw && p2 <= 0.f && p2 >= s.p2_min) {
