@@ -548,40 +548,36 @@ __device__ __forceinline__ void bw_stream(
       g.g7 = fmaf(gp, dxy, g.g7);
       g.g8 = fmaf(gp, dyy, g.g8);
     } else {
+      // same branch-free form with the soft-count term of every walked pair
+      // below the cap
       const int nw = lim >> 1;
-      if (k < nw && p2 <= 0.f && p2 >= s.p2_min) {
-        const float araw = pair_alpha2(s.opa, p2);
-        const bool capped = araw > ALPHA_CAP_F;
-        const float alpha = capped ? ALPHA_CAP_F : araw;
-        // the terminating slot (k == nw - 1 of a terminated walk) is never blended
-        const bool blended = alpha >= ALPHA_MIN_F && k < nw - (lim & 1);
-        float dlda = 0.f;
-        if (blended) {
-          const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
-          const float aT = alpha * T;
-          g.g0 = fmaf(aT, w.x, g.g0);
-          g.g1 = fmaf(aT, w.y, g.g1);
-          g.g2 = fmaf(aT, w.z, g.g2);
-          const float one_m = __fsub_rn(1.f, alpha);
-          const float awc = aT * wc;
-          const float sdot = PB.z - H - awc;
-          dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
-          H += awc;
-          T = __fmul_rn(T, one_m);
-        }
-        if (!capped) {
-          const float sv = soft_sigmoid(alpha);
-          g.g3 = fmaf(fmaf(w.w * sv * (1.f - sv), 100.f, dlda), alpha, g.g3);
-          if (blended) {
-            const float gp = dlda * alpha;
-            g.sx = fmaf(gp, dx, g.sx);
-            g.sy = fmaf(gp, dy, g.sy);
-            g.g6 = fmaf(gp, dxx, g.g6);
-            g.g7 = fmaf(gp, dxy, g.g7);
-            g.g8 = fmaf(gp, dyy, g.g8);
-          }
-        }
-      }
+      const bool walked = (k < nw) & (p2 <= 0.f) & (p2 >= s.p2_min);
+      const float araw = pair_alpha2(s.opa, p2);
+      const bool capped = araw > ALPHA_CAP_F;
+      const float alpha = capped ? ALPHA_CAP_F : araw;
+      // the terminating slot (k == nw - 1 of a terminated walk) is never blended
+      const bool blended = walked & (alpha >= ALPHA_MIN_F) & (k < nw - (lim & 1));
+      const float ab = blended ? alpha : 0.f;
+      const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+      const float aT = ab * T;
+      g.g0 = fmaf(aT, w.x, g.g0);
+      g.g1 = fmaf(aT, w.y, g.g1);
+      g.g2 = fmaf(aT, w.z, g.g2);
+      const float one_m = __fsub_rn(1.f, ab);
+      const float awc = aT * wc;
+      const float sdot = PB.z - H - awc;
+      const float dlda = blended ? fmaf(T, wc, -sdot * rcp_approx(one_m)) : 0.f;
+      H = blended ? H + awc : H;
+      T = __fmul_rn(T, one_m);
+      const bool soft_ok = walked & !capped;
+      const float sv = soft_sigmoid(alpha);
+      g.g3 = soft_ok ? fmaf(fmaf(w.w * sv * (1.f - sv), 100.f, dlda), alpha, g.g3) : g.g3;
+      const float gp = (soft_ok & blended) ? dlda * alpha : 0.f;
+      g.sx = fmaf(gp, dx, g.sx);
+      g.sy = fmaf(gp, dy, g.sy);
+      g.g6 = fmaf(gp, dxx, g.g6);
+      g.g7 = fmaf(gp, dxy, g.g7);
+      g.g8 = fmaf(gp, dyy, g.g8);
     }
   }
 }
@@ -668,6 +664,9 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       }
       mySeed[j] = sd;
     }
+    // the sentinel steps after the live pixels read finite seeds: the
+    // branch-free pair blocks multiply them by zero
+    mySeed[n_live + lane] = make_float2(1.f, 0.f);
     __syncwarp();
     const int k = kb + lane;
     const bool live = k < maxw;

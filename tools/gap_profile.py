@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--view", type=int, default=99)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--u8", action="store_true", help="8-bit target image (as the e2e bench uploads)")
+    ap.add_argument("--paper-weights", action="store_true",
+                    help="losses.py default weights (load-balance term on: soft-count gradients)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -46,7 +48,8 @@ def main():
     if args.u8:
         target = (target * 255.0).round().clamp(0, 255).to(torch.uint8)
     state = TrainState(field=field, optimizer=FieldOptimizer(field, scene_extent=6.6),
-                       weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), scene_extent=6.6,
+                       weights=LossWeights() if args.paper_weights else LossWeights(l1=1.0, ssim=0.2, load=0.0),
+                       scene_extent=6.6,
                        rng=np.random.default_rng(7))
     state.densify_enabled = False
     for _ in range(args.warmup):
