@@ -540,7 +540,9 @@ __device__ __forceinline__ void bw_stream(
       const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
       H = c ? H + awc : H;
       T = __fmul_rn(T, one_m);
-      const float gp = (c & (araw <= ALPHA_CAP_F)) ? dlda * alpha : 0.f;  // capped: no opacity/geometry path
+      // capped: no opacity/geometry path; a lane that does not blend has
+      // alpha = 0 and a finite dlda, so its gp is already zero
+      const float gp = araw <= ALPHA_CAP_F ? dlda * alpha : 0.f;
       g.g3 += gp;
       g.sx = fmaf(gp, dx, g.sx);
       g.sy = fmaf(gp, dy, g.sy);
