@@ -110,14 +110,19 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
         continue;
       }
     }
-    float alpha = pair_alpha2(fabsf(A.w), p2);
-    // alpha < 2.5e-3 is below 1/255 and far from both guard bands: only its
-    // soft-count deviation
-    const float y = __fmul_rn(alpha, 100.f);
+    // staged: A.w = +-100 opacity (sign: fragile), B.w = opacity, so the
+    // soft deviation's y = 100 alpha costs one product; alpha itself
+    // (= opacity * 2^p2, the decisions' operand) only on the large path.
+    // y may differ from fl(alpha * 100) in the last bit: that only moves a
+    // pair between the deviation fit and the exact sigmoid (|diff| < 2e-10).
+    const float e2 = ex2_approx(p2);
+    const float y = __fmul_rn(fabsf(A.w), e2);
     if (y < SOFT_Y0) {
       q.sdev = soft_dev_acc(y, q.sdev);
       continue;
     }
+    const float4 B = sB[j];
+    float alpha = __fmul_rn(B.w, e2);
     if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
       q.flag = true;
       q.nwk = k0 + j;
@@ -139,7 +144,6 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
       return false;
     }
     const float w = __fmul_rn(alpha, q.T);
-    const float4 B = sB[j];
     q.c0 = __fmaf_rn(B.x, w, q.c0);
     q.c1 = __fmaf_rn(B.y, w, q.c1);
     q.c2 = __fmaf_rn(B.z, w, q.c2);
@@ -195,8 +199,8 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         const StagedConic sc = stage_conic(co.x, co.y, co.z);
         const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
         sM[e] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
-        sA[e] = make_float4(sc.a2, sc.b2, sc.c2, co.w);  // opacity < 0 marks a fragile conic
-        sB[e] = col;
+        sA[e] = make_float4(sc.a2, sc.b2, sc.c2, __fmul_rn(co.w, 100.f));  // < 0 marks a fragile conic
+        sB[e] = make_float4(col.x, col.y, col.z, fabsf(co.w));
         fragile |= co.w < 0.f;
       }
     }
