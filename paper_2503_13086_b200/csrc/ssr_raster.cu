@@ -131,23 +131,26 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
     alpha = fminf(alpha, ALPHA_CAP_F);
     q.nbig++;
     q.sbig += (double)soft_sigmoid_accurate(alpha);
-    if (alpha < ALPHA_MIN_F) continue;
-    const float test = __fmul_rn(q.T, __fsub_rn(1.f, alpha));
-    if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
-      q.flag = true;
-      q.nwk = k0 + j;
+    // blend without a branch (most large-path lanes blend): a lane below
+    // 1/255 runs it with alpha = 0, i.e. T * 1 and colour + B * 0
+    const bool bl = alpha >= ALPHA_MIN_F;
+    const float ab = bl ? alpha : 0.f;
+    const float test = __fmul_rn(q.T, __fsub_rn(1.f, ab));
+    if (bl & ((fabsf(test - T_EPS_F) < T_EPS_F * band_t) | (test < T_EPS_F))) {
+      if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
+        q.flag = true;
+        q.nwk = k0 + j;
+      } else {
+        q.term = true;
+        q.nwk = k0 + j + 1;
+      }
       return false;
     }
-    if (test < T_EPS_F) {
-      q.term = true;
-      q.nwk = k0 + j + 1;
-      return false;
-    }
-    const float w = __fmul_rn(alpha, q.T);
+    const float w = __fmul_rn(ab, q.T);
     q.c0 = __fmaf_rn(B.x, w, q.c0);
     q.c1 = __fmaf_rn(B.y, w, q.c1);
     q.c2 = __fmaf_rn(B.z, w, q.c2);
-    q.hard++;
+    q.hard += bl ? 1 : 0;
     q.T = test;
   }
   return true;
