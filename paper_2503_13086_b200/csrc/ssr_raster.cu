@@ -123,7 +123,7 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
     }
     const float4 B = sB[j];
     float alpha = __fmul_rn(B.w, e2);
-    if (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band || fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band) {
+    if ((fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band)) {
       q.flag = true;
       q.nwk = k0 + j;
       return false;
