@@ -348,7 +348,16 @@ __device__ __forceinline__ void eval_slot(const SlotRaw& r, bool valid, double x
   q.capped = alpha > ALPHA_CAP;
   if (q.capped) alpha = ALPHA_CAP;
   q.alpha = alpha;
-  if (with_sv) q.sv = 1.0 / (1.0 + exp(-(alpha - ALPHA_MIN) / SOFT_TAU));
+  if (with_sv) {
+    // the soft-count term only has to meet the value tolerance (the walk's
+    // decisions above stay float64): the fp32 forward's split -- the float64
+    // constant S0 plus the fitted small-alpha deviation, the fp32 sigmoid
+    // above -- so no float64 exp / divide per slot and no systematic fp32
+    // rounding of S0 summed over long walks
+    const float af = (float)alpha;
+    const float y = __fmul_rn(af, 100.f);
+    q.sv = y < SOFT_Y0 ? SOFT_S0 + (double)soft_dev_acc(y, 0.f) : (double)soft_sigmoid_accurate(af);
+  }
   q.cand = alpha >= ALPHA_MIN;
   q.col[0] = r.k0.x;
   q.col[1] = r.k0.y;
