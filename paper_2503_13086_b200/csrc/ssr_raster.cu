@@ -123,21 +123,19 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const fl
     }
     const float4 B = sB[j];
     float alpha = __fmul_rn(B.w, e2);
-    if ((fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band)) {
-      q.flag = true;
-      q.nwk = k0 + j;
-      return false;
-    }
+    const bool fa = (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band);
     alpha = fminf(alpha, ALPHA_CAP_F);
-    q.nbig++;
+    q.nbig++;  // (also for a slot flagged here: the fix-up recomputes a flagged pixel)
     q.sbig += (double)soft_sigmoid_accurate(alpha);
     // blend without a branch (most large-path lanes blend): a lane below
     // 1/255 runs it with alpha = 0, i.e. T * 1 and colour + B * 0
     const bool bl = alpha >= ALPHA_MIN_F;
     const float ab = bl ? alpha : 0.f;
     const float test = __fmul_rn(q.T, __fsub_rn(1.f, ab));
-    if (bl & ((fabsf(test - T_EPS_F) < T_EPS_F * band_t) | (test < T_EPS_F))) {
-      if (fabsf(test - T_EPS_F) < T_EPS_F * band_t) {
+    const bool ft = bl & (fabsf(test - T_EPS_F) < T_EPS_F * band_t);
+    // one exit: an alpha guard band, a transmittance guard band, or termination
+    if (fa | ft | (bl & (test < T_EPS_F))) {
+      if (fa | ft) {
         q.flag = true;
         q.nwk = k0 + j;
       } else {
