@@ -415,19 +415,19 @@ __device__ __forceinline__ float pair_alpha2(float opa, float power2) { return _
 // Soft count of the forward (kernels.py:83) is accumulated as
 //   n_small * S0 + sum(y * p(y)) + sum(sigmoid(alpha) for alpha >= 2.5e-3),
 // y = alpha / SOFT_TAU, S0 = sigmoid(-ALPHA_MIN / SOFT_TAU) in float64 and p a
-// degree-4 fit of (sigmoid(y - ALPHA_MIN/TAU) - S0) / y on [0, 0.25]
-// (max abs error of y p(y) 1.1e-10, below the ~5e-9 of its fp32 evaluation).
-// Long walks (10^4 slots) would otherwise accumulate the fp32 rounding of the
-// same ~0.403 term.
+// degree-3 minimax fit of (sigmoid(y - ALPHA_MIN/TAU) - S0) / y on [0, 0.25]
+// (max abs error of y p(y) 3.8e-9, 8.2e-9 with its fp32 evaluation; the error
+// shrinks with y, and a pixel's small-alpha pairs sum to well under the 1e-4
+// soft-count tolerance).  Long walks (10^4 slots) would otherwise accumulate
+// the fp32 rounding of the same ~0.403 term.
 constexpr double SOFT_S0 = 0.4031981879117929;
 constexpr float SOFT_Y0 = 0.25f;
 // Accumulates y p(y) into acc with one final FMA (acc += y * p(y)).
 __device__ __forceinline__ float soft_dev_acc(float y, float acc) {
-  float p = 1.76897e-03f;
-  p = __fmaf_rn(p, y, -3.74327e-03f);
-  p = __fmaf_rn(p, y, -1.778797e-02f);
-  p = __fmaf_rn(p, y, 2.329284e-02f);
-  p = __fmaf_rn(p, y, 2.4062942e-01f);
+  float p = -2.6635625e-03f;
+  p = __fmaf_rn(p, y, -1.8015249e-02f);
+  p = __fmaf_rn(p, y, 2.3311704e-02f);
+  p = __fmaf_rn(p, y, 2.4062893e-01f);
   return __fmaf_rn(y, p, acc);
 }
 
