@@ -242,11 +242,12 @@ def main():
 
     grads_buf = [None]
 
-    def step(k, target=None):
+    def step(k, target=None, values_out=None):
         cam_i = (k * world + rank) % len(cams)
         cam = cams[cam_i]
         out = render(state.field, cam)
-        br = total_loss(out.image, targets[cam_i] if target is None else target, out, state.weights)
+        br = total_loss(out.image, targets[cam_i] if target is None else target, out, state.weights,
+                        values_out=values_out)
         if world > 1:
             # one view per rank: the chain writes every row (accumulate=False), so
             # the buffer needs no zero fill; the flat buffer is the all-reduce unit
@@ -344,9 +345,10 @@ def main():
         main_stream.wait_event(loaded[b])
         if k + 1 < args.steps:
             prefetch(k + 1)
-        br = step(args.warmup + k, target=dbuf[b])
+        # the loss kernel writes the step's five loss terms (40 bytes) straight
+        # into pinned host memory (mapped), so no copy sits in the stream
+        br = step(args.warmup + k, target=dbuf[b], values_out=host_vals[b])
         consumed[b].record(main_stream)
-        host_vals[b].copy_(br.values, non_blocking=True)  # loss terms back to the host (40 bytes)
         read_done[b].record(main_stream)
         if k > 0:
             read_done[1 - b].synchronize()
@@ -485,7 +487,8 @@ def main():
         "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40,
-                "target": f"{args.e2e_target} image uploaded every step (copy stream, overlapped); loss read back"},
+                "target": f"{args.e2e_target} image uploaded every step (copy stream, overlapped); loss terms "
+                          "written by the loss kernel into pinned host memory"},
         "gpu_launches": launches,
         "progressive": progressive,
         "clocks": clk.summary(),

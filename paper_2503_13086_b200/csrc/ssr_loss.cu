@@ -5,9 +5,10 @@
 //
 // k_ssim_fwd: 32x32 output tile per CTA with a 5-pixel halo in shared
 // memory; computes the five blurred moments, the SSIM map and the three
-// per-pixel adjoint maps (d_mu, d_gx2, d_gxy), plus L1 / SSIM / soft-count
-// partial sums (fp64 atomics).  k_loss_finalize turns the sums into the
-// scalars.  k_ssim_bwd blurs the adjoint maps (the window is self-adjoint)
+// per-pixel adjoint maps (d_mu, d_gx2, d_gxy), plus per-CTA L1 / SSIM /
+// soft-count partial sums (fp64, no atomics).  k_loss_finalize adds them in a
+// fixed order (so the scalars and d_soft are bit-identical run to run) and
+// turns them into the scalars.  k_ssim_bwd blurs the adjoint maps (the window is self-adjoint)
 // and writes d_image and d_soft.
 #include "ssr_common.cuh"
 
@@ -16,6 +17,7 @@ namespace ssr {
 constexpr int LT = 32;           // output tile edge
 constexpr int HALO = 5;          // (11 - 1) / 2
 constexpr int LH = LT + 2 * HALO; // 42
+constexpr int LOSS_TERMS = 6;  // l1, ssim, soft d, soft d^2, hard d, hard d^2 per CTA
 
 struct LossAcc {
   double l1_sum, ssim_sum, soft_d, soft_d2, hard_d, hard_d2, soft0, hard0;
@@ -62,7 +64,7 @@ template <bool U8>
 __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
                                                   const Target tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
-                                                  LossAcc* acc) {
+                                                  double* __restrict__ partials) {
   __shared__ float sx[LH][LH + 1], sy[LH][LH + 1];
   __shared__ float hz[5][LH][HZS];
   __shared__ double red[8];
@@ -200,24 +202,50 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
     hd += dh;
     hd2 += dh * dh;
   }
-  double v;
-  v = block_sum64(l1, red);
-  if (tid == 0) atomicAdd(&acc->l1_sum, v);
-  v = block_sum64(ss, red);
-  if (tid == 0) atomicAdd(&acc->ssim_sum, v);
-  v = block_sum64(sd, red);
-  if (tid == 0) atomicAdd(&acc->soft_d, v);
-  v = block_sum64(sd2, red);
-  if (tid == 0) atomicAdd(&acc->soft_d2, v);
-  v = block_sum64(hd, red);
-  if (tid == 0) atomicAdd(&acc->hard_d, v);
-  v = block_sum64(hd2, red);
-  if (tid == 0) atomicAdd(&acc->hard_d2, v);
+  // per-CTA partial sums (no atomics): k_loss_finalize adds them in a fixed
+  // order, so the scalar terms -- and d_soft, which depends on them -- are
+  // bit-identical run to run
+  double* part = partials + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * LOSS_TERMS;
+  const double vals[LOSS_TERMS] = {l1, ss, sd, sd2, hd, hd2};
+#pragma unroll
+  for (int j = 0; j < LOSS_TERMS; j++) {
+    const double v = block_sum64(vals[j], red);
+    if (tid == 0) part[j] = v;
+  }
 }
 
-__global__ void k_loss_finalize(int W, int H, double w_l1, double w_ssim, double w_load, const double* soft,
-                                LossAcc* acc, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+constexpr int FIN_THREADS = 256;
+
+__global__ void __launch_bounds__(FIN_THREADS) k_loss_finalize(int W, int H, double w_l1, double w_ssim,
+                                                               double w_load, const double* soft,
+                                                               const double* __restrict__ partials, int n_parts,
+                                                               LossAcc* acc, double* out) {
+  // fixed-order sums of the per-CTA partials: thread t adds parts t, t + 256,
+  // ... in order, then a fixed shuffle / warp-order tree
+  __shared__ double red[FIN_THREADS / 32][LOSS_TERMS];
+  double tsum[LOSS_TERMS] = {0, 0, 0, 0, 0, 0};
+  for (int c = threadIdx.x; c < n_parts; c += FIN_THREADS)
+#pragma unroll
+    for (int j = 0; j < LOSS_TERMS; j++) tsum[j] += partials[(size_t)c * LOSS_TERMS + j];
+#pragma unroll
+  for (int j = 0; j < LOSS_TERMS; j++) {
+    for (int o = 16; o > 0; o >>= 1) tsum[j] += __shfl_xor_sync(0xffffffffu, tsum[j], o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = tsum[j];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+#pragma unroll
+  for (int j = 0; j < LOSS_TERMS; j++) {
+    double v = 0.0;
+    for (int w = 0; w < FIN_THREADS / 32; w++) v += red[w][j];
+    tsum[j] = v;
+  }
+  acc->l1_sum = tsum[0];
+  acc->ssim_sum = tsum[1];
+  acc->soft_d = tsum[2];
+  acc->soft_d2 = tsum[3];
+  acc->hard_d = tsum[4];
+  acc->hard_d2 = tsum[5];
   const double n = (double)W * H;
   const double n_crop = (double)(W - 2 * HALO) * (H - 2 * HALO);
   const double l1 = acc->l1_sum / (n * 3.0);
@@ -367,8 +395,13 @@ static int ensure_window() {
 
 using namespace ssr;
 
+static int64_t loss_ctas(int32_t width, int32_t height) {
+  return (int64_t)((width + LT - 1) / LT) * ((height + LT - 1) / LT);
+}
+
 extern "C" int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes) {
-  *bytes = align_up((int64_t)9 * width * height * 4, 256) + align_up(sizeof(LossAcc), 256);
+  *bytes = align_up((int64_t)9 * width * height * 4, 256) + align_up(sizeof(LossAcc), 256) +
+           align_up(loss_ctas(width, height) * LOSS_TERMS * 8, 256);
   return SSR_OK;
 }
 
@@ -394,15 +427,16 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   cudaStream_t st = (cudaStream_t)stream;
   float* dmaps = (float*)workspace;
   LossAcc* acc = (LossAcc*)((char*)workspace + align_up((int64_t)9 * width * height * 4, 256));
-  SSR_TRY(check_cuda(cudaMemsetAsync(acc, 0, sizeof(LossAcc), st), "loss acc"));
+  double* partials = (double*)((char*)acc + align_up(sizeof(LossAcc), 256));
   dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
   const Target tg{target, target_u8 ? 1 : 0};
   if (tg.u8)
-    k_ssim_fwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
+    k_ssim_fwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, partials);
   else
-    k_ssim_fwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, acc);
+    k_ssim_fwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, partials);
   SSR_TRY(check_launch("k_ssim_fwd"));
-  k_loss_finalize<<<1, 32, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, acc, out);
+  k_loss_finalize<<<1, FIN_THREADS, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, partials,
+                                             (int)loss_ctas(width, height), acc, out);
   SSR_TRY(check_launch("k_loss_finalize"));
   if (tg.u8)
     k_ssim_bwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,

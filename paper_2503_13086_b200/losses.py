@@ -33,14 +33,17 @@ class LossWeights:
 class LossBreakdown:
     """d_image (H,W,3) / d_soft (H,W) device tensors plus lazily-read scalars."""
 
-    def __init__(self, values: torch.Tensor, d_image: torch.Tensor, d_soft: torch.Tensor):
-        self.values = values  # float64 device: l1, ssim_loss, load, total, hard_count_std
+    def __init__(self, values: torch.Tensor, d_image: torch.Tensor, d_soft: torch.Tensor, ready=None):
+        self.values = values  # float64 (device, or pinned host): l1, ssim_loss, load, total, hard_count_std
         self.d_image = d_image
         self.d_soft = d_soft
+        self._ready = ready  # event after the write when values is pinned host memory
         self._host = None
 
     def _get(self, i):
         if self._host is None:
+            if self._ready is not None:
+                self._ready.synchronize()
             self._host = self.values.cpu().tolist()
         return float(self._host[i])
 
@@ -62,11 +65,15 @@ class _Workspace:
         return cls.cache[key]
 
 
-def total_loss(rendered, target, output, weights: LossWeights) -> LossBreakdown:
+def total_loss(rendered, target, output, weights: LossWeights, values_out: torch.Tensor | None = None
+               ) -> LossBreakdown:
     """Weighted objective over one rendered view (losses.py:147-173).
 
     ``target`` is float in [0, 1] or uint8 (value / 255, as the reference's
-    io/images.py loads its 8-bit image files)."""
+    io/images.py loads its 8-bit image files).  ``values_out`` (optional): a
+    pinned host float64 tensor of 5 the kernel writes the scalar terms into
+    directly (mapped host memory), so reading them back needs no copy on the
+    stream; the breakdown's properties wait for that write."""
     rendered = torch.as_tensor(rendered)
     target = torch.as_tensor(target)
     if tuple(rendered.shape) != tuple(target.shape) or rendered.dim() != 3 or rendered.shape[2] != 3:
@@ -83,13 +90,23 @@ def total_loss(rendered, target, output, weights: LossWeights) -> LossBreakdown:
     hard = output.hard_count.to(dtype=torch.int32).contiguous()
     d_image = torch.empty_like(x)
     d_soft = torch.empty(soft.shape, dtype=torch.float32, device=dev)
-    vals = torch.empty(5, dtype=torch.float64, device=dev)
+    if values_out is not None:
+        if values_out.device.type != "cpu" or not values_out.is_pinned() or values_out.dtype != torch.float64 \
+                or values_out.numel() < 5 or not values_out.is_contiguous():
+            raise InvalidParameter("values_out must be a contiguous pinned host float64 tensor of >= 5 elements")
+        vals = values_out
+    else:
+        vals = torch.empty(5, dtype=torch.float64, device=dev)
     ws = _Workspace.get(w, h, dev)
     _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), 1 if u8 else 0, soft.data_ptr(), hard.data_ptr(),
               float(weights.l1),
               float(weights.ssim), float(weights.load), d_image.data_ptr(), d_soft.data_ptr(), vals.data_ptr(),
               ws.data_ptr(), ws.numel(), _lib.stream_ptr())
-    return LossBreakdown(vals, d_image, d_soft)
+    ready = None
+    if values_out is not None:
+        ready = torch.cuda.Event()
+        ready.record()
+    return LossBreakdown(vals, d_image, d_soft, ready)
 
 
 def psnr(rendered, target) -> float:

@@ -370,3 +370,27 @@ def test_instance_capacity_reuse_and_growth():
     fields_equal(r_big, ref_big)
     fields_equal(r_big2, ref_big)
     fields_equal(r_small2, ref_small)
+
+
+def test_loss_values_into_pinned_host_memory():
+    """total_loss(values_out=pinned host tensor): the kernel writes the scalar
+    terms straight into mapped host memory; same values as the device buffer."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.errors import InvalidParameter
+    from paper_2503_13086_b200.losses import LossWeights, total_loss
+    from paper_2503_13086_b200.rasterize import render
+
+    f = GaussianField.from_host(scenes.make_params(0, seed=4, n=3000))
+    out = render(f, scenes.camera(0, view=2, width=80, height=64))
+    tgt = torch.rand((64, 80, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    w = LossWeights()
+    ref = total_loss(out.image, tgt, out, w)
+    host = torch.zeros(5, dtype=torch.float64).pin_memory()
+    br = total_loss(out.image, tgt, out, w, values_out=host)
+    for name in ("l1", "ssim_loss", "load", "total", "hard_count_std"):
+        assert getattr(br, name) == getattr(ref, name), name
+    assert torch.equal(br.d_image, ref.d_image) and torch.equal(br.d_soft, ref.d_soft)
+    with pytest.raises(InvalidParameter):
+        total_loss(out.image, tgt, out, w, values_out=torch.zeros(5, dtype=torch.float64))
