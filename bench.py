@@ -271,13 +271,31 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # the e2e loop below replays the warm-up from this same state (field,
+    # moments, step counts, densify statistics), so both loops time the same
+    # iterations on the same field
+    opt = state.optimizer
+    snap = (field.flat.clone(), opt.m.clone(), opt.v.clone(), dict(opt.steps), state.stats.clone(),
+            state.global_iteration)
+
+    def restore():
+        field.flat.copy_(snap[0])
+        opt.m.copy_(snap[1])
+        opt.v.copy_(snap[2])
+        opt.steps = dict(snap[3])
+        state.stats.copy_(snap[4])
+        state.global_iteration = snap[5]
+
     # prime the caching allocator with every view's buffer sizes (instance counts
     # differ per view), then the W warm-up steps proper
-    for k in range(len(cams) // world):
-        step(k)
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
+    def prime_and_warm():
+        for k in range(len(cams) // world):
+            step(k)
+        for k in range(args.warmup):
+            step(k)
+        torch.cuda.synchronize()
+
+    prime_and_warm()
     # ---------------- timed region (device time, CUDA events on the launching stream)
     barrier()
     torch.cuda.synchronize()
@@ -333,11 +351,19 @@ def main():
             dbuf[b].copy_(pinned[view_of(k)], non_blocking=True)
             loaded[b].record(copy_stream)
 
+    restore()
+    prime_and_warm()
     barrier()
     torch.cuda.synchronize()
     for e in consumed:
         e.record(main_stream)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = None
+    if os.environ.get("SSR_E2E_GAPS"):  # diagnostics: device-timeline gaps of the e2e loop (stderr)
+        from torch.profiler import ProfilerActivity, profile
+
+        prof = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+        prof.__enter__()
     f0.record()
     prefetch(0)
     for k in range(args.steps):
@@ -357,8 +383,27 @@ def main():
     losses_seen.append(float(host_vals[(args.steps - 1) % 2][3]))
     f1.record()
     torch.cuda.synchronize()
+    if prof is not None:
+        prof.__exit__(None, None, None)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import contextlib
+
+        from gap_profile import analyse
+
+        with contextlib.redirect_stdout(sys.stderr):
+            analyse(prof, args.steps)
     barrier()
     assert len(losses_seen) == args.steps and all(np.isfinite(losses_seen))
+    if os.environ.get("SSR_E2E_REPEAT"):  # diagnostics: the device-timed loop again, after the e2e loop
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for k in range(args.steps):
+            step(args.warmup + k)
+        g1.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"device_loop_again_its": args.steps / (g0.elapsed_time(g1) / 1e3),
+                          "e2e_its": args.steps / (f0.elapsed_time(f1) / 1e3)}), file=sys.stderr, flush=True)
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
