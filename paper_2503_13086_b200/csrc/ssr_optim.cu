@@ -112,11 +112,59 @@ struct FlagBit {
 };
 
 // field.py:329-372 + optim.py:49-54: kept rows, then clones, then split pairs.
+// Kept rows (field.py:303-375 compaction): one warp per 32 source rows copies
+// each class region's 32 * width contiguous source floats lane-strided
+// (coalesced reads; the kept rows land contiguously, so the writes are too)
+// into their compacted positions, for the parameters and both moments.
+template <int W>
+__device__ __forceinline__ void keep_copy(const float* __restrict__ src, float* __restrict__ dst, int64_t i0,
+                                          int rows, unsigned keep, uint32_t my_off, int lane) {
+  for (int e0 = 0; e0 < rows * W; e0 += 32) {  // same trip count on every lane (the shuffle)
+    const int e = e0 + lane;
+    const int r = min(e / W, 31), j = e - (e / W) * W;
+    const uint32_t off = __shfl_sync(0xffffffffu, my_off, r);
+    if (e < rows * W && ((keep >> r) & 1u)) dst[(int64_t)off * W + j] = src[(i0 + r) * W + j];
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_densify_keep(int64_t n, int64_t n_new, const float* __restrict__ src,
+                                                      const float* __restrict__ m, const float* __restrict__ v,
+                                                      const uint8_t* __restrict__ flags,
+                                                      const uint32_t* __restrict__ keep_off, float* __restrict__ dst,
+                                                      float* __restrict__ new_m, float* __restrict__ new_v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  if (i0 >= n) return;
+  const int rows = (int)min((int64_t)32, n - i0);
+  const bool mine = lane < rows;
+  const bool kp = mine && (flags[i0 + lane] & 1);
+  const unsigned keep = __ballot_sync(0xffffffffu, kp);
+  if (!keep) return;
+  const uint32_t my_off = mine ? keep_off[i0 + lane] : 0u;
+  const int64_t ns = row_stride(n), nns = row_stride(n_new);
+  const float* srcs[3] = {src, m, v};
+  float* dsts[3] = {dst, new_m, new_v};
+#pragma unroll
+  for (int b = 0; b < 3; b++) {
+    if (!dsts[b]) continue;
+    const float* sb = srcs[b];
+    float* db = dsts[b];
+    keep_copy<3>(sb, db, i0, rows, keep, my_off, lane);
+    keep_copy<4>(sb + 3 * ns, db + 3 * nns, i0, rows, keep, my_off, lane);
+    keep_copy<3>(sb + 7 * ns, db + 7 * nns, i0, rows, keep, my_off, lane);
+    keep_copy<1>(sb + 10 * ns, db + 10 * nns, i0, rows, keep, my_off, lane);
+    keep_copy<3 * K>(sb + 11 * ns, db + 11 * nns, i0, rows, keep, my_off, lane);
+  }
+}
+
 __global__ void k_densify_apply(int64_t n, int64_t n_new, int K, const float* __restrict__ src, const float* m,
                                 const float* v, const uint8_t* __restrict__ flags,
                                 const uint32_t* __restrict__ keep_off, const uint32_t* __restrict__ clone_off,
                                 const uint32_t* __restrict__ split_off, const double* __restrict__ eps, double log_shrink, float* __restrict__ dst,
                                 float* new_m, float* new_v) {
+  // kept rows are copied by k_densify_keep; this kernel writes the clones and
+  // the split children
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint8_t f = flags[i];
@@ -127,16 +175,6 @@ __global__ void k_densify_apply(int64_t n, int64_t n_new, int K, const float* __
   const int64_t ns = row_stride(n), nns = row_stride(n_new);
   const int64_t so[5] = {0, 3 * ns, 7 * ns, 10 * ns, 11 * ns};
   const int64_t dof[5] = {0, 3 * nns, 7 * nns, 10 * nns, 11 * nns};
-  if (f & 1) {
-    const int64_t d = keep_off[i];
-    for (int c = 0; c < 5; c++)
-      for (int j = 0; j < width[c]; j++) {
-        const int64_t s = so[c] + i * width[c] + j, t = dof[c] + d * width[c] + j;
-        dst[t] = src[s];
-        if (new_m) new_m[t] = m[s];
-        if (new_v) new_v[t] = v[s];
-      }
-  }
   if (f & 2) {
     const int64_t d = (int64_t)n_keep + clone_off[i];
     for (int c = 0; c < 5; c++)
@@ -276,6 +314,14 @@ extern "C" int ssr_densify_apply(int64_t n, int64_t n_new, int32_t sh_degree, co
     size_t tb2 = tb;
     SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)w, tb2, it, offs[b], (int)n, st), "densify scan"));
   }
+  const unsigned kb = (unsigned)((n + 255) / 256);
+  switch (K) {
+    case 1: k_densify_keep<1><<<kb, 256, 0, st>>>(n, n_new, params, m, v, flags, offs[0], new_params, new_m, new_v); break;
+    case 4: k_densify_keep<4><<<kb, 256, 0, st>>>(n, n_new, params, m, v, flags, offs[0], new_params, new_m, new_v); break;
+    case 9: k_densify_keep<9><<<kb, 256, 0, st>>>(n, n_new, params, m, v, flags, offs[0], new_params, new_m, new_v); break;
+    default: k_densify_keep<16><<<kb, 256, 0, st>>>(n, n_new, params, m, v, flags, offs[0], new_params, new_m, new_v); break;
+  }
+  SSR_TRY(check_launch("k_densify_keep"));
   k_densify_apply<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, n_new, K, params, m, v, flags, offs[0], offs[1],
                                                                offs[2], eps, log_shrink, new_params,
                                                                new_m, new_v);
