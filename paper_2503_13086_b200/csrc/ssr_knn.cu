@@ -4,7 +4,7 @@
 // filter (field.py:139-151) and median_nn_spacing (field.py:154-161).
 //
 // Build: counting sort of the pool by cell (histogram -> scan -> scatter),
-// coordinates copied into cell order.  Query: one thread per query walks
+// coordinates copied into cell order.  Query: one warp per query walks
 // Chebyshev rings of cells around its cell and keeps the k smallest squared
 // distances; after ring r every unseen point is at least r*h away (the query
 // lies inside its own cell, the bbox covers pool and queries), so the walk
@@ -51,10 +51,40 @@ __global__ void k_knn_scatter(int64_t n, const double* __restrict__ pool, const 
   sorted[(int64_t)pos * 3 + 2] = pool[i * 3 + 2];
 }
 
-__global__ void __launch_bounds__(128) k_knn_query(int64_t nq, const double* __restrict__ queries, int k, Grid g,
-                                                   const uint32_t* __restrict__ start,
-                                                   const double* __restrict__ sorted, double* __restrict__ out) {
-  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per query: the rows of cells of each Chebyshev ring are split over
+// the lanes (each lane keeps its own k smallest squared distances), and after
+// every ring the warp merges the lanes' lists to test the stop condition, so
+// a query whose nearest points are many rings away is searched 32 cells at a
+// time.  The k smallest distances of a set do not depend on the visiting
+// order, so the result equals the one-thread walk's.
+constexpr int KNN_WARPS = 4;
+
+// k-th smallest (1-based kk) of the union of the lanes' sorted lists, without
+// consuming them (work on copies), warp-uniform result.
+__device__ __forceinline__ double warp_kth(const double* best, int k) {
+  double head[KNN_MAX_K];
+  for (int j = 0; j < KNN_MAX_K; j++) head[j] = best[j];
+  int pos = 0;
+  double v = CUDART_INF;
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < k; j++) {
+    const double mine = pos < k ? head[pos] : CUDART_INF;
+    double m = mine;
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    v = m;
+    // the lowest lane holding the minimum pops it
+    const unsigned who = __ballot_sync(0xffffffffu, mine == m);
+    if (lane == __ffs(who) - 1) pos++;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_query(int64_t nq, const double* __restrict__ queries, int k,
+                                                              Grid g, const uint32_t* __restrict__ start,
+                                                              const double* __restrict__ sorted,
+                                                              double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = (int64_t)blockIdx.x * KNN_WARPS + (threadIdx.x >> 5);
   if (qi >= nq) return;
   const double qx = queries[qi * 3], qy = queries[qi * 3 + 1], qz = queries[qi * 3 + 2];
   const int cx = cell_coord(qx, g.bx, g.inv_h, g.dx);
@@ -65,42 +95,54 @@ __global__ void __launch_bounds__(128) k_knn_query(int64_t nq, const double* __r
   int found = 0;
   const int rmax = max(g.dx, max(g.dy, g.dz));
   for (int r = 0; r <= rmax; r++) {
-    for (int oz = -r; oz <= r; oz++) {
-      const int z = cz + oz;
-      if (z < 0 || z >= g.dz) continue;
-      for (int oy = -r; oy <= r; oy++) {
-        const int y = cy + oy;
-        if (y < 0 || y >= g.dy) continue;
-        const bool face = (oz == -r || oz == r || oy == -r || oy == r);
-        const int step = face ? 1 : 2 * r;  // interior rows: only the two x faces
-        for (int ox = -r; ox <= r; ox += (step > 0 ? step : 1)) {
-          const int x = cx + ox;
-          if (x < 0 || x >= g.dx) continue;
-          const uint32_t c = ((uint32_t)z * g.dy + y) * g.dx + x;
-          const uint32_t e = start[c + 1];
-          for (uint32_t p = start[c]; p < e; p++) {
-            const double ddx = sorted[(int64_t)p * 3] - qx;
-            const double ddy = sorted[(int64_t)p * 3 + 1] - qy;
-            const double ddz = sorted[(int64_t)p * 3 + 2] - qz;
-            const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
-            if (d2 < best[k - 1]) {
-              int j = k - 1;
-              while (j > 0 && best[j - 1] > d2) {
-                best[j] = best[j - 1];
-                j--;
-              }
-              best[j] = d2;
+    const int side = 2 * r + 1;
+    // rows (oz, oy) of the ring, lane-strided; a face row holds all x, an
+    // interior row only x = -r and x = +r
+    for (int row = lane; row < side * side; row += 32) {
+      const int oz = row / side - r, oy = row % side - r;
+      const int z = cz + oz, y = cy + oy;
+      if (z < 0 || z >= g.dz || y < 0 || y >= g.dy) continue;
+      const bool face = (oz == -r || oz == r || oy == -r || oy == r);
+      const int step = (face || r == 0) ? 1 : 2 * r;
+      for (int ox = -r; ox <= r; ox += step) {
+        const int x = cx + ox;
+        if (x < 0 || x >= g.dx) continue;
+        const uint32_t c = ((uint32_t)z * g.dy + y) * g.dx + x;
+        const uint32_t e = start[c + 1];
+        for (uint32_t p = start[c]; p < e; p++) {
+          const double ddx = sorted[(int64_t)p * 3] - qx;
+          const double ddy = sorted[(int64_t)p * 3 + 1] - qy;
+          const double ddz = sorted[(int64_t)p * 3 + 2] - qz;
+          const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
+          if (d2 < best[k - 1]) {
+            int j = k - 1;
+            while (j > 0 && best[j - 1] > d2) {
+              best[j] = best[j - 1];
+              j--;
             }
-            found++;
+            best[j] = d2;
           }
-          if (r == 0) break;
+          found++;
         }
       }
     }
-    const double reach = (double)r * g.h;
-    if (found >= k && best[k - 1] <= reach * reach) break;
+    int total = found;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    if (total >= k) {
+      const double reach = (double)r * g.h;
+      if (warp_kth(best, k) <= reach * reach) break;
+    }
   }
-  for (int j = 0; j < k; j++) out[qi * k + j] = sqrt(best[j]);
+  // the k smallest of the lanes' lists, in ascending order
+  int pos = 0;
+  for (int j = 0; j < k; j++) {
+    const double mine = pos < k ? best[pos] : CUDART_INF;
+    double m = mine;
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const unsigned who = __ballot_sync(0xffffffffu, mine == m);
+    if (lane == __ffs(who) - 1) pos++;
+    if (lane == 0) out[qi * k + j] = sqrt(m);
+  }
 }
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -174,6 +216,7 @@ extern "C" int ssr_knn(const double* pool, int64_t n_pool, const double* queries
     k_knn_scatter<<<(unsigned)((n_pool + 255) / 256), 256, 0, st>>>(n_pool, pool, cell_of, cursor, sorted);
     SSR_TRY(check_launch("k_knn_scatter"));
   }
-  k_knn_query<<<(unsigned)((n_q + 127) / 128), 128, 0, st>>>(n_q, queries, k, g, start, sorted, out_dist);
+  k_knn_query<<<(unsigned)((n_q + KNN_WARPS - 1) / KNN_WARPS), KNN_WARPS * 32, 0, st>>>(n_q, queries, k, g, start,
+                                                                                      sorted, out_dist);
   return check_launch("k_knn_query");
 }
