@@ -52,6 +52,16 @@ def flat_size(n: int, k: int, extra: int = 0) -> int:
     return (11 + 3 * k + extra) * row_stride(n)
 
 
+def alloc_growing(numel: int, device, dtype=torch.float32) -> torch.Tensor:
+    """Uninitialised 1-D buffer of ``numel`` elements whose allocation is rounded
+    up to 1/16 of the size's leading power of two, so a buffer that grows by a
+    little every event (field expansion) reuses the block its predecessor
+    freed instead of a fresh device allocation each time."""
+    step = 1 << max(20, int(numel).bit_length() - 4)
+    cap = (int(numel) + step - 1) // step * step
+    return torch.empty(cap, dtype=dtype, device=device)[:numel]
+
+
 def pack_classes(parts, n: int, k: int, device, dtype=torch.float32) -> torch.Tensor:
     """Flat, padded class-major buffer from the five class arrays (each n rows)."""
     flat = torch.zeros(flat_size(n, k), dtype=dtype, device=device)
@@ -241,7 +251,7 @@ class GaussianField:
         n_add = parts[0].shape[0]
         n_old, k = self._n, self.n_sh_coeffs
         n_tot = n_old + n_add
-        flat = torch.empty(flat_size(n_tot, k), dtype=torch.float32, device=self.device)
+        flat = alloc_growing(flat_size(n_tot, k), self.device)
         old_sl, new_sl = class_slices(n_old, k), class_slices(n_tot, k)
         for (o_off, w), (n_off, _), part in zip(old_sl, new_sl, parts):
             if n_old:

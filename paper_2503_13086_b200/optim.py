@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from .errors import InvalidParameter, StaleFieldError
-from .field import CLASSES, class_slices, flat_size, pack_classes
+from .field import CLASSES, alloc_growing, class_slices, flat_size, pack_classes, row_stride
 
 BETA1 = 0.9
 BETA2 = 0.999
@@ -83,9 +83,11 @@ class FieldOptimizer:
 
     def _grow(self, buf, n_added):
         n, k = self.n_rows, (self.sh_degree + 1) ** 2
-        out = torch.zeros(flat_size(n + n_added, k), dtype=buf.dtype, device=buf.device)
-        for (o_off, w), (n_off, _) in zip(class_slices(n, k), class_slices(n + n_added, k)):
+        n_tot = n + n_added
+        out = alloc_growing(flat_size(n_tot, k), buf.device, buf.dtype)
+        for (o_off, w), (n_off, _) in zip(class_slices(n, k), class_slices(n_tot, k)):
             out[n_off: n_off + w * n] = buf[o_off: o_off + w * n]
+            out[n_off + w * n: n_off + w * row_stride(n_tot)] = 0.0  # new rows start cold; padding zero
         return out
 
     def step(self, fld, grads, position_rate):

@@ -47,3 +47,14 @@ def insert():
 timed("insert_arrays (total)", insert, reps=1)
 keep = np.ones(n0, dtype=bool)
 timed("optimizer.sync (grow moments)", lambda: opt.sync(field, keep, len(field) - n0), reps=1)
+
+
+# steady state: three more events (expansion + moment growth each)
+for ev in range(3):
+    n0 = len(field)
+
+    def one_event():
+        field.insert_arrays(pos + 0.01 * (ev + 1), cols)
+        opt.sync(field, np.ones(n0, dtype=bool), len(field) - n0)
+
+    timed(f"event {ev}: insert_arrays + optimizer.sync", one_event, reps=1)
