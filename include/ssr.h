@@ -86,7 +86,7 @@ typedef struct ssr_frame {
                         * then n_tiles slots (first pixel entry of each
                         * flagged tile, unordered), n_tiles bucket-plan
                         * slots, then W*H pixel entries (tile << 8 | pixel in tile),
-                        * contiguous per tile and in pixel order within it */
+                        * contiguous per tile, in a fixed order within it */
 } ssr_frame;
 
 const char* ssr_last_error(void);

@@ -162,11 +162,16 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const int tid = threadIdx.x;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int x00 = tx * TILE, y00 = ty * TILE;
-  const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
+  // warp w covers the 8x4 pixel block (w & 1, w >> 1) of the tile: a splat's
+  // footprint splits the lanes of a compact block less often than a 16x2 strip
+  const int lane_ = tid & 31, wrp = tid >> 5;
+  const int lx = (wrp & 1) * 8 + (lane_ & 7), ly = (wrp >> 1) * 4 + (lane_ >> 3);
+  const int pidx = ly * TILE + lx;  // row-major pixel index in the tile (checkpoints, fix list)
+  const int px = x00 + lx, py = y00 + ly;
   const bool inside = px < a.width && py < a.height;
   const int2 rg = a.ranges[t];
   const int s0 = rg.x, s1 = rg.y;
-  const float fpx = (float)(tid & 15), fpy = (float)(tid >> 4);
+  const float fpx = (float)lx, fpy = (float)ly;
   const float band = a.band, band_t = a.band_t;
 
   __shared__ float4 sM[FWD_BATCH];  // staged mean (x int, x frac, y int, y frac)
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   q.nbig = 0;
   q.term = q.flag = false;
   bool done = !inside;
-  float4* ck = a.ckpt + ckpt_base(s0, t) + tid;
+  float4* ck = a.ckpt + ckpt_base(s0, t) + pidx;
 
   for (int base = s0; base < s1; base += FWD_BATCH) {
     if (__syncthreads_count(done) == TILE_PX) break;
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
     if (fl) {
       int r = __popc(fm & ((1u << (tid & 31)) - 1u));
       for (int w = 0; w < (tid >> 5); w++) r += sCnt[w];
-      fix_pixels(a)[sBase + r] = (t << 8) | tid;
+      fix_pixels(a)[sBase + r] = (t << 8) | pidx;
     }
   }
 }
