@@ -394,3 +394,98 @@ def test_loss_values_into_pinned_host_memory():
     assert torch.equal(br.d_image, ref.d_image) and torch.equal(br.d_soft, ref.d_soft)
     with pytest.raises(InvalidParameter):
         total_loss(out.image, tgt, out, w, values_out=torch.zeros(5, dtype=torch.float64))
+
+
+def test_render_invariants_and_stale_render_rejected():
+    """test_rasterize.py:109-118 invariants (image in [0, 1], T in (0, 1], hard <= n_walk,
+    soft <= n_walk) and :254-259 (a render of an older field generation is rejected)."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.errors import StaleFieldError
+    from paper_2503_13086_b200.rasterize import backward, render
+
+    f = GaussianField.from_host(scenes.make_params(1, seed=6, n=20000))
+    out = render(f, scenes.camera(1, view=4, width=200, height=150))
+    img, t = out.image, out.t_final
+    assert float(img.min()) >= 0.0 and float(img.max()) <= 1.0
+    assert float(t.min()) > 0.0 and float(t.max()) <= 1.0
+    nw = out.n_walk.to(torch.int64)
+    assert bool((out.hard_count.to(torch.int64) <= nw).all())
+    assert bool((out.soft_count <= nw.to(torch.float64) + 1e-9).all())
+    f.insert_arrays(np.array([[0.0, 0.0, 1.0]]), np.array([[0.5, 0.5, 0.5]]))
+    with pytest.raises(StaleFieldError):
+        backward(f, out, torch.zeros_like(out.image))
+
+
+def test_iteration_is_bit_deterministic():
+    """Same state, same view: render + loss + fused backward/Adam twice give bit-identical
+    parameters, moments and loss terms (the reference's worker-count invariance)."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.train import TrainState, train_iteration
+
+    hp = scenes.make_params(1, seed=8, n=30000)
+    cam = scenes.camera(1, view=5, width=240, height=160)
+    target = torch.rand((160, 240, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    runs = []
+    for _ in range(2):
+        f = GaussianField.from_host(hp)
+        st = TrainState(field=f, optimizer=FieldOptimizer(f, 3.0), weights=LossWeights(), densify_enabled=False)
+        totals = [train_iteration(st, cam, target, 1e-4).total for _ in range(3)]
+        torch.cuda.synchronize()
+        runs.append((f.flat.clone(), st.optimizer.m.clone(), st.optimizer.v.clone(), totals))
+    a, b = runs
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    assert a[3] == b[3]
+
+
+def test_gradient_matches_finite_differences():
+    """test_rasterize.py:158-191 style: for every parameter class, the directional
+    derivative of a linear image functional along a random direction matches central
+    differences of the CUDA forward.  Pixels whose discrete decisions (blend set,
+    termination, guard-band flag) differ between the +eps / -eps renders are left out
+    of both sides (the functional is masked before the backward); eps = 1e-4 keeps the
+    position curvature term below the bar; relative 2e-2 plus an fp32 noise floor."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.field import class_slices
+    from paper_2503_13086_b200.rasterize import backward, render
+
+    hp = scenes.make_params(0, seed=11, n=400)
+    cam = scenes.camera(0, view=2, width=64, height=48)
+    f = GaussianField.from_host(hp)
+    n, k = len(f), f.n_sh_coeffs
+    gen = torch.Generator("cuda").manual_seed(5)
+    w = torch.randn((48, 64, 3), device="cuda", generator=gen)
+    base = f.flat.clone()
+    out0 = render(f, cam)
+    eps = 1e-4
+    names = ("positions", "rotations", "log_scales", "opacity_logits", "sh")
+    for (off, width), name in zip(class_slices(n, k), names):
+        d = torch.zeros_like(base)
+        d[off: off + width * n] = torch.randn(width * n, device="cuda", generator=gen)
+        imgs, same = [], (out0.flagged == 0)
+        for sgn in (1.0, -1.0):
+            f.flat.copy_(base + sgn * eps * d)
+            o = render(f, cam)
+            imgs.append(o.image.double())
+            same &= (o.n_walk == out0.n_walk) & (o.hard_count == out0.hard_count) & (o.flagged == 0)
+            # a changed (tile, depth) order -- two splats swapping depth -- is a jump too
+            for t in range(out0.splats.tiles_x * out0.splats.tiles_y):
+                a0, a1 = (int(v) for v in out0.splats.tile_ranges[t])
+                b0, b1 = (int(v) for v in o.splats.tile_ranges[t])
+                if a1 - a0 != b1 - b0 or not torch.equal(out0.splats.inst_gauss[a0:a1], o.splats.inst_gauss[b0:b1]):
+                    ty, tx = divmod(t, out0.splats.tiles_x)
+                    same[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = False
+        f.flat.copy_(base)
+        assert float(same.float().mean()) > 0.3, name
+        wm = w * same[..., None].float()
+        fd = float(((imgs[0] - imgs[1]) * wm.double()).sum()) / (2 * eps)
+        g = backward(f, render(f, cam), wm)
+        analytic = float((getattr(g, name).reshape(-1).double() * d[off: off + width * n].double()).sum())
+        assert abs(fd - analytic) <= 2e-2 * abs(analytic) + 1e-2, (name, fd, analytic)
