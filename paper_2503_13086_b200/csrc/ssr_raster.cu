@@ -375,10 +375,18 @@ struct Pix64 {
 // Front-to-back walk of one pixel by one warp (lanes = 32 consecutive slots).
 // When ck != nullptr the fp32 bucket checkpoint (T, C_front) of every chunk
 // boundary is written for the backward fix-up (chunks coincide with buckets).
+//
+// `kfast`: walk slots before which every decision is known to agree with the
+// fp32 walk (a flagged pixel's first ambiguous slot): whole chunks before it
+// cannot terminate, so they skip the termination test and the per-chunk
+// colour / soft-count reductions (each lane accumulates its own terms, reduced
+// once when the light chunks end) and keep the fp32 forward's checkpoints.
 __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, double yy, Pix64& r,
-                             float4* ck = nullptr) {
+                             float4* ck = nullptr, int kfast = 0) {
   const int lane = threadIdx.x & 31;
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, soft = 0.0;
+  double lc0 = 0.0, lc1 = 0.0, lc2 = 0.0, lsoft = 0.0;  // light-chunk per-lane sums
+  bool light_pending = false;
   int hard = 0, nw = s1 - s0, term = 0;
   // Two-stage prefetch: the next chunk's field data and the index of the one
   // after it are in flight while the current chunk is evaluated.
@@ -386,7 +394,15 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
   load_slot(a, s0 + lane, s1, cur);
   uint32_t g_next = s0 + 32 + lane < s1 ? a.inst[s0 + 32 + lane] : 0u;
   for (int cb = s0; cb < s1; cb += 32) {
-    if (ck && cb > s0 && lane == 0)
+    const bool light = cb - s0 + 32 <= kfast;
+    if (!light && light_pending) {  // leaving the light chunks: reduce their per-lane sums
+      C0 += warp_sum64(lc0);
+      C1 += warp_sum64(lc1);
+      C2 += warp_sum64(lc2);
+      soft += warp_sum64(lsoft);
+      light_pending = false;
+    }
+    if (ck && cb > s0 && !light && lane == 0)
       ck[(size_t)((cb - s0) >> 5) * TILE_PX] = make_float4((float)T, (float)C0, (float)C1, (float)C2);
     SlotRaw nxt;
     nxt.valid = cb + 32 + lane < s1;
@@ -410,6 +426,18 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
     double Pex = __shfl_up_sync(FULL, P, 1);
     if (lane == 0) Pex = 1.0;
     const double Tb = T * Pex;
+    if (light) {
+      const double wgt = q.cand ? q.alpha * Tb : 0.0;
+      lc0 += q.col[0] * wgt;
+      lc1 += q.col[1] * wgt;
+      lc2 += q.col[2] * wgt;
+      lsoft += q.skip ? 0.0 : q.sv;
+      hard += __popc(__ballot_sync(FULL, q.cand));
+      light_pending = true;
+      T = T * __shfl_sync(FULL, P, 31);
+      cur = nxt;
+      continue;
+    }
     const bool tc = q.cand && (Tb * (1.0 - q.alpha) < T_EPS);
     const unsigned tm = __ballot_sync(FULL, tc);
     const int tl = tm ? __ffs(tm) - 1 : 32;
@@ -428,6 +456,12 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
     }
     T = T * __shfl_sync(FULL, P, 31);
     cur = nxt;
+  }
+  if (light_pending) {  // the walk ended inside the light chunks
+    C0 += warp_sum64(lc0);
+    C1 += warp_sum64(lc1);
+    C2 += warp_sum64(lc2);
+    soft += warp_sum64(lsoft);
   }
   r.T = T;
   r.C[0] = C0;
@@ -453,7 +487,7 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
     const size_t pix = (size_t)py * a.width + px;
     const int2 rg = a.ranges[t];
     Pix64 r;
-    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt + ckpt_base(rg.x, t) + p);
+    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt + ckpt_base(rg.x, t) + p, fix_kflag(a)[pix]);
     if (lane == 0) {
       a.image[pix * 3 + 0] = (float)(r.C[0] + a.bg64[0] * r.T);
       a.image[pix * 3 + 1] = (float)(r.C[1] + a.bg64[1] * r.T);
