@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const
       const uint32_t sw = __shfl_sync(FULLM, w, src), sg = __shfl_sync(FULLM, g, src);
       const int sx = __shfl_sync(FULLM, rc.x, src), sy = __shfl_sync(FULLM, rc.y, src);
       if (k < total) {
-        const uint32_t q = k - se;
-        keys[so + q] = ((uint32_t)sy + q / sw) * (uint32_t)tiles_x + (uint32_t)sx + q % sw;
+        const uint32_t q = k - se;  // < 32: q / sw from a float reciprocal is exact
+        const uint32_t row = __float2uint_rz(((float)q + 0.5f) * __frcp_rn((float)sw));
+        keys[so + q] = ((uint32_t)sy + row) * (uint32_t)tiles_x + (uint32_t)sx + (q - row * sw);
         vals[so + q] = sg;
       }
     }
@@ -229,9 +230,20 @@ __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const
     const int4 rc = rect[g];
     const uint32_t o = offset[g];
     const uint32_t w = (uint32_t)(rc.z - rc.x), cnt = __shfl_sync(FULLM, nt, l);
+    // (row, col) of instance j = lane + 32 i advanced incrementally (no division per instance)
+    uint32_t row = (uint32_t)lane / w, col = (uint32_t)lane - row * w;
+    const uint32_t drow = 32u / w, dcol = 32u - drow * w;
+    uint32_t key = ((uint32_t)rc.y + row) * (uint32_t)tiles_x + (uint32_t)rc.x + col;
     for (uint32_t j = lane; j < cnt; j += 32) {
-      keys[o + j] = ((uint32_t)rc.y + j / w) * (uint32_t)tiles_x + (uint32_t)rc.x + j % w;
+      keys[o + j] = key;
       vals[o + j] = (uint32_t)g;
+      col += dcol;
+      row += drow;
+      if (col >= w) {
+        col -= w;
+        row++;
+      }
+      key = ((uint32_t)rc.y + row) * (uint32_t)tiles_x + (uint32_t)rc.x + col;
     }
   }
 }
