@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, co
 }
 
 // ------------------------------------------------------------------ geometry chain
-constexpr int CHAIN_ROWS = 128;
-constexpr int CHAIN_STAGE_FLOATS = 9 * 1024;
+constexpr int CHAIN_ROWS = 64;
+constexpr int CHAIN_STAGE_FLOATS = 9 * 512;
 
 template <bool FUSED>
 __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
