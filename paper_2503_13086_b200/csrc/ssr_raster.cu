@@ -78,78 +78,96 @@ struct FwdState {
   bool term, flag;
 };
 
-// kernels.py:68-95 over slots [j0, jend) of the staged batch (walk index
-// k0 + j).  FRAGILE: the batch holds a near-singular conic (negative staged
-// opacity), so the power > 0 guard band is tested; batches without one (the
-// common case) skip that test entirely.  Returns false once the pixel
-// terminated or was flagged.
-template <bool FRAGILE, bool FULL>
-__device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sM, const float4* sA, const float4* sB, int j0,
-                                         int jend, int k0, float fpx, float fpy, float band, float band_t) {
-  // FULL: a whole 32-slot bucket, constant trip count (no per-slot bound test)
-  const int nj = FULL ? BUCKET : jend - j0;
-#pragma unroll 8
-  for (int jj = 0; jj < nj; jj++) {
-    const int j = j0 + jj;
-    const float4 M = sM[j];
-    const float4 A = sA[j];
-    const float dx = pair_d(fpx, M.x, M.y), dy = pair_d(fpy, M.z, M.w);
-    const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
-    float qpos;
-    const float p2 = pair_power2(dxx, dxy, dyy, A.x, A.y, A.z, qpos);
-    if (p2 < FAR_POWER2) continue;  // soft term S0, nothing else
-    if (FRAGILE && A.w < 0.f) {
-      // only near-singular conics can round to power > 0: flag near that decision
-      if (p2 > 1e-6f * qpos && qpos != 0.f) {
-        q.flag = true;
-        q.nwk = k0 + j;  // flagged: the slot of the ambiguous decision
-        return false;
-      }
-      if (p2 > 0.f) {
-        q.nbig++;  // skipped: no soft term (counted out of the S0 total)
-        continue;
-      }
-    }
-    // staged: A.w = +-100 opacity (sign: fragile), B.w = opacity, so the
-    // soft deviation's y = 100 alpha costs one product; alpha itself
-    // (= opacity * 2^p2, the decisions' operand) only on the large path.
-    // y may differ from fl(alpha * 100) in the last bit: that only moves a
-    // pair between the deviation fit and the exact sigmoid (|diff| < 2e-10).
-    const float e2 = ex2_approx(p2);
-    const float y = __fmul_rn(fabsf(A.w), e2);
-    if (y < SOFT_Y0) {
-      q.sdev = soft_dev_acc(y, q.sdev);
-      continue;
-    }
-    const float4 B = sB[j];
-    float alpha = __fmul_rn(B.w, e2);
-    const bool fa = (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band);
-    alpha = fminf(alpha, ALPHA_CAP_F);
-    q.nbig++;  // (also for a slot flagged here: the fix-up recomputes a flagged pixel)
-    q.sbig += (double)soft_sigmoid_accurate(alpha);
-    // blend without a branch (most large-path lanes blend): a lane below
-    // 1/255 runs it with alpha = 0, i.e. T * 1 and colour + B * 0
-    const bool bl = alpha >= ALPHA_MIN_F;
-    const float ab = bl ? alpha : 0.f;
-    const float test = __fmul_rn(q.T, __fsub_rn(1.f, ab));
-    const bool ft = bl & (fabsf(test - T_EPS_F) < T_EPS_F * band_t);
-    // one exit: an alpha guard band, a transmittance guard band, or termination
-    if (fa | ft | (bl & (test < T_EPS_F))) {
-      if (fa | ft) {
-        q.flag = true;
-        q.nwk = k0 + j;
-      } else {
-        q.term = true;
-        q.nwk = k0 + j + 1;
-      }
+// One walked slot past the far test (kernels.py:68-95): fragile guard,
+// small-alpha soft deviation, or the large path (exact sigmoid, guard bands,
+// blend).  w100 = staged +-100 opacity (sign: fragile).  Returns false once
+// the pixel terminated or was flagged.
+template <bool FRAGILE>
+__device__ __forceinline__ bool fwd_slot(FwdState& q, float p2, float qpos, float w100, const float4* sB, int j,
+                                         int k0, float band, float band_t) {
+  if (FRAGILE && w100 < 0.f) {
+    // only near-singular conics can round to power > 0: flag near that decision
+    if (p2 > 1e-6f * qpos && qpos != 0.f) {
+      q.flag = true;
+      q.nwk = k0 + j;  // flagged: the slot of the ambiguous decision
       return false;
     }
-    const float w = __fmul_rn(ab, q.T);
-    q.c0 = __fmaf_rn(B.x, w, q.c0);
-    q.c1 = __fmaf_rn(B.y, w, q.c1);
-    q.c2 = __fmaf_rn(B.z, w, q.c2);
-    q.hard += bl ? 1 : 0;
-    q.T = test;
+    if (p2 > 0.f) {
+      q.nbig++;  // skipped: no soft term (counted out of the S0 total)
+      return true;
+    }
+  }
+  // y = 100 alpha costs one product; alpha itself (= opacity * 2^p2, the
+  // decisions' operand) only on the large path.  y may differ from
+  // fl(alpha * 100) in the last bit: that only moves a pair between the
+  // deviation fit and the exact sigmoid (|diff| < 2e-10).
+  const float e2 = ex2_approx(p2);
+  const float y = __fmul_rn(fabsf(w100), e2);
+  if (y < SOFT_Y0) {
+    q.sdev = soft_dev_acc(y, q.sdev);
+    return true;
+  }
+  const float4 B = sB[j];
+  float alpha = __fmul_rn(B.w, e2);
+  const bool fa = (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band);
+  alpha = fminf(alpha, ALPHA_CAP_F);
+  q.nbig++;  // (also for a slot flagged here: the fix-up recomputes a flagged pixel)
+  q.sbig += (double)soft_sigmoid_accurate(alpha);
+  // blend without a branch (most large-path lanes blend): a lane below
+  // 1/255 runs it with alpha = 0, i.e. T * 1 and colour + B * 0
+  const bool bl = alpha >= ALPHA_MIN_F;
+  const float ab = bl ? alpha : 0.f;
+  const float test = __fmul_rn(q.T, __fsub_rn(1.f, ab));
+  const bool ft = bl & (fabsf(test - T_EPS_F) < T_EPS_F * band_t);
+  // one exit: an alpha guard band, a transmittance guard band, or termination
+  if (fa | ft | (bl & (test < T_EPS_F))) {
+    if (fa | ft) {
+      q.flag = true;
+      q.nwk = k0 + j;
+    } else {
+      q.term = true;
+      q.nwk = k0 + j + 1;
+    }
+    return false;
+  }
+  const float w = __fmul_rn(ab, q.T);
+  q.c0 = __fmaf_rn(B.x, w, q.c0);
+  q.c1 = __fmaf_rn(B.y, w, q.c1);
+  q.c2 = __fmaf_rn(B.z, w, q.c2);
+  q.hard += bl ? 1 : 0;
+  q.T = test;
+  return true;
+}
+
+// kernels.py:68-95 over slots [j0, jend) of the staged batch (walk index
+// k0 + j), two slots at a time: the staged pair (j, j + 1) holds
+// {x int, x frac}, {y int, y frac}, {a2, b2}, {c2, +-100 opacity} as lane
+// pairs, so the far test of both splats is 7 packed operations; slots that
+// pass it run fwd_slot in walk order.  FRAGILE: the batch holds a
+// near-singular conic (negative staged opacity), so the power > 0 guard band
+// is tested; batches without one (the common case) skip that test entirely.
+// Returns false once the pixel terminated or was flagged.
+template <bool FRAGILE, bool FULL>
+__device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sP, const float4* sB, int j0, int jend, int k0,
+                                         float fpx, float fpy, float band, float band_t) {
+  // FULL: a whole 32-slot bucket, constant trip count (no per-slot bound test)
+  const int nj = FULL ? BUCKET : jend - j0;
+  const float2 px2 = make_float2(fpx, fpx), py2 = make_float2(fpy, fpy);
+#pragma unroll 4
+  for (int jj = 0; jj < nj; jj += 2) {
+    const int j = j0 + jj;  // even: pair j / 2
+    const float4* P = sP + 2 * j;
+    const float4 MX = P[0], MY = P[1], C = P[2], D = P[3];
+    const float2 dx = f2_sub(f2_sub(px2, make_float2(MX.x, MX.y)), make_float2(MX.z, MX.w));
+    const float2 dy = f2_sub(f2_sub(py2, make_float2(MY.x, MY.y)), make_float2(MY.z, MY.w));
+    const float2 dxx = f2_mul(dx, dx), dxy = f2_mul(dx, dy), dyy = f2_mul(dy, dy);
+    const float2 qp = f2_fma(make_float2(D.x, D.y), dyy, f2_mul(make_float2(C.x, C.y), dxx));
+    const float2 p2 = f2_fma(make_float2(C.z, C.w), dxy, qp);
+    // far (power < -25): soft term S0 only, nothing else
+    if (!(p2.x < FAR_POWER2) && !fwd_slot<FRAGILE>(q, p2.x, qp.x, D.z, sB, j, k0, band, band_t)) return false;
+    if ((FULL || jj + 1 < nj) && !(p2.y < FAR_POWER2) &&
+        !fwd_slot<FRAGILE>(q, p2.y, qp.y, D.w, sB, j + 1, k0, band, band_t))
+      return false;
   }
   return true;
 }
@@ -174,9 +192,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const float fpx = (float)lx, fpy = (float)ly;
   const float band = a.band, band_t = a.band_t;
 
-  __shared__ float4 sM[FWD_BATCH];  // staged mean (x int, x frac, y int, y frac)
-  __shared__ float4 sA[FWD_BATCH];  // staged conic a2, b2, c2; opacity
-  __shared__ float4 sB[FWD_BATCH];  // r, g, b
+  // staged splat pairs (fwd_walk): {xi}, {xf}, {yi}, {yf}, {a2}, {b2}, {c2},
+  // {100 opacity, < 0 marks a fragile conic} as lane pairs, 4 float4 per pair
+  __shared__ float4 sP[2 * FWD_BATCH];
+  __shared__ float4 sB[FWD_BATCH];  // r, g, b, opacity
   __shared__ int sMax[8];
 
   FwdState q;
@@ -204,8 +223,15 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         const float4 col = a.color[g];
         const StagedConic sc = stage_conic(co.x, co.y, co.z);
         const StagedMean sm = stage_mean(m.x, m.y, x00, y00);
-        sM[e] = make_float4(sm.xi, sm.xf, sm.yi, sm.yf);
-        sA[e] = make_float4(sc.a2, sc.b2, sc.c2, __fmul_rn(co.w, 100.f));  // < 0 marks a fragile conic
+        float* P = reinterpret_cast<float*>(sP + 2 * (e & ~1)) + (e & 1);
+        P[0] = sm.xi;
+        P[2] = sm.xf;
+        P[4] = sm.yi;
+        P[6] = sm.yf;
+        P[8] = sc.a2;
+        P[10] = sc.b2;
+        P[12] = sc.c2;
+        P[14] = __fmul_rn(co.w, 100.f);  // < 0 marks a fragile conic
         sB[e] = make_float4(col.x, col.y, col.z, fabsf(co.w));
         fragile |= co.w < 0.f;
       }
@@ -223,11 +249,11 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         const int jend = min(j0 + BUCKET, n);
         bool go;
         if (jend - j0 == BUCKET)
-          go = batch_fragile ? fwd_walk<true, true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
-                             : fwd_walk<false, true>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
+          go = batch_fragile ? fwd_walk<true, true>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, true>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
         else
-          go = batch_fragile ? fwd_walk<true, false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t)
-                             : fwd_walk<false, false>(q, sM, sA, sB, j0, jend, k0, fpx, fpy, band, band_t);
+          go = batch_fragile ? fwd_walk<true, false>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, false>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
         if (!go) {
           done = true;
           break;
