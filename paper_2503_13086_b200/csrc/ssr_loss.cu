@@ -61,7 +61,7 @@ constexpr int VSEG = 4;                 // vertical outputs per thread (32 x 8 =
 constexpr int HZS = LT + 1;             // padded row stride of the horizontal results
 
 template <bool U8>
-__global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __restrict__ img,
+__global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* __restrict__ img,
                                                   const Target tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
                                                   double* __restrict__ partials) {
@@ -116,26 +116,36 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
     __syncthreads();
     if (tid < HITEMS) {
       const int r = tid / (LT / HSEG), cs = (tid % (LT / HSEG)) * HSEG;
-      float xv[HSEG + 10], yv[HSEG + 10];
+      float2 xy[HSEG + 10];
 #pragma unroll
-      for (int j = 0; j < HSEG + 10; j++) {
-        xv[j] = sx[r][cs + j];
-        yv[j] = sy[r][cs + j];
+      for (int j = 0; j < HSEG + 10; j++) xy[j] = make_float2(sx[r][cs + j], sy[r][cs + j]);
+      // maps (x, y) and (x^2, y^2) as packed lane pairs (FFMA2, each lane the
+      // scalar FMA chain), then x y: the map's inputs are formed once per input
+      // element, then 11 FMAs per output
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        float2 in[HSEG + 10];
+#pragma unroll
+        for (int j = 0; j < HSEG + 10; j++) in[j] = k == 0 ? xy[j] : f2_mul(xy[j], xy[j]);
+#pragma unroll
+        for (int o = 0; o < HSEG; o++) {
+          float2 v = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int t = 0; t < 11; t++) v = f2_fma(make_float2(wv[t], wv[t]), in[o + t], v);
+          hz[2 * k][r][cs + o] = v.x;
+          hz[2 * k + 1][r][cs + o] = v.y;
+        }
       }
-      // one map at a time: the map's inputs (x, y, x^2, y^2, xy) are formed once
-      // per input element, then 11 FMAs per output
-#pragma unroll
-      for (int k = 0; k < 5; k++) {
+      {
         float in[HSEG + 10];
 #pragma unroll
-        for (int j = 0; j < HSEG + 10; j++)
-          in[j] = k == 0 ? xv[j] : k == 1 ? yv[j] : k == 2 ? xv[j] * xv[j] : k == 3 ? yv[j] * yv[j] : xv[j] * yv[j];
+        for (int j = 0; j < HSEG + 10; j++) in[j] = xy[j].x * xy[j].y;
 #pragma unroll
         for (int o = 0; o < HSEG; o++) {
           float v = 0.f;
 #pragma unroll
           for (int t = 0; t < 11; t++) v = fmaf(wv[t], in[o + t], v);
-          hz[k][r][cs + o] = v;
+          hz[4][r][cs + o] = v;
         }
       }
     }
@@ -144,16 +154,29 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(int W, int H, const float* __r
       const int c = tid % LT, rs = (tid / LT) * VSEG;
       float mom[5][VSEG];
 #pragma unroll
-      for (int k = 0; k < 5; k++) {
+      for (int k = 0; k < 4; k += 2) {  // maps (k, k + 1) as lane pairs
+        float2 col[VSEG + 10];
+#pragma unroll
+        for (int j = 0; j < VSEG + 10; j++) col[j] = make_float2(hz[k][rs + j][c], hz[k + 1][rs + j][c]);
+#pragma unroll
+        for (int o = 0; o < VSEG; o++) {
+          float2 v = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int t = 0; t < 11; t++) v = f2_fma(make_float2(wv[t], wv[t]), col[o + t], v);
+          mom[k][o] = v.x;
+          mom[k + 1][o] = v.y;
+        }
+      }
+      {
         float col[VSEG + 10];
 #pragma unroll
-        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[k][rs + j][c];
+        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[4][rs + j][c];
 #pragma unroll
         for (int o = 0; o < VSEG; o++) {
           float v = 0.f;
 #pragma unroll
-          for (int t = 0; t < 11; t++) v += wv[t] * col[o + t];
-          mom[k][o] = v;
+          for (int t = 0; t < 11; t++) v = fmaf(wv[t], col[o + t], v);
+          mom[4][o] = v;
         }
       }
       float l1f = 0.f, ssf = 0.f;  // <= 4 terms per channel: fp32 partials, fp64 from here on
@@ -316,17 +339,29 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
     __syncthreads();
     if (tid < HITEMS) {
       const int r = tid / (LT / HSEG), cs = (tid % (LT / HSEG)) * HSEG;
+      {  // maps 0 and 1 as lane pairs, then map 2
+        float2 xv[HSEG + 10];
 #pragma unroll
-      for (int k = 0; k < 3; k++) {
+        for (int j = 0; j < HSEG + 10; j++) xv[j] = make_float2(sm[0][r][cs + j], sm[1][r][cs + j]);
+#pragma unroll
+        for (int o = 0; o < HSEG; o++) {
+          float2 v = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int t = 0; t < 11; t++) v = f2_fma(make_float2(wv[t], wv[t]), xv[o + t], v);
+          hz[0][r][cs + o] = v.x;
+          hz[1][r][cs + o] = v.y;
+        }
+      }
+      {
         float xv[HSEG + 10];
 #pragma unroll
-        for (int j = 0; j < HSEG + 10; j++) xv[j] = sm[k][r][cs + j];
+        for (int j = 0; j < HSEG + 10; j++) xv[j] = sm[2][r][cs + j];
 #pragma unroll
         for (int o = 0; o < HSEG; o++) {
           float v = 0.f;
 #pragma unroll
-          for (int t = 0; t < 11; t++) v += wv[t] * xv[o + t];
-          hz[k][r][cs + o] = v;
+          for (int t = 0; t < 11; t++) v = fmaf(wv[t], xv[o + t], v);
+          hz[2][r][cs + o] = v;
         }
       }
     }
@@ -334,17 +369,29 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
     {
       const int c = tid % LT, rs = (tid / LT) * VSEG;
       float bm[3][VSEG];
+      {  // maps 0 and 1 as lane pairs, then map 2
+        float2 col[VSEG + 10];
 #pragma unroll
-      for (int k = 0; k < 3; k++) {
+        for (int j = 0; j < VSEG + 10; j++) col[j] = make_float2(hz[0][rs + j][c], hz[1][rs + j][c]);
+#pragma unroll
+        for (int o = 0; o < VSEG; o++) {
+          float2 v = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int t = 0; t < 11; t++) v = f2_fma(make_float2(wv[t], wv[t]), col[o + t], v);
+          bm[0][o] = v.x;
+          bm[1][o] = v.y;
+        }
+      }
+      {
         float col[VSEG + 10];
 #pragma unroll
-        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[k][rs + j][c];
+        for (int j = 0; j < VSEG + 10; j++) col[j] = hz[2][rs + j][c];
 #pragma unroll
         for (int o = 0; o < VSEG; o++) {
           float v = 0.f;
 #pragma unroll
-          for (int t = 0; t < 11; t++) v += wv[t] * col[o + t];
-          bm[k][o] = v;
+          for (int t = 0; t < 11; t++) v = fmaf(wv[t], col[o + t], v);
+          bm[2][o] = v;
         }
       }
 #pragma unroll
