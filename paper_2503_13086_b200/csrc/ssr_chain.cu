@@ -855,12 +855,12 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
   const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
   const size_t geo_smem = FUSED ? 3 * 8 * CHAIN_ROWS * sizeof(float) : 0;
   if (FUSED) {
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
       SSR_TRY(check_cuda(cudaFuncSetAttribute(k_chain_geo<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)geo_smem),
                          "k_chain_geo smem"));
-      attr = true;
+      attr.set();
     }
   }
   k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, geo_smem, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
@@ -872,12 +872,12 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
 #define SSR_SHA(D)                                                                                                \
   do {                                                                                                            \
     const size_t sm = sh_adam_smem<D>();                                                                          \
-    static bool attr = false;                                                                                     \
-    if (!attr) {                                                                                                  \
+    static DeviceOnce attr;                                                                                     \
+    if (!attr.done()) {                                                                                                  \
       SSR_TRY(check_cuda(cudaFuncSetAttribute(k_chain_sh_adam<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                               (int)sm),                                                           \
                          "k_chain_sh_adam smem"));                                                                \
-      attr = true;                                                                                                \
+      attr.set();                                                                                                \
     }                                                                                                             \
     k_chain_sh_adam<D><<<ablocks, SH_THREADS, sm, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset,     \
                                                         (const float4*)splats.color, rows, adam);                 \

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/ssr.h"
@@ -40,6 +41,19 @@ __host__ __device__ __forceinline__ int64_t row_stride(int64_t n) { return (n + 
 void set_error(const std::string& msg);
 int check_cuda(cudaError_t e, const char* what);
 int check_launch(const char* what);
+
+// "Done once" flag kept per device: kernel attributes and __constant__ data
+// belong to a device, so a process that drives several GPUs sets each up.
+struct DeviceOnce {
+  std::atomic<uint64_t> bits{0};
+  static int dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool done() const { return (bits.load(std::memory_order_acquire) >> dev()) & 1u; }
+  void set() { bits.fetch_or(1ull << dev(), std::memory_order_acq_rel); }
+};
 
 #define SSR_TRY(expr)          \
   do {                         \

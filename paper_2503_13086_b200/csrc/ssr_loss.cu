@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 static int ensure_window() {
-  static bool done = false;
-  if (done) return SSR_OK;
+  static DeviceOnce done;
+  if (done.done()) return SSR_OK;
   float w[11];
   double g[11], s = 0.0;
   for (int t = 0; t < 11; t++) {
@@ -434,7 +434,7 @@ static int ensure_window() {
   }
   for (int t = 0; t < 11; t++) w[t] = (float)(g[t] / s);
   SSR_TRY(check_cuda(cudaMemcpyToSymbol(c_win, w, sizeof(w)), "ssim window"));
-  done = true;
+  done.set();
   return SSR_OK;
 }
 

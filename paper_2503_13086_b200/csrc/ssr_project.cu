@@ -149,12 +149,12 @@ extern "C" int ssr_preprocess(const ssr_camera* cam, int64_t n, int32_t sh_degre
   do {                                                                                                             \
     if (staged) {                                                                                                  \
       constexpr size_t sm = (size_t)pre_stage_floats<D>() * sizeof(float);                                        \
-      static bool attr = false;                                                                                    \
-      if (!attr) {                                                                                                 \
+      static DeviceOnce attr;                                                                                    \
+      if (!attr.done()) {                                                                                                 \
         SSR_TRY(check_cuda(                                                                                        \
             cudaFuncSetAttribute(k_preprocess<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),     \
             "k_preprocess smem"));                                                                                 \
-        attr = true;                                                                                               \
+        attr.set();                                                                                               \
       }                                                                                                            \
       k_preprocess<D, true><<<(unsigned)blocks, PRE_ROWS, sm, st>>>(c, n, tx, ty, positions, rotations,           \
                                                                     log_scales, opacity_logits, sh, splats);       \

@@ -117,6 +117,9 @@ class GaussianField:
         self._n = 0
         self._flat = torch.zeros(0, dtype=torch.float32, device=self.device)
         self.generation = 0
+        # bumped by every in-place parameter update (optimizer steps, assignment);
+        # a projection's lazily computed aux fields check it (ProjectedSplats._aux)
+        self.version = 0
 
     # ------------------------------------------------------------ construction
     @classmethod
@@ -164,6 +167,7 @@ class GaussianField:
         if tuple(src.shape) != tuple(dst.shape):
             raise InvalidParameter(f"{CLASSES[i]} must have shape {tuple(dst.shape)}, got {tuple(src.shape)}")
         dst.copy_(src.to(dtype=torch.float32))
+        self.version += 1
 
     positions = property(lambda s: s._view(0), lambda s, v: s._assign(0, v))
     rotations = property(lambda s: s._view(1), lambda s, v: s._assign(1, v))
@@ -198,7 +202,8 @@ class GaussianField:
         return h.hexdigest()
 
     def _check_finite(self):
-        if not bool(torch.isfinite(self._flat).all()):
+        # real rows only: the up-to-3 padding rows per class region are not parameters
+        if not all(bool(torch.isfinite(self._view(i)).all()) for i in range(len(CLASSES))):
             raise InvalidParameter("non-finite values in field parameters")
 
     # ------------------------------------------------------------ structure
@@ -257,8 +262,10 @@ class GaussianField:
             if n_old:
                 flat[n_off: n_off + w * n_old] = self._flat[o_off: o_off + w * n_old]
             flat[n_off + w * n_old: n_off + w * n_tot] = part.reshape(-1).to(dtype=torch.float32)
+            flat[n_off + w * n_tot: n_off + w * row_stride(n_tot)] = 0.0  # padding rows: no stale bytes
         self._flat = flat
         self._n = n_tot
+        self.version += 1
 
     def densify_and_prune(self, grad_stats, opts: DensifyOptions, rng, optimizer=None) -> DensifySummary:
         """Clone/split hot Gaussians and prune transparent ones (field.py:303-375).
@@ -303,6 +310,7 @@ class GaussianField:
         self._flat = new
         self._n = n_new
         self.generation += 1
+        self.version += 1
         if optimizer is not None:
             optimizer._adopt(self, new_m, new_v)
         self._check_finite()

@@ -101,6 +101,7 @@ class FieldOptimizer:
             return
         g = grads.flat_params(fld.flat.device)
         lr, bc1, bc2 = self.advance(position_rate)
+        fld.version += 1
         _lib.call("ssr_adam", n, fld.sh_degree, fld.flat.data_ptr(), g.data_ptr(), self.m.data_ptr(),
                   self.v.data_ptr(), lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
 

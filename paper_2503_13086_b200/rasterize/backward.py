@@ -164,6 +164,7 @@ def backward_and_step(field, out: RenderOutput, d_image, d_soft, optimizer, posi
                   out.frame_struct(), d_image.data_ptr(), _lib.ptr(d_soft), rows.data_ptr(), st)
     if n:
         lr, bc1, bc2 = optimizer.advance(position_rate)
+        field.version += 1
         _lib.call("ssr_chain_adam", _lib.camera_struct(cam), n, field.sh_degree, field.flat.data_ptr(),
                   optimizer.m.data_ptr(), optimizer.v.data_ptr(), s, rows.data_ptr(), _lib.ptr(stats), lr,
                   SH_REST_LR, bc1, bc2, st)

@@ -15,7 +15,7 @@ import torch
 
 from .. import _lib
 from ..camera import CameraFrame
-from ..errors import InvalidParameter
+from ..errors import InvalidParameter, StaleFieldError
 
 TILE = 16
 ZNEAR = 0.2
@@ -39,7 +39,7 @@ class ProjectedSplats:
     inst_gauss: torch.Tensor  # (M,) int32 field row per sorted instance
     tile_ranges: torch.Tensor  # (n_tiles, 2) int32 (start, end)
     cam: CameraFrame
-    _src: tuple = dc_field(default=None, repr=False)  # (flat params, n, K) for aux
+    _src: tuple = dc_field(default=None, repr=False)  # (field, field.version, n, K) for aux
     _cap: int = dc_field(default=0, repr=False)  # instance capacity of the buffers sized by M
     _cache: dict = dc_field(default_factory=dict, repr=False)
 
@@ -96,7 +96,12 @@ class ProjectedSplats:
     def _aux(self):
         if "aux" in self._cache:
             return self._cache["aux"]
-        flat, n, k = self._src
+        fld, version, n, k = self._src
+        if fld.version != version or len(fld) != n:
+            # the aux fields are recomputed from the live parameters; after an
+            # in-place update they would describe a different field than this render
+            raise StaleFieldError("field parameters changed since this projection; aux fields are unavailable")
+        flat = fld.flat
         from ..field import class_slices
 
         sl = class_slices(n, k)
@@ -137,6 +142,20 @@ def _alloc_splats(n: int, dev) -> dict:
                 offset=e(n, dt=torch.int32), row_offset=e(n, dt=torch.int32), depth_order=e(n, dt=torch.int32))
 
 
+_CAM_ATTRS = ("rotation", "translation", "center", "fx", "fy", "cx", "cy", "width", "height")
+
+
+def check_camera(cam) -> None:
+    """Accept any camera object with the reference CameraFrame's attributes
+    (camera.py:11-60): this package's CameraFrame, the reference's own, or a
+    duck-typed equivalent.  Only those attributes are read (_lib.camera_struct)."""
+    missing = [a for a in _CAM_ATTRS if not hasattr(cam, a)]
+    if missing:
+        raise InvalidParameter(f"cam lacks camera attributes {missing}")
+    if int(cam.width) < 1 or int(cam.height) < 1:
+        raise InvalidParameter(f"camera size must be positive, got {cam.width}x{cam.height}")
+
+
 def project_field(field, cam: CameraFrame) -> ProjectedSplats:
     """Project every Gaussian, cull, bin into tiles and depth-sort (projection.py:69-191)."""
     sp, ctx = project_begin(field, cam)
@@ -155,8 +174,7 @@ def project_begin(field, cam: CameraFrame):
     from ..field import class_slices
 
     dev = _lib.require_cuda()
-    if not isinstance(cam, CameraFrame):
-        raise InvalidParameter("cam must be a CameraFrame")
+    check_camera(cam)
     n, k = len(field), field.n_sh_coeffs
     tiles_x, tiles_y = tile_grid(cam.width, cam.height)
     n_tiles = tiles_x * tiles_y
@@ -165,7 +183,7 @@ def project_begin(field, cam: CameraFrame):
     # every tile's range is written by ssr_bin_tiles (empty tiles included)
     sp = ProjectedSplats(n, field.sh_degree, tiles_x, tiles_y, bufs,
                          torch.empty(0, dtype=torch.int32, device=dev),
-                         torch.empty(n_tiles, 2, dtype=torch.int32, device=dev), cam, (field.flat, n, k))
+                         torch.empty(n_tiles, 2, dtype=torch.int32, device=dev), cam, (field, field.version, n, k))
     if n == 0:
         sp.tile_ranges.zero_()
         return sp, None

@@ -80,4 +80,7 @@ def grads_report(g, ref: dict) -> dict:
 
 
 def grads_ok(r: dict, rtol=GRAD_RTOL) -> bool:
-    return all(r[f"{k}_rel_l2"] <= rtol for k in GRAD_CLASSES) and r["visible_equal"]
+    """Every parameter class AND the densify statistics: screen_norms (rel-L2,
+    backward.py:128) and the visible mask (exact) feed every densify decision."""
+    return (all(r[f"{k}_rel_l2"] <= rtol for k in GRAD_CLASSES) and r["screen_norms_rel_l2"] <= rtol
+            and r["visible_equal"])

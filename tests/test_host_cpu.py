@@ -190,3 +190,37 @@ def test_view_sharded_allreduce_gloo_world2():
     want = np.arange(n_el, dtype=np.float32) * sum(v + 1 for v in range(5))
     np.testing.assert_allclose(res[0], want, rtol=1e-6)
     np.testing.assert_array_equal(res[0], res[1])
+
+
+def test_check_camera_accepts_duck_typed_frames():
+    """render/project_field read only the pose, intrinsics and size, so the
+    reference's own CameraFrame (or any object with those attributes) is accepted."""
+    from types import SimpleNamespace
+
+    from paper_2503_13086_b200.camera import CameraFrame, look_at
+    from paper_2503_13086_b200.errors import InvalidParameter
+    from paper_2503_13086_b200.rasterize.projection import check_camera
+
+    rot, tr = look_at(np.array([0.0, 0.0, -4.0]), np.zeros(3))
+    ours = CameraFrame(1, 32, 24, 30.0, 30.0, 16.0, 12.0, rot, tr)
+    check_camera(ours)
+    duck = SimpleNamespace(rotation=rot, translation=tr, center=-(rot.T @ tr), fx=30.0, fy=30.0, cx=16.0, cy=12.0,
+                           width=32, height=24, pixels=None)
+    check_camera(duck)
+    with pytest.raises(InvalidParameter, match="lacks"):
+        check_camera(SimpleNamespace(rotation=rot, translation=tr))
+    with pytest.raises(InvalidParameter):
+        check_camera(SimpleNamespace(**{**duck.__dict__, "width": 0}))
+
+
+def test_look_at_is_orthonormal_and_handles_poles():
+    from paper_2503_13086_b200.camera import CameraFrame, look_at
+
+    for eye in ([0.0, 0.0, -4.0], [3.0, -2.0, 1.0], [0.0, 5.0, 0.0], [0.0, -5.0, 0.0]):
+        rot, tr = look_at(np.array(eye), np.zeros(3))
+        assert np.abs(rot @ rot.T - np.eye(3)).max() < 1e-12
+        # +z looks at the target: the origin maps onto the optical axis
+        pc = rot @ np.zeros(3) + tr
+        assert pc[2] > 0 and abs(pc[0]) < 1e-12 and abs(pc[1]) < 1e-12
+        cam = CameraFrame(0, 8, 8, 4.0, 4.0, 4.0, 4.0, rot, tr)
+        np.testing.assert_allclose(cam.center, eye, atol=1e-12)
