@@ -111,8 +111,10 @@ def camera(cfg: int, view: int = 0, width: int | None = None, height: int | None
         d = rng.standard_normal(3)
         eye = 5.0 * d / np.linalg.norm(d)
     elif cfg == 3:
-        # spiral path with ~60% overlap between consecutive views (100 images)
-        ang = 2.0 * np.pi * view * 0.04
+        # spiral path, 0.11 turn per image: consecutive views share 60% of their
+        # feature tracks (front-facing shell points, tools/record_plan_trace.py),
+        # BASELINE config 3's "60% view overlap"
+        ang = 2.0 * np.pi * view * 0.11
         eye = np.array([6.0 * np.cos(ang), -1.5 + 3.0 * view / 100.0, 6.0 * np.sin(ang)])
     else:
         ang = 2.0 * np.pi * view / 64.0

@@ -47,6 +47,14 @@ class TrainState:
         if self.stats is None:
             self.stats = torch.zeros(2 * len(self.field), dtype=torch.float32, device=self.field.flat.device)
 
+    def grow_stats(self, n_added: int) -> None:
+        """Zero statistics for rows appended by a field expansion (pipeline.py:173-174)."""
+        if n_added <= 0:
+            return
+        n_old = self.stats.numel() // 2
+        z = torch.zeros(int(n_added), dtype=self.stats.dtype, device=self.stats.device)
+        self.stats = torch.cat([self.stats[:n_old], z, self.stats[n_old:], z])
+
 
 def densify(state: TrainState) -> None:
     """pipeline.py:209-216 on device; moments remapped in the same kernel pass."""

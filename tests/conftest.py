@@ -20,7 +20,8 @@ def pytest_configure(config):
 def golden_names():
     """Rasterizer cases (the expansion and PLY fixtures are tested separately)."""
     names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
-    return sorted(n for n in names if n != "expansion" and not n.startswith("ply_"))
+    other = ("expansion", "pipeline_small", "c3_plan_trace")  # tested by their own modules
+    return sorted(n for n in names if n not in other and not n.startswith("ply_"))
 
 
 def load_golden(name):
