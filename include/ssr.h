@@ -110,16 +110,20 @@ int ssr_project_aux(const ssr_camera* cam, int64_t n, int32_t sh_degree, const f
                     uint8_t* sh_hi, double* radii, void* stream);
 
 /* ---------------------------------------------------------- stage 2 */
-/* Depth pre-sort of the N rows by fp32(depth) with an fp64 tie-fix, then the
- * exclusive scan of splats.tiles in that order into splats.offset (so each
- * row's instances are emitted at depth-ordered positions); *total_dev gets M. */
+/* Hand-written (no library sort or scan).  Depth pre-sort of the N rows: three
+ * stable 8-bit radix passes over a 24-bit monotone key of fp32(depth) with an
+ * fp64 (depth, row) tie-fix -> splats.depth_order; then one launch with two
+ * decoupled-look-back scans of splats.tiles: in depth order into splats.offset
+ * (each row's instances are emitted at depth-ordered positions) and in field-row
+ * order into splats.row_offset.  *total_dev gets M, summed in 64 bits. */
 int ssr_scan_workspace(int64_t n, int64_t* bytes);
 int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int64_t workspace_bytes,
-                   uint32_t* total_dev, void* stream);
+                   uint64_t* total_dev, void* stream);
 
 /* projection.py:165-191: duplicate each visible splat per overlapped tile at
- * its depth-ordered offset, stable radix sort by tile id (ceil(log2 n_tiles)
- * bits) -> (tile, fp64 depth, row) order, searchsorted tile ranges.  Outputs:
+ * its depth-ordered offset, two stable 8-bit radix passes over the tile id
+ * (<= 65536 tiles) -> (tile, fp64 depth, row) order, searchsorted tile ranges.
+ * M must be below 2^30 (SSR_ERR_CAPACITY otherwise).  Outputs:
  *   inst_gauss[M]   field row of each sorted instance
  *   tile_ranges[2*n_tiles]  (start, end) per tile, searchsorted semantics */
 int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes);
@@ -135,7 +139,7 @@ int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tiles_y, ssr_sp
  * *m_out and calls ssr_bin_tiles).  Lets the binning start without a round
  * trip through the host language after the path's one synchronisation. */
 int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y, ssr_splats splats,
-                           const uint32_t* total_dev, int64_t* m_out, uint32_t* inst_gauss, int32_t* tile_ranges,
+                           const uint64_t* total_dev, int64_t* m_out, uint32_t* inst_gauss, int32_t* tile_ranges,
                            void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Floats needed for the checkpoint buffer of a frame with M instances. */

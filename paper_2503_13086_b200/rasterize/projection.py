@@ -194,7 +194,7 @@ def project_begin(field, cam: CameraFrame):
     _lib.call("ssr_preprocess", cstruct, n, field.sh_degree, flat[sl[0][0]:].data_ptr(), flat[sl[1][0]:].data_ptr(),
               flat[sl[2][0]:].data_ptr(), flat[sl[3][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(), s, st)
     ws = torch.empty(_lib.query("ssr_scan_workspace", n), dtype=torch.uint8, device=dev)
-    total = torch.empty(1, dtype=torch.int32, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)
     _lib.call("ssr_scan_tiles", n, s, ws.data_ptr(), ws.numel(), total.data_ptr(), st)
     cap = int(getattr(field, "_m_hint", 0) or 0)
     inst_cap = ws_cap = None
@@ -228,8 +228,8 @@ def project_end(sp: ProjectedSplats, ctx, field=None) -> ProjectedSplats:
             _lib.raise_last("ssr_bin_tiles_capacity", rc)
     if m < 0:
         m = int(total.item())  # host needs M to size the instance buffers
-    if m < 0:
-        raise InvalidParameter("instance count overflow")
+    if m < 0 or m >= 1 << 30:
+        raise InvalidParameter(f"instance count {m} exceeds the 2^30 - 1 limit of the tile sort")
     sp.inst_gauss = torch.empty(m, dtype=torch.int32, device=dev)
     ws = torch.empty(_lib.query("ssr_bin_workspace", m, n_tiles), dtype=torch.uint8, device=dev)
     sp._cap = m
