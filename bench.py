@@ -4,9 +4,17 @@ One step = one training iteration of the hot path per GPU on one view:
 render (preprocess + tile sort + forward) -> fused loss (L1 + 0.2 D-SSIM) ->
 backward (splat-parallel + chain) -> fused Adam (+ densify statistics),
 i.e. pipeline.py:_train_one_iteration on device.  With N GPUs every rank
-trains its own view each step and the 59-float-per-Gaussian gradients are
-summed with one NCCL all-reduce before the identical Adam step (view-sharded
-semi-global batch, weak scaling: value = N * steps / time).
+trains its own view each step and the ranks' gradients are combined before the
+identical Adam step (train.exchange_and_step; weak scaling: value =
+N * steps / time).
+
+Extra blocks on the same JSON line (each its own workload, timed the same way):
+  paper_objective      config 2 under the reference's default LossWeights() (load 0.41)
+  no_splat_parallel    config 2 with the pixel-parallel backward (the paper's No_SPB ablation)
+  semi_global_batch    config 4: 3M Gaussians, a 64-view 1080p batch sharded 64/N per rank,
+                       summed gradients exchanged once per batch (strong scaling)
+  progressive          config 3 seconds per new image (reference plan replayed), both objectives
+  cpu_baseline         the float64 C port of the reference on the host cores
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config C]
 
@@ -43,7 +51,7 @@ def _args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--progressive-events", type=int, default=2,
+    ap.add_argument("--progressive-events", type=int, default=3,
                     help="also time the progressive loop (config 3, seconds per new image) over this many "
                          "events after one warm-up event; 0 skips it (single GPU only)")
     ap.add_argument("--fused", type=int, default=1,
@@ -51,6 +59,12 @@ def _args():
     ap.add_argument("--e2e-target", default="u8", choices=["u8", "f32"],
                     help="e2e upload of each step's target image: 8-bit like the reference's image files "
                          "(io/images.py; read natively by the loss kernels) or float32")
+    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "sharded"],
+                    help="N > 1: how the ranks' gradient sums meet (train.exchange_and_step)")
+    ap.add_argument("--batch-views", type=int, default=64, help="semi_global_batch: views per batch (config 4)")
+    ap.add_argument("--batch-steps", type=int, default=2, help="semi_global_batch: timed batches (0 skips)")
+    ap.add_argument("--extra-steps", type=int, default=10,
+                    help="timed steps of the paper_objective / no_splat_parallel legs (0 skips them)")
     return ap.parse_args()
 
 
@@ -65,6 +79,22 @@ def _workload(cfg):
 def _views(args):
     # spread the ring cameras of config 2 over the circle
     return [v * (64 // max(args.views, 1)) for v in range(args.views)]
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
 class ClockSampler:
@@ -142,54 +172,79 @@ def _oracle_iteration(orc, P, opt, cam, target, weights):
     return br["total"]
 
 
-def _cpu_setup(cfg, views):
-    from oracle import oracle as orc
-    from paper_2503_13086_b200 import scenes
+class _CpuWorkload:
+    """The GPU arm's workload for the C port: same field, same 8 ring views in
+    the same order, targets rendered (untimed, lazily) from the second seed."""
 
-    orc.build()
-    hp = scenes.make_params(cfg, seed=0)
-    P = orc.Params(*(getattr(hp, k).astype(np.float64) for k in (
-        "positions", "rotations", "log_scales", "opacity_logits", "sh")))
-    tp = scenes.make_params(cfg, seed=1)
-    TP = orc.Params(*(getattr(tp, k).astype(np.float64) for k in (
-        "positions", "rotations", "log_scales", "opacity_logits", "sh")))
-    cams = [scenes.camera(cfg, view=v) for v in views[:2]]
-    targets = [orc.render(TP, c)["image"] for c in cams]
-    opt = orc.Optimizer(P, scene_extent=6.6)
-    return orc, P, opt, cams, targets
+    def __init__(self, cfg, views):
+        from oracle import oracle as orc
+        from paper_2503_13086_b200 import scenes
+
+        orc.build()
+        self.orc = orc
+        hp = scenes.make_params(cfg, seed=0)
+        self.P = orc.Params(*(getattr(hp, k).astype(np.float64) for k in (
+            "positions", "rotations", "log_scales", "opacity_logits", "sh")))
+        tp = scenes.make_params(cfg, seed=1)
+        self.TP = orc.Params(*(getattr(tp, k).astype(np.float64) for k in (
+            "positions", "rotations", "log_scales", "opacity_logits", "sh")))
+        self.cams = [scenes.camera(cfg, view=v) for v in views]
+        self.targets = {}
+        self.opt = orc.Optimizer(self.P, scene_extent=6.6)
+        self.w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
+
+    def target(self, i):
+        if i not in self.targets:
+            self.targets[i] = self.orc.render(self.TP, self.cams[i])["image"]
+        return self.targets[i]
+
+    def iteration(self, k):
+        i = k % len(self.cams)
+        t = self.target(i)
+        return _oracle_iteration(self.orc, self.P, self.opt, self.cams[i], t, self.w)
 
 
-def cpu_baseline(cfg, views, budget_s=25.0, min_iters=1, max_iters=3):
-    orc, P, opt, cams, targets = _cpu_setup(cfg, views)
-    orc.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
-    w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
+def cpu_baseline(cfg, views, budget_s=25.0, max_iters=3, single_thread=True):
+    wl = _CpuWorkload(cfg, views)
+    wl.orc.set_threads(_host_cores())
+    wl.target(0)
     n, t0 = 0, time.perf_counter()
-    while n < max_iters and (n < min_iters or time.perf_counter() - t0 < budget_s / 2):
-        _oracle_iteration(orc, P, opt, cams[n % len(cams)], targets[n % len(cams)], w)
+    while n < max_iters and (n < 1 or time.perf_counter() - t0 < budget_s / 2):
+        wl.iteration(n)
         n += 1
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "iters/s", "cores": orc.num_threads(), "kind": "port",
-            "sample": f"{n} full iteration(s) (render+loss+backward+Adam) of {_workload(cfg).split(',')[0]}, "
-                      f"float64 C port of the reference (oracle/), OpenMP"}
+    out = {"value": n / dt, "unit": "iters/s", "cores": wl.orc.num_threads(), "kind": "port",
+           "cpu_model": _cpu_model(), "host_cores": _host_cores(),
+           "sample": f"{n} full iteration(s) (render+loss+backward+Adam) of {_workload(cfg).split(',')[0]} on the "
+                     f"GPU arm's ring views in its order, float64 C port of the reference (oracle/), OpenMP"}
+    if single_thread:
+        # workers=1 (SURVEY 8d): one iteration on one host thread
+        wl.orc.set_threads(1)
+        t1 = time.perf_counter()
+        wl.iteration(n)
+        out["single_thread"] = {"value": 1.0 / (time.perf_counter() - t1), "unit": "iters/s", "cores": 1,
+                                "sample": "1 iteration, same workload, 1 OpenMP thread"}
+        wl.orc.set_threads(_host_cores())
+    return out
 
 
 def run_reference(args):
     rank, world, _ = _dist()
     if rank != 0:
         return
-    views = _views(args)
-    orc, P, opt, cams, targets = _cpu_setup(args.config, views)
+    wl = _CpuWorkload(args.config, _views(args))
     # every host core: torchrun sets OMP_NUM_THREADS=1 for its workers, which
     # would understate the reference arm at N > 1
-    orc.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
-    w = orc.LossWeights(l1=1.0, ssim=0.2, load=0.0)
-    for i in range(args.warmup and 1):  # one warm-up iteration is enough for the C port
-        _oracle_iteration(orc, P, opt, cams[i % 2], targets[i % 2], w)
+    wl.orc.set_threads(_host_cores())
+    for i in range(len(wl.cams)):  # the targets are inputs: rendered before the timed region
+        if i < max(args.steps, 1) + 1:
+            wl.target(i)
+    wl.iteration(0)  # one warm-up iteration is enough for the C port
     t0 = time.perf_counter()
     k = 0
     budget = 150.0
     while k < args.steps:
-        _oracle_iteration(orc, P, opt, cams[k % 2], targets[k % 2], w)
+        wl.iteration(1 + k)
         k += 1
         if time.perf_counter() - t0 > budget:
             break
@@ -199,12 +254,95 @@ def run_reference(args):
             "steps": k, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": dt / k * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config generator, seeded)",
-            "config": {"workload": _workload(args.config), "parallelism": "host threads"},
-            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": orc.num_threads(), "kind": "port",
-                             "sample": f"{k} iteration(s), float64 C port of the reference, "
-                                       f"{orc.num_threads()} OpenMP threads"},
+            "config": {"workload": _workload(args.config), "views": len(wl.cams), "parallelism": "host threads"},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": wl.orc.num_threads(), "kind": "port",
+                             "cpu_model": _cpu_model(),
+                             "sample": f"{k} iteration(s) cycling the GPU arm's {len(wl.cams)} views in its order, "
+                                       f"float64 C port of the reference, {wl.orc.num_threads()} OpenMP threads"},
             "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm helpers
+def _device_loop(fn, steps):
+    """Device ms of `steps` calls of fn(k), CUDA events on the launching stream."""
+    import torch
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(steps):
+        fn(k)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def semi_global_batch(args, rank, world, local):
+    """Config 4: 3M Gaussians, a fixed batch of views sharded over the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_13086_b200 import GaussianField, _lib, scenes
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.rasterize import render
+    from paper_2503_13086_b200.train import SemiGlobalBatch, TrainState, shard_views
+
+    cfg = 4
+    nv = args.batch_views
+    cams = [scenes.camera(cfg, view=v * (64 // max(1, min(nv, 64))) % 64 if nv <= 64 else v) for v in range(nv)]
+    mine = shard_views(list(range(nv)), rank, world)
+    tf = GaussianField.from_host(scenes.make_params(cfg, seed=1))
+    targets = [None] * nv
+    for i in mine:  # 8-bit targets, as the reference's image files (io/images.py)
+        targets[i] = (render(tf, cams[i], for_backward=False).image * 255.0).round().clamp(0, 255).to(torch.uint8)
+    del tf
+    torch.cuda.empty_cache()
+    field = GaussianField.from_host(scenes.make_params(cfg, seed=0))
+    state = TrainState(field=field, optimizer=FieldOptimizer(field, scene_extent=6.6),
+                       weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), scene_extent=6.6)
+    batch = SemiGlobalBatch(state, mode=args.exchange, densify_every=100, densify_fraction=0.05)
+    rates = [1.6e-4] * nv
+    batch.step(cams, targets, rates, rank=rank, world=world)  # warm-up batch
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        ms = _device_loop(lambda k: batch.step(cams, targets, rates, rank=rank, world=world), args.batch_steps)
+    if world > 1:
+        dist.barrier()
+    _lib.enable_timers(True)
+    batch.step(cams, targets, rates, rank=rank, world=world)
+    stage_ms = _lib.timer_ms()
+    _lib.enable_timers(False)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=field.flat.device)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    out = None
+    if rank == 0:
+        P = 0
+        for i in mine[:2]:
+            P += int(render(field, cams[i], for_backward=False).n_walk.sum())
+        P /= max(1, min(2, len(mine)))
+        bwd_ms = stage_ms.get("ssr_backward", 0.0)
+        sm_count = torch.cuda.get_device_properties(field.flat.device).multi_processor_count
+        fp32_peak = sm_count * 128 * 2 * 1965.0e6 / 1e12
+        ach = FLOP_BWD_PER_PAIR * P / (bwd_ms / 1e3) / 1e12 if bwd_ms else None
+        out = {"metric": "semi-global batches/s (64-view batch, config 4)", "value": args.batch_steps / (ms / 1e3),
+               "unit": "batches/s", "views_per_s": nv * args.batch_steps / (ms / 1e3),
+               "ms_per_batch": ms / args.batch_steps, "batches": args.batch_steps, "n_gpus": world,
+               "views_per_batch": nv, "views_per_rank": len(mine), "scaling": "strong", "exchange": args.exchange,
+               "n_gaussians": len(field), "width": cams[0].width, "height": cams[0].height,
+               "densify": "every 100 batch steps: hottest 5% clone/split (train.densify_top_fraction)",
+               "walked_pairs_per_view": P,
+               "roofline": {"bound": "fp32", "kernel": "ssr_backward (per view)", "achieved": ach, "peak": fp32_peak,
+                            "unit": "TFLOP/s", "frac": (ach / fp32_peak) if ach else None},
+               "stage_ms_per_call": {k: round(v, 4) for k, v in stage_ms.items() if not k.endswith("workspace")},
+               "clocks": clk.summary()}
+    del state, batch, field, targets
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -221,7 +359,7 @@ def main():
     from paper_2503_13086_b200.optim import FieldOptimizer
     from paper_2503_13086_b200.rasterize import backward, render
     from paper_2503_13086_b200.rasterize.backward import FieldGrads, backward_and_step
-    from paper_2503_13086_b200.train import TrainState, allreduce_grads
+    from paper_2503_13086_b200.train import TrainState, exchange_and_step
 
     rank, world, local = _dist()
     torch.cuda.set_device(local)
@@ -232,7 +370,7 @@ def main():
     tp = scenes.make_params(cfg, seed=1)
     cams = [scenes.camera(cfg, view=v) for v in views]
     tfield = GaussianField.from_host(tp)
-    targets = [render(tfield, c).image.clone() for c in cams]
+    targets = [render(tfield, c, for_backward=False).image.clone() for c in cams]
     del tfield
     field = GaussianField.from_host(hp)
     state = TrainState(field=field, optimizer=FieldOptimizer(field, scene_extent=6.6),
@@ -241,6 +379,7 @@ def main():
     n = len(field)
 
     grads_buf = [None]
+    layout = ["splat"]
 
     def step(k, target=None, values_out=None):
         cam_i = (k * world + rank) % len(cams)
@@ -250,19 +389,19 @@ def main():
                         values_out=values_out)
         if world > 1:
             # one view per rank: the chain writes every row (accumulate=False), so
-            # the buffer needs no zero fill; the flat buffer is the all-reduce unit
+            # the buffer needs no zero fill; the flat buffer is the exchange unit
             if grads_buf[0] is None:
                 grads_buf[0] = FieldGrads.zeros(n, field.sh_degree, dev)
             grads = grads_buf[0]
-            backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=False)
-            allreduce_grads(grads.flat)
+            backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=False, layout=layout[0])
+            exchange_and_step(state.field, grads, state.optimizer, rate, mode=args.exchange)
             state.stats[:n] += grads.screen_norms
             state.stats[n:] += grads.visible_count
         elif args.fused:
-            backward_and_step(state.field, out, br.d_image, br.d_soft, state.optimizer, rate, stats=state.stats)
+            backward_and_step(state.field, out, br.d_image, br.d_soft, state.optimizer, rate, stats=state.stats,
+                              layout=layout[0])
         else:
-            grads = backward(state.field, out, br.d_image, br.d_soft, stats=state.stats)
-        if world > 1 or not args.fused:
+            grads = backward(state.field, out, br.d_image, br.d_soft, stats=state.stats, layout=layout[0])
             state.optimizer.step(state.field, grads, position_rate=rate)
         state.global_iteration += 1
         return br
@@ -298,16 +437,9 @@ def main():
     prime_and_warm()
     # ---------------- timed region (device time, CUDA events on the launching stream)
     barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        e0.record()
-        for k in range(args.steps):
-            step(args.warmup + k)
-        e1.record()
-        torch.cuda.synchronize()
+        ms = _device_loop(lambda k: step(args.warmup + k), args.steps)
     barrier()
-    ms = e0.elapsed_time(e1)
     # per-ABI-call device times, from a separate (untimed) pass: the event pairs
     # around every call would otherwise perturb the timed region
     _lib.enable_timers(True)
@@ -373,7 +505,7 @@ def main():
             prefetch(k + 1)
         # the loss kernel writes the step's five loss terms (40 bytes) straight
         # into pinned host memory (mapped), so no copy sits in the stream
-        br = step(args.warmup + k, target=dbuf[b], values_out=host_vals[b])
+        step(args.warmup + k, target=dbuf[b], values_out=host_vals[b])
         consumed[b].record(main_stream)
         read_done[b].record(main_stream)
         if k > 0:
@@ -394,16 +526,6 @@ def main():
             analyse(prof, args.steps)
     barrier()
     assert len(losses_seen) == args.steps and all(np.isfinite(losses_seen))
-    if os.environ.get("SSR_E2E_REPEAT"):  # diagnostics: the device-timed loop again, after the e2e loop
-        torch.cuda.synchronize()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        for k in range(args.steps):
-            step(args.warmup + k)
-        g1.record()
-        torch.cuda.synchronize()
-        print(json.dumps({"device_loop_again_its": args.steps / (g0.elapsed_time(g1) / 1e3),
-                          "e2e_its": args.steps / (f0.elapsed_time(f1) / 1e3)}), file=sys.stderr, flush=True)
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
@@ -417,79 +539,118 @@ def main():
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             step(0)
             torch.cuda.synchronize()
-        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"
-                 and ("ssr" in e.name or "cub" in e.name.lower())]
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA" and "ssr" in e.name]
         launches = len(names) * args.steps
     except Exception:
         pass
 
-    if rank != 0:
-        return
+    # ---------------- the same workload under other settings (paper objective, No_SPB ablation)
+    extras = {}
+    if args.extra_steps > 0:
+        for name, weights, lay in (("paper_objective", LossWeights(), "splat"),
+                                   ("no_splat_parallel", state.weights, "pixel")):
+            restore()
+            keep_w = state.weights
+            state.weights, layout[0] = weights, lay
+            for k in range(3):
+                step(k)
+            barrier()
+            ms_x = _device_loop(lambda k: step(args.warmup + k), args.extra_steps)
+            _lib.enable_timers(True)
+            for k in range(3):
+                step(args.warmup + k)
+            st_x = _lib.timer_ms()
+            _lib.enable_timers(False)
+            ms_xt = torch.tensor([ms_x], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms_xt, op=dist.ReduceOp.MAX)
+            extras[name] = {"value": world * args.extra_steps / (float(ms_xt.item()) / 1e3), "unit": "iters/s",
+                            "steps": args.extra_steps, "ms_per_step": float(ms_xt.item()) / args.extra_steps,
+                            "objective": "LossWeights() = (0.47, 0.12, 0.41) (losses.py:24-27)"
+                            if name == "paper_objective" else "L1 + 0.2 D-SSIM",
+                            "backward_layout": lay, "backward_ms": round(st_x.get("ssr_backward", 0.0), 4)}
+            state.weights, layout[0] = keep_w, "splat"
+
     # ---------------- roofline of the dominant kernel
-    P = M = 0
-    for c in cams:
-        o = render(state.field, c)
-        P += int(o.n_walk.sum().item())
-        M += o.splats.n_instances
-    P_mean, M_mean = P / len(cams), M / len(cams)
-    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp32_peak = sm_count * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s (no measured fp32 peak exists)
-    fwd_ms = stage_ms.get("ssr_forward", 0.0)
-    bwd_ms = stage_ms.get("ssr_backward", 0.0)
-    if bwd_ms >= fwd_ms:
-        dom, flops, dms = "ssr_backward (k_backward_splat + k_backward_fixup)", FLOP_BWD_PER_PAIR * P_mean, bwd_ms
-    else:
-        dom, flops, dms = "ssr_forward (k_forward + k_forward_fixup)", FLOP_FWD_PER_PAIR * P_mean, fwd_ms
-    achieved = flops / (dms / 1e3) / 1e12
-    traffic = None
-    try:
-        prof_sum = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof_sum.get(dom.split(" ")[0])
-    except Exception:
-        pass
-    roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic,
-                "peak_source": f"nominal {sm_count} SMs x 128 FMA/clk x 2 x {sm_max:.0f} MHz "
-                               "(MEASURED_PEAKS.json has no fp32 figure)",
-                "work": f"{flops / 1e9:.2f} GFLOP per launch = {FLOP_BWD_PER_PAIR if 'backward' in dom else FLOP_FWD_PER_PAIR:.0f}"
-                        f" flop x {P_mean / 1e6:.1f} M walked pairs"}
-    # HBM roofline of the streaming Adam pass (7 x S bytes per row: p, g, m, v
-    # read; p, m, v written) against the measured copy bandwidth
-    # HBM roofline of the streaming optimizer pass against the measured copy
-    # bandwidth: k_adam moves 7 x S bytes per row (p, g, m, v read; p, m, v
-    # written); the fused chain+Adam 6 x S bytes per row plus the 36-byte
-    # instance rows it merges
-    roofline_hbm = None
-    s_bytes = 4 * (11 + 3 * (field.sh_degree + 1) ** 2)
-    n_rows = len(state.field)
-    if stage_ms.get("ssr_adam"):
-        kname, kms = "ssr_adam (k_adam)", stage_ms["ssr_adam"]
-        kbytes = 7.0 * s_bytes * n_rows
-        work = f"7 x {s_bytes} B x {n_rows:,} rows"
-    elif stage_ms.get("ssr_chain_adam"):
-        kname, kms = "ssr_chain_adam (k_merge_big + k_chain_geo + k_chain_sh, fused Adam)", stage_ms["ssr_chain_adam"]
-        kbytes = 6.0 * s_bytes * n_rows + 36.0 * M_mean
-        work = f"6 x {s_bytes} B x {n_rows:,} rows + 36 B x {M_mean:,.0f} instance rows"
-    else:
-        kms = None
-    if kms:
-        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        ach = kbytes / (kms / 1e3) / 1e9
-        roofline_hbm = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                        "frac": ach / hbm_peak, "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
-                        "work": f"{kbytes / 1e9:.3f} GB per launch = {work}", "traffic": None}
+    roofline = roofline_hbm = None
+    P_mean = M_mean = 0.0
+    if rank == 0:
+        P = M = 0
+        for c in cams:
+            o = render(state.field, c, for_backward=False)
+            P += int(o.n_walk.sum().item())
+            M += o.splats.n_instances
+        P_mean, M_mean = P / len(cams), M / len(cams)
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        peaks = {}
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            roofline_hbm["traffic"] = tr.get("ssr_adam") if "k_adam" in kname else (
-                (tr.get("ssr_chain_sh_fused") or 0) + (tr.get("ssr_chain_geo_fused") or 0) or None)
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
             pass
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        fp32_peak = sm_count * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s (no measured fp32 peak exists)
+        fwd_ms = stage_ms.get("ssr_forward", 0.0)
+        bwd_ms = stage_ms.get("ssr_backward", 0.0)
+        if bwd_ms >= fwd_ms:
+            dom, flops, dms = "ssr_backward (k_backward_splat + k_backward_fixup)", FLOP_BWD_PER_PAIR * P_mean, bwd_ms
+        else:
+            dom, flops, dms = "ssr_forward (k_forward + k_forward_fixup)", FLOP_FWD_PER_PAIR * P_mean, fwd_ms
+        achieved = flops / (dms / 1e3) / 1e12
+        traffic = None
+        try:
+            prof_sum = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = prof_sum.get(dom.split(" ")[0])
+        except Exception:
+            pass
+        roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": traffic,
+                    "peak_source": f"nominal {sm_count} SMs x 128 FMA/clk x 2 x {sm_max:.0f} MHz "
+                                   "(MEASURED_PEAKS.json has no fp32 figure)",
+                    "work": f"{flops / 1e9:.2f} GFLOP per launch = "
+                            f"{FLOP_BWD_PER_PAIR if 'backward' in dom else FLOP_FWD_PER_PAIR:.0f}"
+                            f" flop x {P_mean / 1e6:.1f} M walked pairs"}
+        # HBM roofline of the streaming optimizer pass against the measured copy
+        # bandwidth: k_adam moves 7 x S bytes per row (p, g, m, v read; p, m, v
+        # written); the fused chain+Adam 6 x S bytes per row plus the 36-byte
+        # instance rows it merges
+        s_bytes = 4 * (11 + 3 * (field.sh_degree + 1) ** 2)
+        n_rows = len(state.field)
+        kms = None
+        if stage_ms.get("ssr_adam"):
+            kname, kms = "ssr_adam (k_adam)", stage_ms["ssr_adam"]
+            kbytes = 7.0 * s_bytes * n_rows
+            work = f"7 x {s_bytes} B x {n_rows:,} rows"
+        elif stage_ms.get("ssr_chain_adam"):
+            kname, kms = ("ssr_chain_adam (k_merge_big + k_chain_geo + k_chain_sh, fused Adam)",
+                          stage_ms["ssr_chain_adam"])
+            kbytes = 6.0 * s_bytes * n_rows + 36.0 * M_mean
+            work = f"6 x {s_bytes} B x {n_rows:,} rows + 36 B x {M_mean:,.0f} instance rows"
+        if kms:
+            hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+            ach = kbytes / (kms / 1e3) / 1e9
+            roofline_hbm = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                            "frac": ach / hbm_peak, "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                            "work": f"{kbytes / 1e9:.3f} GB per launch = {work}", "traffic": None}
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+                roofline_hbm["traffic"] = tr.get("ssr_adam") if "k_adam" in kname else (
+                    (tr.get("ssr_chain_sh_fused") or 0) + (tr.get("ssr_chain_geo_fused") or 0) or None)
+            except Exception:
+                pass
+    h2d = int(pinned[0].numel() * pinned[0].element_size())
+    del state, targets, pinned, dbuf
+    grads_buf[0] = None
+    torch.cuda.empty_cache()
+
+    # ---------------- config 4: the semi-global view batch (every rank takes part)
+    batch_block = None
+    if args.batch_steps > 0:
+        try:
+            batch_block = semi_global_batch(args, rank, world, local)
+        except Exception as ex:  # pragma: no cover
+            batch_block = {"error": f"{type(ex).__name__}: {ex}"}
+    if rank != 0:
+        return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -499,33 +660,35 @@ def main():
     # ---------------- seconds per new image (BASELINE metric, second half): config 3
     progressive = None
     if world == 1 and args.progressive_events > 0:
-        try:
-            import contextlib
-            import io
+        import contextlib
+        import io
 
-            sys.path.insert(0, os.path.join(ROOT, "tools"))
-            import progressive as prog
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import progressive as prog
 
-            del state, targets
-            torch.cuda.empty_cache()
-            with contextlib.redirect_stdout(io.StringIO()):
-                summ = prog.main(["--events", str(args.progressive_events), "--warmup-events", "1"])
-            progressive = {"metric": "seconds per new image", "value": summ["value"], "unit": "s/image",
-                           "higher_is_better": False, "events": summ["events"],
-                           "ms_per_iteration": summ["ms_per_iteration"], "field": summ["field_final"],
-                           "config": "config 3: 1297x840, +20k Gaussians per image, 200 iterations per image "
-                                     "(Local & Semi-Global plan stand-in), expansion + 2 PSNR renders included, "
-                                     "wall clock"}
-        except Exception as ex:  # pragma: no cover
-            progressive = {"error": str(ex)}
-    h2d = int(pinned[0].numel() * pinned[0].element_size())
+        progressive = {}
+        for name, extra in (("bench_objective", []), ("paper_objective", ["--paper-weights"])):
+            try:
+                torch.cuda.empty_cache()
+                with contextlib.redirect_stdout(io.StringIO()):
+                    summ = prog.main(["--events", str(args.progressive_events), "--warmup-events", "1"] + extra)
+                progressive[name] = {
+                    "metric": "seconds per new image", "value": summ["value"], "unit": "s/image",
+                    "higher_is_better": False, "worst": summ["worst"], "events": summ["events"],
+                    "field_final": summ["field_final"], "objective": summ["objective"],
+                    "value_with_reference_scheduler": summ["value_with_reference_scheduler"],
+                    "config": "config 3: 1297x840, +20k Gaussians per image, T_I = 200, reference build_plan / "
+                              "lr_blended replayed, expansion + 2 render-only PSNRs included, wall clock"}
+            except Exception as ex:  # pragma: no cover
+                progressive[name] = {"error": f"{type(ex).__name__}: {ex}"}
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE config generator, seeded; targets = "
                                                       "renders of a second seed's field)",
         "config": {"workload": _workload(cfg), "n_gaussians": n, "width": cams[0].width, "height": cams[0].height,
-                   "views": len(cams), "parallelism": f"view-sharded dp{world}" if world > 1 else "single GPU",
+                   "views": len(cams), "parallelism": f"view-sharded dp{world} ({args.exchange})" if world > 1
+                   else "single GPU",
                    "l2": "inputs larger than L2 (field + Adam moments 708 MB, per-step working set > 1 GB)",
                    "walked_pairs_per_view": P_mean},
         "roofline": roofline,
@@ -535,6 +698,8 @@ def main():
                 "target": f"{args.e2e_target} image uploaded every step (copy stream, overlapped); loss terms "
                           "written by the loss kernel into pinned host memory"},
         "gpu_launches": launches,
+        **extras,
+        "semi_global_batch": batch_block,
         "progressive": progressive,
         "clocks": clk.summary(),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if not k.endswith("workspace")},

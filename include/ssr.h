@@ -195,6 +195,14 @@ int ssr_chain_adam(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* p
 int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, float* m, float* v,
              const double* lr, double lr_sh_rest, const double* bc1, const double* bc2, void* stream);
 
+/* ssr_adam restricted to the flat elements [lo, hi) of the same class-major
+ * buffers: the owner's share of a sharded (reduce-scatter -> Adam -> all-gather)
+ * view-batch step.  grads[e - grads_offset] is element e's gradient,
+ * so a rank passes just its reduced chunk (grads_offset = lo). */
+int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const float* grads, int64_t grads_offset,
+                   float* m, float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest,
+                   const double* bc1, const double* bc2, void* stream);
+
 /* field.py:303-375: per-row flags (bit0 keep, bit1 clone, bit2 split) and
  * counts[3] = (n_clone, n_split, n_prune) in device memory. stats = the
  * already averaged grad_accum / max(count, 1) (pipeline.py:209-210). */

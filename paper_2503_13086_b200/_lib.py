@@ -68,6 +68,9 @@ _SIGS = {
                        ctypes.POINTER(c_double), c_void_p],
     "ssr_adam": [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_double), c_double,
                  ctypes.POINTER(c_double), ctypes.POINTER(c_double), c_void_p],
+    "ssr_adam_range": [c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64,
+                       ctypes.POINTER(c_double), c_double, ctypes.POINTER(c_double), ctypes.POINTER(c_double),
+                       c_void_p],
     "ssr_densify_masks": [c_int64, c_void_p, c_int32, c_void_p, c_double, c_double, c_double, c_void_p,
                           c_void_p, c_void_p],
     "ssr_densify_workspace": [c_int64, ctypes.POINTER(c_int64)],

@@ -15,6 +15,7 @@ namespace ssr {
 // uniform learning rate and bias correction (no per-element class lookup).
 struct AdamRegion {
   int64_t start, count;  // element range in the flat buffer
+  int64_t phase0;        // start of the class region (sh coefficient index = (e - phase0) % K)
   int64_t block0;        // first block of this region
   float lr, lr_rest;     // sh region: lr = DC rate, lr_rest = rest rate
   float inv_bc1, inv_bc2;
@@ -32,10 +33,13 @@ __device__ __forceinline__ float adam_one(float p, float g, float& m, float& v, 
   return adam_update(p, g, m, v, lr, ib1, ib2);
 }
 
+// g is indexed by (e - goff): a rank of a sharded step holds only its chunk
+// of the reduced gradients (ssr_adam_range).
 template <int K>
 __global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __restrict__ p,
-                                                       const float* __restrict__ g, float* __restrict__ m,
-                                                       float* __restrict__ v) {
+                                                       const float* __restrict__ g_base, int64_t goff,
+                                                       float* __restrict__ m, float* __restrict__ v) {
+  const float* __restrict__ g = g_base - goff;
   const int64_t bid = blockIdx.x;
   int ri = 0;
 #pragma unroll
@@ -44,7 +48,7 @@ __global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __r
   const AdamRegion R = plan.r[ri];
   const int64_t e0 = R.start + (bid - R.block0) * ADAM_PER_BLOCK;
   const int64_t e_end = R.start + R.count;
-  const bool vec = ((R.start & 3) == 0);
+  const bool vec = ((R.start & 3) == 0) && ((goff & 3) == 0);
   if (vec && e0 + ADAM_PER_BLOCK <= e_end) {
 #pragma unroll
     for (int u = 0; u < ADAM_PER_THREAD / 4; u++) {
@@ -55,7 +59,7 @@ __global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __r
       float4 vv = *reinterpret_cast<float4*>(v + e);
       float lr0 = R.lr, lr1 = R.lr, lr2 = R.lr, lr3 = R.lr;
       if (R.is_sh) {
-        const int64_t j = e - R.start;
+        const int64_t j = e - R.phase0;
         lr0 = ((j + 0) % K) == 0 ? R.lr : R.lr_rest;
         lr1 = ((j + 1) % K) == 0 ? R.lr : R.lr_rest;
         lr2 = ((j + 2) % K) == 0 ? R.lr : R.lr_rest;
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __r
     for (int u = 0; u < ADAM_PER_THREAD; u++) {
       const int64_t e = e0 + (int64_t)u * ADAM_THREADS + threadIdx.x;
       if (e >= e_end) break;
-      const float lr = (R.is_sh && ((e - R.start) % K) != 0) ? R.lr_rest : R.lr;
+      const float lr = (R.is_sh && ((e - R.phase0) % K) != 0) ? R.lr_rest : R.lr;
       float mm = m[e], vv = v[e];
       p[e] = adam_one(p[e], g[e], mm, vv, lr, R.inv_bc1, R.inv_bc2);
       m[e] = mm;
@@ -222,13 +226,11 @@ static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 
 using namespace ssr;
 
-extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, float* m, float* v,
-                        const double* lr, double lr_sh_rest, const double* bc1, const double* bc2, void* stream) {
-  if (n < 0 || sh_degree < 0 || sh_degree > 3 || !lr || !bc1 || !bc2) {
-    set_error("ssr_adam: invalid argument");
-    return SSR_ERR_INVALID;
-  }
-  if (n == 0) return SSR_OK;
+// Adam over the flat elements [lo, hi) of the class-major buffers (padding
+// rows excluded); grads[e - goff] is the gradient of element e.
+static int launch_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, int64_t goff, float* m,
+                       float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest, const double* bc1,
+                       const double* bc2, cudaStream_t st) {
   const int K = (sh_degree + 1) * (sh_degree + 1);
   const int64_t widths[5] = {3, 4, 3, 1, 3 * (int64_t)K};
   AdamPlan plan;
@@ -236,8 +238,12 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
   const int64_t ns = row_stride(n);
   for (int c = 0; c < 5; c++) {
     AdamRegion& R = plan.r[c];
-    R.start = start;
-    R.count = widths[c] * n;
+    const int64_t a = start > lo ? start : lo;
+    const int64_t b0 = start + widths[c] * n;
+    const int64_t b = b0 < hi ? b0 : hi;
+    R.start = a;
+    R.count = b > a ? b - a : 0;
+    R.phase0 = start;
     R.block0 = blocks;
     R.lr = (float)lr[c];
     R.lr_rest = (float)lr_sh_rest;
@@ -247,14 +253,38 @@ extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float
     start += widths[c] * ns;
     blocks += (R.count + ADAM_PER_BLOCK - 1) / ADAM_PER_BLOCK;
   }
-  cudaStream_t st = (cudaStream_t)stream;
+  if (blocks == 0) return SSR_OK;
   switch (K) {
-    case 1: k_adam<1><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
-    case 4: k_adam<4><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
-    case 9: k_adam<9><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
-    default: k_adam<16><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, m, v); break;
+    case 1: k_adam<1><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
+    case 4: k_adam<4><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
+    case 9: k_adam<9><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
+    default: k_adam<16><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
   }
   return check_launch("k_adam");
+}
+
+
+extern "C" int ssr_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, float* m, float* v,
+                        const double* lr, double lr_sh_rest, const double* bc1, const double* bc2, void* stream) {
+  if (n < 0 || sh_degree < 0 || sh_degree > 3 || !lr || !bc1 || !bc2) {
+    set_error("ssr_adam: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  if (n == 0) return SSR_OK;
+  return launch_adam(n, sh_degree, params, grads, 0, m, v, 0, INT64_MAX, lr, lr_sh_rest, bc1, bc2,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const float* grads, int64_t grads_offset,
+                              float* m, float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest,
+                              const double* bc1, const double* bc2, void* stream) {
+  if (n < 0 || sh_degree < 0 || sh_degree > 3 || !lr || !bc1 || !bc2 || lo < 0 || hi < lo || grads_offset > lo) {
+    set_error("ssr_adam_range: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  if (n == 0 || hi == lo) return SSR_OK;
+  return launch_adam(n, sh_degree, params, grads, grads_offset, m, v, lo, hi, lr, lr_sh_rest, bc1, bc2,
+                     (cudaStream_t)stream);
 }
 
 extern "C" int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degree, const float* stats,

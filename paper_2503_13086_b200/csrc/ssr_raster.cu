@@ -175,6 +175,9 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sP, const fl
 // Splats staged per batch: two per thread (half the barriers of one per thread).
 constexpr int FWD_BATCH = 2 * TILE_PX;
 
+// CK = false: render-only (view_psnr, pipeline.py:180-182): no bucket
+// checkpoints are written (the backward's seeds, ~16 B per live pixel-bucket).
+template <bool CK>
 __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   q.nbig = 0;
   q.term = q.flag = false;
   bool done = !inside;
-  float4* ck = a.ckpt + ckpt_base(s0, t) + pidx;
+  float4* ck = CK ? a.ckpt + ckpt_base(s0, t) + pidx : nullptr;
 
   for (int base = s0; base < s1; base += FWD_BATCH) {
     if (__syncthreads_count(done) == TILE_PX) break;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
       const int k0 = base - s0;
       for (int j0 = 0; j0 < n; j0 += BUCKET) {
         if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
-          ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
+          if (CK) ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
           q.sbig += (double)q.sdev;
           q.sdev = 0.f;
         }
@@ -513,7 +516,8 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
     const size_t pix = (size_t)py * a.width + px;
     const int2 rg = a.ranges[t];
     Pix64 r;
-    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt + ckpt_base(rg.x, t) + p, fix_kflag(a)[pix]);
+    walk_pixel64(a, rg.x, rg.y, (double)px, (double)py, r, a.ckpt ? a.ckpt + ckpt_base(rg.x, t) + p : nullptr,
+                 fix_kflag(a)[pix]);
     if (lane == 0) {
       a.image[pix * 3 + 0] = (float)(r.C[0] + a.bg64[0] * r.T);
       a.image[pix * 3 + 1] = (float)(r.C[1] + a.bg64[1] * r.T);
@@ -1161,7 +1165,11 @@ extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_ga
   }
   if (cudaMemsetAsync(frame.fix_list, 0, FIX_HEAD * sizeof(int32_t), st) != cudaSuccess)
     return check_launch("fix_list reset");
-  k_forward<<<n_tiles, TILE_PX, 0, st>>>(a);
+  // frame.ckpt == NULL: render-only (no backward state beyond the per-pixel outputs)
+  if (frame.ckpt)
+    k_forward<true><<<n_tiles, TILE_PX, 0, st>>>(a);
+  else
+    k_forward<false><<<n_tiles, TILE_PX, 0, st>>>(a);
   SSR_TRY(check_launch("k_forward"));
   k_forward_fixup<<<num_sms() * 4, 256, 0, st>>>(a);
   return check_launch("k_forward_fixup");
@@ -1177,6 +1185,10 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     return SSR_ERR_INVALID;
   }
   if (m == 0) return SSR_OK;
+  if (!frame.ckpt) {
+    set_error("ssr_backward: the frame was rendered without checkpoints (render-only)");
+    return SSR_ERR_INVALID;
+  }
   RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f, 0.f);
   if (layout == 0)
     k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);

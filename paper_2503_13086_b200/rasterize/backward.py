@@ -103,6 +103,8 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
     """
     if out.generation != field.generation:
         raise StaleFieldError(f"render saw generation {out.generation}, field is at {field.generation}")
+    if out.ckpt is None or (out.ckpt.numel() == 0 and out.splats.n_instances > 0):
+        raise InvalidParameter("this RenderOutput came from render(for_backward=False) and cannot be differentiated")
     if layout not in LAYOUTS:
         raise ValueError(f"unknown backward layout {layout!r}")
     cam, sp = out.cam, out.splats
@@ -146,6 +148,8 @@ def backward_and_step(field, out: RenderOutput, d_image, d_soft, optimizer, posi
 
     if out.generation != field.generation:
         raise StaleFieldError(f"render saw generation {out.generation}, field is at {field.generation}")
+    if out.ckpt is None or (out.ckpt.numel() == 0 and out.splats.n_instances > 0):
+        raise InvalidParameter("this RenderOutput came from render(for_backward=False) and cannot be differentiated")
     if layout not in LAYOUTS:
         raise ValueError(f"unknown backward layout {layout!r}")
     optimizer.check(field)

@@ -58,8 +58,13 @@ class RenderOutput:
 
 
 def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: float = None,
-           band_t: float = None) -> RenderOutput:
-    """Render the field from ``cam`` over a constant background colour."""
+           band_t: float = None, *, for_backward: bool = True) -> RenderOutput:
+    """Render the field from ``cam`` over a constant background colour.
+
+    ``for_backward=False`` is the render-only path (view_psnr, pipeline.py:180-182):
+    identical outputs, but the bucket checkpoints the backward seeds from are not
+    written (~16 B per live pixel-bucket, ~320 MB at 1M Gaussians / 1080p), so the
+    result cannot be passed to ``backward``."""
     if workers < 1:
         raise InvalidParameter(f"workers must be >= 1, got {workers}")
     band = GUARD_BAND if band is None else float(band)
@@ -81,7 +86,8 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
     out = RenderOutput(
         image=image, t_final=t_final, n_walk=n_walk, terminated=terminated, hard_count=hard, soft_count=soft,
         splats=splats, cam=cam, bg=bg, generation=field.generation, workers=workers, flagged=flagged,
-        tile_info=tile_info, ckpt=e(int(_lib.load().ssr_ckpt_floats(max(m, splats._cap), n_tiles))),
+        tile_info=tile_info,
+        ckpt=e(int(_lib.load().ssr_ckpt_floats(max(m, splats._cap), n_tiles)) if for_backward else 0),
         fix_list=fix_list,
     )
     _lib.call("ssr_forward", m, splats.struct(), splats.inst_gauss.data_ptr() if m else None,

@@ -20,6 +20,7 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 import torch
 
+from . import _lib
 from .field import DensifyOptions, GaussianField
 from .losses import LossBreakdown, LossWeights, total_loss
 from .optim import FieldOptimizer
@@ -107,33 +108,151 @@ def allreduce_grads(flat: torch.Tensor, group=None) -> torch.Tensor:
     return flat
 
 
+def shard_layout(param_floats: int, world: int):
+    """(chunk, main) of a sharded step: the first ``main = world * chunk``
+    floats of the flat parameter buffer are split into equal, 16-byte aligned
+    chunks (rank r owns [r * chunk, (r + 1) * chunk)); the short tail
+    [main, param_floats) is reduced and stepped on every rank."""
+    chunk = (param_floats // (4 * world)) * 4
+    return chunk, world * chunk
+
+
+def exchange_and_step(field, grads, optimizer, position_rate: float, mode: str = "allreduce", group=None,
+                      adam_range=None):
+    """Combine the ranks' gradient sums and apply the identical Adam step.
+
+    ``mode="allreduce"``: one all-reduce of the whole 61-float-per-row buffer,
+    then every replica runs the full Adam.  ``mode="sharded"``: reduce-scatter
+    of the parameter gradients, each rank runs Adam on its own 1/world chunk
+    (ssr_adam_range), an all-gather of the updated parameters, plus one small
+    all-reduce of the tail and the densify statistics.  Same bytes on the wire
+    as the all-reduce, 1/world of the Adam traffic per rank; rank r's moments
+    are current only inside its chunk (``gather_moments`` before a densify).
+
+    ``adam_range(lo, hi, g, goff)`` overrides the CUDA Adam (host-logic tests).
+    """
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if world == 1 or mode == "allreduce":
+        allreduce_grads(grads.flat, group)
+        if adam_range is None:
+            optimizer.step(field, grads, position_rate=position_rate)
+        else:
+            adam_range(0, field.flat.numel(), grads.flat, 0)
+        return
+    if mode != "sharded":
+        raise ValueError(f"unknown exchange mode {mode!r}")
+    rank = dist.get_rank(group)
+    p_floats = field.flat.numel()
+    chunk, main = shard_layout(p_floats, world)
+    g = grads.flat
+    mine = torch.empty(chunk, dtype=g.dtype, device=g.device)
+    dist.reduce_scatter_tensor(mine, g[:main], group=group)
+    dist.all_reduce(g[main:], group=group)  # parameter tail + screen_norms + visible
+    lo = rank * chunk
+    if adam_range is None:
+        optimizer.check(field)
+        lr, bc1, bc2 = optimizer.advance(position_rate)
+        from .optim import SH_REST_LR
+
+        n, deg = len(field), field.sh_degree
+        field.version += 1
+        for a, b, gt, goff in ((lo, lo + chunk, mine, lo), (main, p_floats, g, 0)):
+            _lib.call("ssr_adam_range", n, deg, field.flat.data_ptr(), gt.data_ptr(), goff, optimizer.m.data_ptr(),
+                      optimizer.v.data_ptr(), a, b, lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
+    else:
+        adam_range(lo, lo + chunk, mine, lo)
+        adam_range(main, p_floats, g, 0)
+    src = field.flat[lo:lo + chunk]
+    if dist.get_backend(group) != "nccl":
+        src = src.clone()  # in-place all-gather is an NCCL feature
+    dist.all_gather_into_tensor(field.flat[:main], src, group=group)
+
+
+def gather_moments(field, optimizer, group=None):
+    """Make every rank's Adam moments complete after sharded steps (before a
+    densify remaps rows across chunk boundaries)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    chunk, main = shard_layout(field.flat.numel(), world)
+    for buf in (optimizer.m, optimizer.v):
+        src = buf[rank * chunk:(rank + 1) * chunk]
+        if dist.get_backend(group) != "nccl":
+            src = src.clone()
+        dist.all_gather_into_tensor(buf[:main], src, group=group)
+
+
+def densify_top_fraction(state: TrainState, fraction: float) -> None:
+    """Config-4 rule (BASELINE: "densify/prune of 5% per 100 iterations"):
+    the clone/split threshold is the (1 - fraction) quantile of the averaged
+    screen-gradient statistic over rows seen at least once, so the hottest
+    ``fraction`` of the field densifies; prune and size rules are the
+    reference's (field.py:321-327, where the threshold is a fixed 2e-4)."""
+    n = len(state.field)
+    accum, count = state.stats[:n], state.stats[n:]
+    grad_stats = accum / torch.clamp(count, min=1.0)
+    seen = grad_stats[count > 0]
+    thr = float(torch.quantile(seen.double(), 1.0 - fraction)) if seen.numel() else float("inf")
+    opts = DensifyOptions(**{**state.densify.__dict__, "scene_extent": state.scene_extent, "grad_threshold": thr})
+    state.field.densify_and_prune(grad_stats, opts, state.rng, optimizer=state.optimizer)
+    state.stats = torch.zeros(2 * len(state.field), dtype=torch.float32, device=state.field.flat.device)
+
+
 class SemiGlobalBatch:
     """View-sharded multi-view step: sum_v grad(view v) at fixed parameters.
 
     Batch rule (documented deviation): gradients of the batch's
     views are summed; the position rate is the mean of the per-view rates.
+    Each rank renders and differentiates its contiguous shard of the views into
+    one flat buffer (``backward(accumulate=True)``), the buffers are combined by
+    ``exchange_and_step`` (all-reduce, or reduce-scatter -> sharded Adam ->
+    all-gather), and ``densify_every`` batch steps the field densifies, either
+    by the reference's fixed threshold or, with ``densify_fraction`` set, by the
+    config-4 top-fraction rule.
     """
 
-    def __init__(self, state: TrainState, group=None):
+    def __init__(self, state: TrainState, group=None, mode: str = "allreduce", densify_every: int = 0,
+                 densify_fraction: float | None = None):
         self.state = state
         self.group = group
+        self.mode = mode
+        self.densify_every = int(densify_every)
+        self.densify_fraction = densify_fraction
+        self._grads = None
+
+    def _buffer(self):
+        f = self.state.field
+        if self._grads is None or self._grads._n != len(f) or self._grads.flat.device != f.flat.device:
+            self._grads = FieldGrads.zeros(len(f), f.sh_degree, f.flat.device)
+        else:
+            self._grads.flat.zero_()
+        return self._grads
 
     def step(self, cams, targets, position_rates, rank: int = 0, world: int = 1, bg=(0.0, 0.0, 0.0)):
         st = self.state
         f = st.field
         idx = shard_views(list(range(len(cams))), rank, world)
-        grads = FieldGrads.zeros(len(f), f.sh_degree, f.flat.device)
+        grads = self._buffer()
         losses = []
         for i in idx:
             out = render(f, cams[i], bg=bg)
             br = total_loss(out.image, targets[i], out, st.weights)
             backward(f, out, br.d_image, br.d_soft, layout=st.layout, grads=grads, accumulate=True)
             losses.append(br)
-        allreduce_grads(grads.flat, self.group)
+        rate = float(np.mean(position_rates)) if len(position_rates) else 0.0
+        exchange_and_step(f, grads, st.optimizer, rate, mode=self.mode, group=self.group)
         n = len(f)
         st.stats[:n] += grads.screen_norms
         st.stats[n:] += grads.visible_count
-        rate = float(np.mean(position_rates)) if len(position_rates) else 0.0
-        st.optimizer.step(f, grads, position_rate=rate)
         st.global_iteration += 1
+        if self.densify_every and st.global_iteration % self.densify_every == 0:
+            if self.mode == "sharded" and world > 1:
+                gather_moments(f, st.optimizer, self.group)
+            if self.densify_fraction:
+                densify_top_fraction(st, self.densify_fraction)
+            else:
+                densify(st)
         return grads, losses

@@ -138,3 +138,36 @@ def test_densify_moment_remap_matches_reference_sync(seed):
     s2 = f2.densify_and_prune(stats, opts, np.random.default_rng(99))
     assert (s2.cloned, s2.split, s2.pruned) == (s.cloned, s.split, s.pruned)
     assert torch.equal(f.flat, f2.flat)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_adam_range_chunks_equal_full_adam(world):
+    """ssr_adam_range over a sharded step's chunks (each with only its chunk of
+    the gradients, grads_offset = lo) + the tail == one full ssr_adam."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, _lib, scenes
+    from paper_2503_13086_b200.optim import SH_REST_LR, FieldOptimizer
+    from paper_2503_13086_b200.rasterize import FieldGrads
+    from paper_2503_13086_b200.train import shard_layout
+
+    hp = scenes.make_params(1, seed=31, n=10007)
+    fa, fb = GaussianField.from_host(hp), GaussianField.from_host(hp)
+    oa, ob = FieldOptimizer(fa, 2.0), FieldOptimizer(fb, 2.0)
+    gen = torch.Generator("cuda").manual_seed(world)
+    for o in (oa, ob):
+        o.m.copy_(torch.randn(o.m.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(1)))
+        o.v.copy_(torch.rand(o.v.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(2)))
+    g = FieldGrads.zeros(len(fa), fa.sh_degree, fa.flat.device)
+    g.flat.copy_(torch.randn(g.flat.shape, device="cuda", generator=gen))
+    oa.step(fa, g, position_rate=1e-4)
+    lr, bc1, bc2 = ob.advance(1e-4)
+    p = fb.flat.numel()
+    chunk, main = shard_layout(p, world)
+    pieces = [(r * chunk, (r + 1) * chunk, g.flat[r * chunk:(r + 1) * chunk].clone(), r * chunk) for r in range(world)]
+    pieces.append((main, p, g.flat, 0))
+    for lo, hi, gt, goff in pieces:
+        _lib.call("ssr_adam_range", len(fb), fb.sh_degree, fb.flat.data_ptr(), gt.data_ptr(), goff, ob.m.data_ptr(),
+                  ob.v.data_ptr(), lo, hi, lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(fa.flat, fb.flat) and torch.equal(oa.m, ob.m) and torch.equal(oa.v, ob.v)

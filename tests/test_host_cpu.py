@@ -224,3 +224,100 @@ def test_look_at_is_orthonormal_and_handles_poles():
         assert pc[2] > 0 and abs(pc[0]) < 1e-12 and abs(pc[1]) < 1e-12
         cam = CameraFrame(0, 8, 8, 4.0, 4.0, 4.0, 4.0, rot, tr)
         np.testing.assert_allclose(cam.center, eye, atol=1e-12)
+
+
+# ---------------------------------------------------------------- sharded batch step over gloo
+class _FlatField:
+    def __init__(self, flat, n, deg):
+        self.flat, self._n, self.sh_degree, self.version = flat, n, deg, 0
+
+    def __len__(self):
+        return self._n
+
+
+def _cpu_adam(field, opt, rate, steps):
+    """optim.py AdamBuffer.apply restated over the flat class-major layout:
+    returns adam_range(lo, hi, g, goff) updating field.flat / opt.m / opt.v."""
+    from paper_2503_13086_b200.field import class_slices
+    from paper_2503_13086_b200.optim import (BETA1, BETA2, EPS, OPACITY_LR, ROTATION_LR, SCALE_LR, SH_DC_LR,
+                                             SH_REST_LR)
+
+    n, k = len(field), (field.sh_degree + 1) ** 2
+    lrs = (rate * opt.scene_extent, ROTATION_LR, SCALE_LR, OPACITY_LR, SH_DC_LR)
+    lr = torch.zeros_like(field.flat)
+    real = torch.zeros_like(field.flat, dtype=torch.bool)
+    for c, ((off, w), base) in enumerate(zip(class_slices(n, k), lrs)):
+        lr[off: off + w * n] = base
+        real[off: off + w * n] = True
+        if c == 4:
+            j = torch.arange(w * n)
+            lr[off: off + w * n] = torch.where(j % k == 0, torch.tensor(SH_DC_LR), torch.tensor(SH_REST_LR))
+    bc1, bc2 = 1.0 - BETA1 ** steps, 1.0 - BETA2 ** steps
+
+    def adam_range(lo, hi, g, goff):
+        sl = slice(lo, hi)
+        gg = g[lo - goff: hi - goff]
+        msk = real[sl]
+        m = BETA1 * opt.m[sl] + (1.0 - BETA1) * gg
+        v = BETA2 * opt.v[sl] + (1.0 - BETA2) * gg * gg
+        p = field.flat[sl] - lr[sl] * (m / bc1) / (torch.sqrt(v / bc2) + EPS)
+        field.flat[sl] = torch.where(msk, p, field.flat[sl])
+        opt.m[sl] = torch.where(msk, m, opt.m[sl])
+        opt.v[sl] = torch.where(msk, v, opt.v[sl])
+
+    return adam_range
+
+
+def _sharded_worker(rank, world, port, q):
+    import types
+
+    import torch.distributed as dist
+
+    from paper_2503_13086_b200.field import flat_size
+    from paper_2503_13086_b200.rasterize import FieldGrads
+    from paper_2503_13086_b200.train import exchange_and_step, gather_moments, shard_layout
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, deg = 37, 1
+    gen = torch.Generator().manual_seed(0)
+    base = torch.randn(flat_size(n, 4), generator=gen)
+    out = {}
+    for mode in ("allreduce", "sharded"):
+        fld = _FlatField(base.clone(), n, deg)
+        opt = types.SimpleNamespace(m=torch.zeros_like(base), v=torch.zeros_like(base), scene_extent=2.0)
+        g = FieldGrads.zeros(n, deg, torch.device("cpu"))
+        g.flat.copy_(torch.randn(g.flat.shape, generator=torch.Generator().manual_seed(10 + rank)))
+        exchange_and_step(fld, g, opt, 1e-3, mode=mode, adam_range=_cpu_adam(fld, opt, 1e-3, 1))
+        if mode == "sharded":
+            gather_moments(fld, opt)
+        out[mode] = (fld.flat.clone(), opt.m.clone(), opt.v.clone(), g.flat[fld.flat.numel():].clone())
+    q.put((rank, {k: [t.numpy() for t in v] for k, v in out.items()}, shard_layout(base.numel(), world)))
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_step_matches_allreduce_gloo_world2():
+    """reduce-scatter -> Adam on the owned chunk -> all-gather gives the same
+    parameters and (after gather_moments) moments as all-reduce -> full Adam,
+    and both equal one step on the summed gradients (host logic over gloo)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, d, layout = q.get(timeout=180)
+        res[r] = d
+    for p in procs:
+        p.join(timeout=60)
+    chunk, main = layout
+    assert chunk % 4 == 0 and 0 < main <= res[0]["sharded"][0].size
+    for r in (0, 1):
+        for a, b in zip(res[r]["allreduce"], res[r]["sharded"]):
+            np.testing.assert_allclose(b, a, rtol=1e-6, atol=1e-7)
+    for i in range(4):
+        np.testing.assert_array_equal(res[0]["sharded"][i], res[1]["sharded"][i])
