@@ -332,14 +332,11 @@ __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t*
 // k_tile_sums writes each CTA's 64-bit sum; k_scan2's CTA t then sums the
 // sums of CTAs < t itself (independent loads, no chain through the
 // predecessors) and scans its items.  Blocks [0, n_per) scan A, the rest B.
-__global__ void __launch_bounds__(RX_THREADS) k_tile_sums(int64_t n, const uint32_t* __restrict__ cnt,
-                                                          const uint32_t* __restrict__ tiles, int n_per,
-                                                          uint64_t* __restrict__ sums) {
+__global__ void __launch_bounds__(RX_THREADS) k_tile_sums(int64_t n, const uint32_t* __restrict__ src,
+                                                          uint64_t* __restrict__ sums,
+                                                          unsigned long long* __restrict__ total) {
   __shared__ uint64_t s_red[RX_WARPS];
-  const bool a = (int)blockIdx.x < n_per;
-  const int tile = a ? blockIdx.x : blockIdx.x - n_per;
-  const uint32_t* src = a ? cnt : tiles;
-  const int64_t base = (int64_t)tile * RX_TILE + threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * RX_TILE + threadIdx.x;
   uint64_t v = 0;
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) {
@@ -355,6 +352,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_tile_sums(int64_t n, const uint3
 #pragma unroll
     for (int w = 0; w < RX_WARPS; w++) t += s_red[w];
     sums[blockIdx.x] = t;
+    if (total) atomicAdd(total, (unsigned long long)t);
   }
 }
 
@@ -362,8 +360,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_scan2(int64_t n, const uint32_t*
                                                       const uint32_t* __restrict__ order,
                                                       const uint32_t* __restrict__ tiles,
                                                       uint32_t* __restrict__ offset, uint32_t* __restrict__ row_offset,
-                                                      const uint64_t* __restrict__ sums, int n_per,
-                                                      uint64_t* __restrict__ total) {
+                                                      const uint64_t* __restrict__ sums, int n_per) {
   __shared__ uint64_t s_red[RX_WARPS];
   __shared__ uint64_t s_pre[RX_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -401,7 +398,6 @@ __global__ void __launch_bounds__(RX_THREADS) k_scan2(int64_t n, const uint32_t*
     tile_sum += s_red[w];
     prefix += s_pre[w];
   }
-  if (!a && threadIdx.x == 0 && (int64_t)(tile + 1) * RX_TILE >= n) *total = prefix + tile_sum;
   uint64_t run = prefix + wbase + incl - sum;
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) {
@@ -551,6 +547,40 @@ static int sm_count() {
 
 static inline int64_t rx_ctas(int64_t n) { return (n + RX_TILE - 1) / RX_TILE; }
 
+// The instance total M of the last ssr_scan_tiles of this host thread: copied
+// into pinned memory right after it is computed, with an event behind the copy.
+struct PendingTotal {
+  uint64_t* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  const uint64_t* dev = nullptr;
+  int device = -1;
+  bool armed = false;
+};
+
+static PendingTotal& pending_total() {
+  static thread_local PendingTotal pt;
+  return pt;
+}
+
+static int arm_pending_total(const uint64_t* total_dev, cudaStream_t st) {
+  PendingTotal& pt = pending_total();
+  int dev = 0;
+  SSR_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (!pt.host) SSR_TRY(check_cuda(cudaMallocHost(&pt.host, sizeof(uint64_t)), "pinned total"));
+  if (pt.ev && pt.device != dev) {
+    cudaEventDestroy(pt.ev);
+    pt.ev = nullptr;
+  }
+  if (!pt.ev) SSR_TRY(check_cuda(cudaEventCreateWithFlags(&pt.ev, cudaEventDisableTiming), "total event"));
+  pt.device = dev;
+  SSR_TRY(check_cuda(cudaMemcpyAsync(pt.host, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st),
+                     "instance total"));
+  SSR_TRY(check_cuda(cudaEventRecord(pt.ev, st), "total event record"));
+  pt.dev = total_dev;
+  pt.armed = true;
+  return SSR_OK;
+}
+
 // One stable radix pass: counts -> digit scan -> ranked scatter.
 template <int MODE>
 static int radix_pass(int64_t n, int shift, const uint32_t* keys_in, const uint32_t* vals_in, const uint32_t* tiles,
@@ -642,6 +672,14 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   uint32_t* keys_b = (uint32_t*)(w + L.keys_b);
   uint32_t* cnt = (uint32_t*)(w + L.cnt);
   SSR_TRY(check_cuda(cudaMemsetAsync(w, 0, L.zero_bytes, st), "scan workspace memset"));
+  SSR_TRY(check_cuda(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), st), "total memset"));
+  const int ctas = (int)L.ctas;
+  // M first (field-row tile sums, summed into *total_dev), then its copy to
+  // the host and an event: the host waits for M (ssr_bin_tiles_capacity) while
+  // the device runs the depth sort queued behind the event
+  k_tile_sums<<<ctas, RX_THREADS, 0, st>>>(n, splats.tiles, sums + ctas, (unsigned long long*)total_dev);
+  SSR_TRY(check_launch("k_tile_sums rows"));
+  SSR_TRY(arm_pending_total(total_dev, st));
   // pass 0: keys from (tiles, depth) -> (keys_a, vals_a); pass 1 -> (keys_b, cnt as scratch);
   // pass 2 -> (keys_a, depth_order); the tie-fix then fixes depth_order in place and fills cnt
   SSR_TRY(radix_pass<1>(n, 0, nullptr, nullptr, splats.tiles, splats.depth, keys_a, vals_a, counts, offsets, hist,
@@ -652,11 +690,10 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   k_depth_tiefix<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, keys_a, splats.depth_order, splats.depth,
                                                               splats.tiles, cnt);
   SSR_TRY(check_launch("k_depth_tiefix"));
-  const int ctas = (int)L.ctas;
-  k_tile_sums<<<2 * ctas, RX_THREADS, 0, st>>>(n, cnt, splats.tiles, ctas, sums);
-  SSR_TRY(check_launch("k_tile_sums"));
+  k_tile_sums<<<ctas, RX_THREADS, 0, st>>>(n, cnt, sums, nullptr);
+  SSR_TRY(check_launch("k_tile_sums depth"));
   k_scan2<<<2 * ctas, RX_THREADS, 0, st>>>(n, cnt, splats.depth_order, splats.tiles, splats.offset,
-                                           splats.row_offset, sums, ctas, total_dev);
+                                           splats.row_offset, sums, ctas);
   return check_launch("k_scan2");
 }
 
@@ -721,13 +758,22 @@ extern "C" int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles
     return SSR_ERR_INVALID;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // one pinned word per host thread for the instance total
-  static thread_local uint64_t* host_total = nullptr;
-  if (!host_total) SSR_TRY(check_cuda(cudaMallocHost(&host_total, sizeof(uint64_t)), "pinned total"));
-  SSR_TRY(check_cuda(cudaMemcpyAsync(host_total, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st),
-                     "instance total"));
-  SSR_TRY(check_cuda(cudaStreamSynchronize(st), "instance total"));
-  const int64_t m = (int64_t)*host_total;
+  PendingTotal& pt = pending_total();
+  int64_t m;
+  if (pt.armed && pt.dev == total_dev) {
+    // the copy was queued by ssr_scan_tiles ahead of its depth sort: wait for
+    // it alone, so the binning is launched while the device still sorts
+    SSR_TRY(check_cuda(cudaEventSynchronize(pt.ev), "instance total"));
+    m = (int64_t)*pt.host;
+    pt.armed = false;
+  } else {
+    static thread_local uint64_t* host_total = nullptr;
+    if (!host_total) SSR_TRY(check_cuda(cudaMallocHost(&host_total, sizeof(uint64_t)), "pinned total"));
+    SSR_TRY(check_cuda(cudaMemcpyAsync(host_total, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st),
+                       "instance total"));
+    SSR_TRY(check_cuda(cudaStreamSynchronize(st), "instance total"));
+    m = (int64_t)*host_total;
+  }
   *m_out = m;
   if (m > MAX_INSTANCES) {
     set_error("ssr_bin_tiles_capacity: instance count exceeds 2^30 - 1");

@@ -547,6 +547,10 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
 // (pixel 256: blend limit 0), so the stream needs no bounds checks.  The mean
 // gradient is accumulated as sum(gp dx), sum(gp dy) and mapped through the
 // conic once per row (linear), so a contributing pair costs ~30 instructions.
+#ifndef SSR_BW_UNROLL
+#define SSR_BW_UNROLL 2
+#endif
+constexpr int BW_UNROLL = SSR_BW_UNROLL;
 constexpr int BW_PAD = 32;
 constexpr int BW_LIST = BW_PAD + TILE_PX + BW_PAD;
 
@@ -587,7 +591,7 @@ __device__ __forceinline__ void bw_stream(
   const char* sPixb = reinterpret_cast<const char*>(sPix);
   constexpr int B_OFF = (TILE_PX + 1) * sizeof(float4);
   float4 PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF), PAn = *reinterpret_cast<const float4*>(sPixb + on);
-#pragma unroll 2
+#pragma unroll BW_UNROLL
   for (int i = 0; i < n_steps; i++) {
     float Tin = __shfl_up_sync(FULL, T, 1);
     float Hin = __shfl_up_sync(FULL, H, 1);
@@ -600,8 +604,18 @@ __device__ __forceinline__ void bw_stream(
     PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF);
     PAn = *reinterpret_cast<const float4*>(sPixb + on);
     const int lim = __float_as_int(PB.w);
+#ifdef SSR_BW_PACKED
+    // (dx, dy) and (dxx, dyy) as packed pairs: each lane bit-identical to the
+    // scalar __fsub_rn / __fmul_rn the forward uses
+    const float2 d2 = f2_sub(f2_sub(make_float2(PB.x, PB.y), make_float2(s.sm.xi, s.sm.yi)),
+                             make_float2(s.sm.xf, s.sm.yf));
+    const float dx = d2.x, dy = d2.y;
+    const float2 sq = f2_mul(d2, d2);
+    const float dxx = sq.x, dyy = sq.y, dxy = __fmul_rn(dx, dy);
+#else
     const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
     const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+#endif
     float qpos;
     const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
     if (!SOFT) {
@@ -627,11 +641,22 @@ __device__ __forceinline__ void bw_stream(
       // alpha = 0 and a finite dlda, so its gp is already zero
       const float gp = araw <= ALPHA_CAP_F ? dlda * alpha : 0.f;
       g.g3 += gp;
+#ifdef SSR_BW_PACKED
+      {
+        const float2 s2 = f2_fma(make_float2(gp, gp), d2, make_float2(g.sx, g.sy));
+        const float2 q2 = f2_fma(make_float2(gp, gp), sq, make_float2(g.g6, g.g8));
+        g.sx = s2.x;
+        g.sy = s2.y;
+        g.g6 = q2.x;
+        g.g8 = q2.y;
+      }
+#else
       g.sx = fmaf(gp, dx, g.sx);
       g.sy = fmaf(gp, dy, g.sy);
       g.g6 = fmaf(gp, dxx, g.g6);
-      g.g7 = fmaf(gp, dxy, g.g7);
       g.g8 = fmaf(gp, dyy, g.g8);
+#endif
+      g.g7 = fmaf(gp, dxy, g.g7);
     } else {
       // same branch-free form with the soft-count term of every walked pair
       // below the cap
