@@ -16,9 +16,18 @@ namespace ssr {
 // full CTA (the last, partial one reads global memory directly).
 constexpr int PRE_ROWS = 128;
 
+// SH rows are not staged: only the rows that survive culling read theirs
+// (12 float4 loads at degree 3, sh_color64), so culled rows (~40% at config 2)
+// cost no SH traffic.  SSR_PRE_STAGE_SH restores staging every row's SH.
+#ifdef SSR_PRE_STAGE_SH
+constexpr bool PRE_STAGE_SH = true;
+#else
+constexpr bool PRE_STAGE_SH = false;
+#endif
+
 template <int DEG>
 __host__ __device__ constexpr int pre_stage_floats() {
-  return PRE_ROWS * (3 + 4 + 3 + 3 * (DEG + 1) * (DEG + 1));
+  return PRE_ROWS * (3 + 4 + 3 + (PRE_STAGE_SH ? 3 * (DEG + 1) * (DEG + 1) : 0));
 }
 
 template <int DEG, bool STAGED>
@@ -42,7 +51,7 @@ __global__ void __launch_bounds__(PRE_ROWS, 7) k_preprocess(Cam cam, int64_t n, 
       bulk_g2s(s_pre, rot + i0 * 4, PRE_ROWS * 16, &mbar);
       bulk_g2s(s_pre + 4 * PRE_ROWS, pos + i0 * 3, PRE_ROWS * 12, &mbar);
       bulk_g2s(s_pre + 7 * PRE_ROWS, ls + i0 * 3, PRE_ROWS * 12, &mbar);
-      bulk_g2s(s_pre + 10 * PRE_ROWS, sh + i0 * W, PRE_ROWS * W * 4, &mbar);
+      if (PRE_STAGE_SH) bulk_g2s(s_pre + 10 * PRE_ROWS, sh + i0 * W, PRE_ROWS * W * 4, &mbar);
     }
     __syncthreads();
     mbar_wait(&mbar, 0);
@@ -52,8 +61,8 @@ __global__ void __launch_bounds__(PRE_ROWS, 7) k_preprocess(Cam cam, int64_t n, 
   const float* prow = staged ? s_pre + 4 * PRE_ROWS + r * 3 : pos + i * 3;
   const float* qrow = staged ? s_pre + r * 4 : rot + i * 4;
   const float* lrow = staged ? s_pre + 7 * PRE_ROWS + r * 3 : ls + i * 3;
-  const float* shrow = staged ? s_pre + 10 * PRE_ROWS + r * W : sh + i * W;
-  if (!staged) {
+  const float* shrow = staged && PRE_STAGE_SH ? s_pre + 10 * PRE_ROWS + r * W : sh + i * W;
+  if (!staged && PRE_STAGE_SH) {
     // start the row's SH coefficients on their way to L2 while the fp64
     // projection runs (culled rows waste 3K floats of L2 fill, visible rows
     // then read them at L2 latency)
