@@ -11,6 +11,7 @@ N * steps / time).
 Extra blocks on the same JSON line (each its own workload, timed the same way):
   paper_objective      config 2 under the reference's default LossWeights() (load 0.41)
   no_splat_parallel    config 2 with the pixel-parallel backward (the paper's No_SPB ablation)
+  small_configs        configs 0 and 1 at N=1 (launch- and latency-bound sizes)
   semi_global_batch    config 4: 3M Gaussians, a 64-view 1080p batch sharded 64/N per rank,
                        summed gradients exchanged once per batch (strong scaling)
   progressive          config 3 seconds per new image (reference plan replayed), both objectives
@@ -276,6 +277,38 @@ def _device_loop(fn, steps):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1)
+
+
+def small_configs(args, local, steps=20):
+    """Configs 0 and 1 (BASELINE's CPU-reference case and the 200k/800x800
+    case) at N=1: the same single-view iteration, device-timed."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.rasterize import render
+    from paper_2503_13086_b200.train import TrainState, train_iteration
+
+    out = {}
+    for cfg in (0, 1):
+        cams = [scenes.camera(cfg, view=v) for v in range(8)]
+        tf = GaussianField.from_host(scenes.make_params(cfg, seed=1))
+        targets = [render(tf, c, for_backward=False).image.clone() for c in cams]
+        del tf
+        f = GaussianField.from_host(scenes.make_params(cfg, seed=0))
+        st = TrainState(field=f, optimizer=FieldOptimizer(f, scene_extent=4.4 if cfg == 0 else 5.5),
+                        weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), densify_enabled=False)
+        for k in range(8 + 3):
+            train_iteration(st, cams[k % 8], targets[k % 8], 1.6e-4)
+        ms = _device_loop(lambda k: train_iteration(st, cams[k % 8], targets[k % 8], 1.6e-4), steps)
+        c = scenes.CONFIGS[cfg]
+        out[f"config{cfg}"] = {"value": steps / (ms / 1e3), "unit": "iters/s", "ms_per_step": ms / steps,
+                               "workload": f"{c['n']:,} Gaussians SH{c['sh_degree']} {c['width']}x{c['height']}, "
+                                           "render + L1/D-SSIM + backward + Adam, 8 views cycled"}
+        del st, f, targets
+        torch.cuda.empty_cache()
+    return out
 
 
 def semi_global_batch(args, rank, world, local):
@@ -651,6 +684,12 @@ def main():
             batch_block = {"error": f"{type(ex).__name__}: {ex}"}
     if rank != 0:
         return
+    small = None
+    if world == 1 and args.extra_steps > 0:
+        try:
+            small = small_configs(args, local)
+        except Exception as ex:  # pragma: no cover
+            small = {"error": f"{type(ex).__name__}: {ex}"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -700,6 +739,7 @@ def main():
         "gpu_launches": launches,
         **extras,
         "semi_global_batch": batch_block,
+        "small_configs": small,
         "progressive": progressive,
         "clocks": clk.summary(),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if not k.endswith("workspace")},

@@ -315,6 +315,35 @@ class DeviceSession:
         return t if t.dtype != torch.uint8 else t.float() / 255.0
 
 
+def phase1_initialize(session: DeviceSession, frames, positions, colors, matches=None, initial_iters: int = 0,
+                      fused: bool = True) -> DeviceSession:
+    """pipeline.py:219-253 on a DeviceSession: register the bootstrap frames and
+    their pairwise matches, insert the sparse cloud, start the optimizer and
+    train ``initial_iters`` round-robin iterations."""
+    frames = list(frames)
+    if not frames:
+        raise InvalidParameter("expected at least one bootstrap frame")
+    for f in frames:
+        session.register_frame(f)
+    for (i, j), raw in (matches or {}).items():
+        session.planner.set_matches(i, j, raw)
+    pos = torch.as_tensor(np.asarray(positions) if not torch.is_tensor(positions) else positions)
+    col = torch.as_tensor(np.asarray(colors) if not torch.is_tensor(colors) else colors)
+    if pos.numel() == 0:
+        raise InvalidParameter("initial sparse cloud is empty")
+    n = session.field.insert_arrays(pos, col, init_opacity=session.cfg.init_opacity)
+    if n == 0:
+        raise InvalidParameter("initial sparse cloud has no finite points")
+    ok = torch.isfinite(pos.double().reshape(-1, 3)).all(dim=1) & torch.isfinite(col.double().reshape(-1, 3)).all(dim=1)
+    session.sparse_positions = pos.double().reshape(-1, 3)[ok].to(session.field.flat.device)
+    session.state.stats = torch.zeros(2 * len(session.field), dtype=torch.float32, device=session.field.flat.device)
+    session.start_optimizer()
+    order = [f.image_id for f in frames]
+    for k in range(initial_iters):
+        train_one_iteration(session, order[k % len(order)], fused=fused)
+    return session
+
+
 def train_one_iteration(session: DeviceSession, target_id, fused: bool = True) -> LossBreakdown:
     """pipeline.py:185-206: rate from the scheduler, then the hot path
     (train.train_iteration: render -> total_loss -> backward + Adam with the

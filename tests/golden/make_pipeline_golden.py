@@ -75,6 +75,13 @@ def main(out=os.path.join(HERE, "pipeline_small.npz"), n_events=3):
     bundle, _ = to_bundle(scene)
     stream = ReplayStream(bundle)
     frames, pts, matches = stream.initial(cfg.n0)
+    # the bootstrap field before any training (phase1_initialize's insert_points)
+    boot = GaussianField(sh_degree=cfg.sh_degree)
+    usable = [p for p in pts if p.finite]
+    boot.insert_points(usable, init_opacity=cfg.init_opacity)
+    boot_rec = {f"boot_{k}": np.array(getattr(boot, k)) for k in PARAM_KEYS}
+    boot_rec["boot_points_pos"] = np.array([p.position for p in pts]).reshape(-1, 3)
+    boot_rec["boot_points_col"] = np.array([p.color for p in pts]).reshape(-1, 3)
     state = phase1_initialize(frames, pts, cfg, matches=matches)
 
     # float32 storage: round parameters and moments before phase 2
@@ -84,7 +91,7 @@ def main(out=os.path.join(HERE, "pipeline_small.npz"), n_events=3):
         buf.m, buf.v = f32(buf.m), f32(buf.v)
     state.grad_accum = f32(state.grad_accum)
 
-    rec = {}
+    rec = dict(boot_rec)
     save_state(rec, "p1", state)
     rec["init_ids"] = np.array([f.image_id for f in frames])
     rec["init_matches"] = np.array([[i, j, c] for (i, j), c in sorted((matches or {}).items())],

@@ -146,3 +146,31 @@ def test_phase2_event_matches_reference_loop(event):
         "loss_total_rel_max": float(np.max(np.abs(got[:, 3] - ref_losses[:, 3]) / np.abs(ref_losses[:, 3]))),
         "psnr_after": [rep.psnr_after, float(psnr_a)], "param_rel_l2": rels}))
     assert all(r <= 2e-2 for r in rels.values()), rels
+
+
+def test_phase1_bootstrap_matches_reference_insert():
+    """pipeline.phase1_initialize (before training) == the reference's
+    phase1_initialize insert_points on the same sparse cloud (3-NN scales on the
+    GPU index), same extent and sparse cloud."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.pipeline import DeviceSession, LoopConfig, TracePlanner, phase1_initialize
+
+    g = _load()
+    c = json.loads(str(g["cfg"]))
+    cfg = LoopConfig(t_i=c["t_i"], n_m=c["n_m"], loss_weights=LossWeights(*c["weights"]),
+                     init_opacity=c["init_opacity"])
+    s = DeviceSession(GaussianField(sh_degree=c["sh_degree"]), cfg, TracePlanner({}))
+    frames = [_frame(g, i) for i in g["init_ids"]]
+    for f in frames:
+        f.pixels = g[f"frame{f.image_id}_pixels"]
+    phase1_initialize(s, frames, g["boot_points_pos"], g["boot_points_col"], initial_iters=0)
+    for k in PARAM_KEYS:
+        np.testing.assert_allclose(getattr(s.field, k).cpu().numpy(), g[f"boot_{k}"], rtol=2e-6, atol=2e-7,
+                                   err_msg=k)
+    assert s.optimizer is not None and s.optimizer.n_rows == len(s.field)
+    assert s.state.stats.numel() == 2 * len(s.field) and float(s.state.stats.abs().sum()) == 0.0
+    torch.testing.assert_close(s.sparse_positions.cpu(), torch.as_tensor(g["boot_points_pos"]), rtol=0, atol=0)
+    assert s.scene_extent == pytest.approx(float(g["p1_extent"]), rel=1e-12)
