@@ -171,3 +171,46 @@ def test_adam_range_chunks_equal_full_adam(world):
                   ob.v.data_ptr(), lo, hi, lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(fa.flat, fb.flat) and torch.equal(oa.m, ob.m) and torch.equal(oa.v, ob.v)
+
+
+@pytest.mark.slow
+def test_config4_batch_gradients_vs_oracle(oracle_lib):
+    """Config 4 at full size (3M Gaussians, SH3, 1080p): a two-view semi-global
+    batch's summed gradients vs the sum of the float64 oracle's per-view
+    backwards (SURVEY 8e parity at the config's scale), with projections and
+    renders of both views checked on the way."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.rasterize import FieldGrads, backward, render
+    from parity import forward_ok, forward_report, projection_report
+
+    hp = scenes.make_params(4, seed=0)
+    f = GaussianField.from_host(hp)
+    P = oracle_lib.Params(*(getattr(hp, k).astype(np.float64) for k in GRAD_CLASSES))
+    rng = np.random.default_rng(7)
+    grads = FieldGrads.zeros(len(f), f.sh_degree, f.flat.device)
+    want = {k: 0.0 for k in GRAD_CLASSES}
+    want_norms, want_vis = 0.0, 0.0
+    for v in (5, 37):
+        cam = scenes.camera(4, view=v)
+        out = render(f, cam)
+        ref = oracle_lib.render(P, cam)
+        pr = projection_report(out.splats, ref["splats"])
+        assert all(x for k, x in pr.items() if k.endswith("_equal")), pr
+        fr = forward_report(out, ref)
+        assert forward_ok(fr), fr
+        d_img = (rng.standard_normal((cam.height, cam.width, 3)) * 1e-6).astype(np.float32)
+        d_soft = (rng.standard_normal((cam.height, cam.width)) * 1e-7).astype(np.float32)
+        backward(f, out, d_img, d_soft, grads=grads, accumulate=True)
+        g = oracle_lib.backward(P, ref, d_img.astype(np.float64), d_soft.astype(np.float64))
+        for k in GRAD_CLASSES:
+            want[k] = want[k] + g[k]
+        want_norms = want_norms + g["screen_norms"]
+        want_vis = want_vis + g["visible"].astype(np.float64)
+        del out, ref
+    torch.cuda.synchronize()
+    want["screen_norms"], want["visible"] = want_norms, want_vis > 0
+    r = grads_report(grads, want)
+    assert grads_ok(r), r
+    np.testing.assert_array_equal(grads.visible_count.cpu().numpy(), want_vis)
