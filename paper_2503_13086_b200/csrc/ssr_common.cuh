@@ -497,4 +497,77 @@ __device__ __forceinline__ float adam_update(float p, float g, float& m, float& 
   return p - __fdividef(lr * (m * ib1), sqrt_approx(v * ib2) + 1e-15f);
 }
 
+// ------------------------------------------------------------------ exclusive scan of uint32
+// Two launches, no library code: per-4096-element CTA sums, then each CTA sums
+// its predecessors' totals directly (no look-back chain) and scans its own
+// elements, 16 consecutive per thread.  Totals are 64-bit (out is uint32).
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 16, SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+static __global__ void __launch_bounds__(SCAN_THREADS) k_u32_tile_sums(int64_t n, const uint32_t* __restrict__ in,
+                                                                     uint64_t* __restrict__ sums) {
+  __shared__ uint64_t red[SCAN_THREADS / 32];
+  uint64_t v = 0;
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t r = (int64_t)blockIdx.x * SCAN_TILE + i * SCAN_THREADS + threadIdx.x;
+    if (r < n) v += in[r];
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; w++) t += red[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
+static __global__ void __launch_bounds__(SCAN_THREADS) k_u32_scan(int64_t n, const uint32_t* __restrict__ in,
+                                                                const uint64_t* __restrict__ sums,
+                                                                uint32_t* __restrict__ out) {
+  __shared__ uint64_t s_w[SCAN_THREADS / 32], s_p[SCAN_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t pre = 0;
+  for (int t = threadIdx.x; t < (int)blockIdx.x; t += SCAN_THREADS) pre += sums[t];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  uint32_t v[SCAN_ITEMS];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    v[i] = base + i < n ? in[base + i] : 0u;
+    sum += v[i];
+  }
+  uint64_t incl = sum;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 31) s_w[warp] = incl;
+  if (lane == 0) s_p[warp] = pre;
+  __syncthreads();
+  uint64_t wb = 0, p = 0;
+  for (int w = 0; w < SCAN_THREADS / 32; w++) {
+    if (w < warp) wb += s_w[w];
+    p += s_p[w];
+  }
+  uint64_t run = p + wb + incl - sum;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    if (base + i < n) out[base + i] = (uint32_t)run;
+    run += v[i];
+  }
+}
+
+static inline int64_t scan_u32_workspace(int64_t n) { return 8 * ((n + SCAN_TILE - 1) / SCAN_TILE + 1); }
+
+// exclusive scan in -> out of n elements; ws holds scan_u32_workspace(n) bytes
+static inline int scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* ws, cudaStream_t st) {
+  if (n <= 0) return SSR_OK;
+  const unsigned ctas = (unsigned)((n + SCAN_TILE - 1) / SCAN_TILE);
+  k_u32_tile_sums<<<ctas, SCAN_THREADS, 0, st>>>(n, in, (uint64_t*)ws);
+  SSR_TRY(check_launch("k_u32_tile_sums"));
+  k_u32_scan<<<ctas, SCAN_THREADS, 0, st>>>(n, in, (const uint64_t*)ws, out);
+  return check_launch("k_u32_scan");
+}
+
 }  // namespace ssr

@@ -10,7 +10,6 @@
 // lies inside its own cell, the bbox covers pool and queries), so the walk
 // stops once the k-th distance is <= r*h.  float64 throughout, so distances
 // are those of a float64 k-d tree.
-#include <cub/device/device_scan.cuh>
 #include <math_constants.h>
 
 #include "ssr_common.cuh"
@@ -147,12 +146,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn_query(int64_t nq, const 
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-static size_t knn_scan_bytes(int64_t n_cells) {
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                (int)(n_cells + 1));
-  return b;
-}
+static size_t knn_scan_bytes(int64_t n_cells) { return (size_t)scan_u32_workspace(n_cells + 1); }
 
 }  // namespace ssr
 
@@ -208,9 +202,7 @@ extern "C" int ssr_knn(const double* pool, int64_t n_pool, const double* queries
     k_knn_count<<<(unsigned)((n_pool + 255) / 256), 256, 0, st>>>(n_pool, pool, g, cell_of, count);
     SSR_TRY(check_launch("k_knn_count"));
   }
-  size_t tb = knn_scan_bytes(n_cells);
-  SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)temp, tb, count, start, (int)(n_cells + 1), st),
-                     "knn scan"));
+  SSR_TRY(scan_u32(count, start, n_cells + 1, temp, st));
   SSR_TRY(check_cuda(cudaMemcpyAsync(cursor, start, 4 * (n_cells + 1), cudaMemcpyDeviceToDevice, st), "knn cursor"));
   if (n_pool > 0) {
     k_knn_scatter<<<(unsigned)((n_pool + 255) / 256), 256, 0, st>>>(n_pool, pool, cell_of, cursor, sorted);

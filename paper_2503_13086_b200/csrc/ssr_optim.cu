@@ -4,9 +4,6 @@
 // The field lives in one flat float32 buffer per quantity, class-major:
 //   [positions 3N | rotations 4N | log_scales 3N | opacity_logits N | sh 3KN]
 // so Adam is a single vectorised pass over params, grads, m and v.
-#include <cub/device/device_scan.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
-
 #include "ssr_common.cuh"
 
 namespace ssr {
@@ -110,10 +107,89 @@ __global__ void k_densify_masks(int64_t n, int K, const float* __restrict__ para
   if (prune) atomicAdd(&counts[2], 1);
 }
 
-struct FlagBit {
-  int bit;
-  __host__ __device__ uint32_t operator()(uint8_t f) const { return (f >> bit) & 1u; }
-};
+// Exclusive scans of the three flag bits (keep, clone, split) over the rows,
+// hand-written: k_flag_sums gives each 4096-row CTA its three counts, then
+// k_flag_scan's CTA t sums its predecessors' counts directly (no look-back
+// chain) and scans its own rows, thread j owning 16 consecutive rows.
+constexpr int FS_THREADS = 256, FS_ITEMS = 16, FS_ROWS = FS_THREADS * FS_ITEMS;
+
+__global__ void __launch_bounds__(FS_THREADS) k_flag_sums(int64_t n, const uint8_t* __restrict__ flags,
+                                                          uint32_t* __restrict__ sums) {
+  __shared__ uint32_t red[3][FS_THREADS / 32];
+  uint32_t c[3] = {0u, 0u, 0u};
+  for (int i = 0; i < FS_ITEMS; i++) {
+    const int64_t r = (int64_t)blockIdx.x * FS_ROWS + i * FS_THREADS + threadIdx.x;
+    if (r < n) {
+      const uint32_t f = flags[r];
+      c[0] += f & 1u;
+      c[1] += (f >> 1) & 1u;
+      c[2] += (f >> 2) & 1u;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 3; b++) {
+    for (int o = 16; o > 0; o >>= 1) c[b] += __shfl_xor_sync(0xffffffffu, c[b], o);
+    if ((threadIdx.x & 31) == 0) red[b][threadIdx.x >> 5] = c[b];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    uint32_t t = 0;
+    for (int w = 0; w < FS_THREADS / 32; w++) t += red[threadIdx.x][w];
+    sums[(size_t)blockIdx.x * 3 + threadIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(FS_THREADS) k_flag_scan(int64_t n, const uint8_t* __restrict__ flags,
+                                                          const uint32_t* __restrict__ sums, uint32_t* __restrict__ o0,
+                                                          uint32_t* __restrict__ o1, uint32_t* __restrict__ o2) {
+  __shared__ uint32_t s_w[3][FS_THREADS / 32], s_p[3][FS_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t pre[3] = {0u, 0u, 0u};
+  for (int t = threadIdx.x; t < (int)blockIdx.x; t += FS_THREADS)
+#pragma unroll
+    for (int b = 0; b < 3; b++) pre[b] += sums[(size_t)t * 3 + b];
+  const int64_t base = (int64_t)blockIdx.x * FS_ROWS + (int64_t)threadIdx.x * FS_ITEMS;
+  uint8_t f[FS_ITEMS];
+  uint32_t sum[3] = {0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < FS_ITEMS; i++) {
+    f[i] = base + i < n ? flags[base + i] : (uint8_t)0;
+#pragma unroll
+    for (int b = 0; b < 3; b++) sum[b] += (f[i] >> b) & 1u;
+  }
+  uint32_t incl[3];
+#pragma unroll
+  for (int b = 0; b < 3; b++) {
+    incl[b] = sum[b];
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, incl[b], d);
+      if (lane >= d) incl[b] += o;
+    }
+    for (int o = 16; o > 0; o >>= 1) pre[b] += __shfl_xor_sync(0xffffffffu, pre[b], o);
+    if (lane == 31) s_w[b][warp] = incl[b];
+    if (lane == 0) s_p[b][warp] = pre[b];
+  }
+  __syncthreads();
+  uint32_t run[3];
+#pragma unroll
+  for (int b = 0; b < 3; b++) {
+    uint32_t wb = 0, p = 0;
+    for (int w = 0; w < FS_THREADS / 32; w++) {
+      if (w < warp) wb += s_w[b][w];
+      p += s_p[b][w];
+    }
+    run[b] = p + wb + incl[b] - sum[b];
+  }
+  uint32_t* outs[3] = {o0, o1, o2};
+#pragma unroll
+  for (int i = 0; i < FS_ITEMS; i++) {
+    if (base + i < n)
+#pragma unroll
+      for (int b = 0; b < 3; b++) outs[b][base + i] = run[b];
+#pragma unroll
+    for (int b = 0; b < 3; b++) run[b] += (f[i] >> b) & 1u;
+  }
+}
 
 // field.py:329-372 + optim.py:49-54: kept rows, then clones, then split pairs.
 // Kept rows (field.py:303-375 compaction): one warp per 32 source rows copies
@@ -303,15 +379,9 @@ extern "C" int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degr
   return check_launch("k_densify_masks");
 }
 
-static size_t densify_scan_bytes(int64_t n) {
-  size_t b = 0;
-  cub::TransformInputIterator<uint32_t, FlagBit, const uint8_t*> it((const uint8_t*)nullptr, FlagBit{0});
-  cub::DeviceScan::ExclusiveSum((void*)nullptr, b, it, (uint32_t*)nullptr, (int)(n > 0 ? n : 1));
-  return b;
-}
-
 extern "C" int ssr_densify_workspace(int64_t n, int64_t* bytes) {
-  *bytes = 3 * align_up(4 * (n > 0 ? n : 1), 256) + align_up((int64_t)densify_scan_bytes(n), 256) + 256;
+  const int64_t nn = n > 0 ? n : 1;
+  *bytes = 3 * align_up(4 * nn, 256) + align_up(12 * ((nn + FS_ROWS - 1) / FS_ROWS), 256) + 256;
   return SSR_OK;
 }
 
@@ -338,12 +408,12 @@ extern "C" int ssr_densify_apply(int64_t n, int64_t n_new, int32_t sh_degree, co
     offs[b] = (uint32_t*)w;
     w += align_up(4 * n, 256);
   }
-  size_t tb = densify_scan_bytes(n);
-  for (int b = 0; b < 3; b++) {
-    cub::TransformInputIterator<uint32_t, FlagBit, const uint8_t*> it(flags, FlagBit{b});
-    size_t tb2 = tb;
-    SSR_TRY(check_cuda(cub::DeviceScan::ExclusiveSum((void*)w, tb2, it, offs[b], (int)n, st), "densify scan"));
-  }
+  const unsigned fs = (unsigned)((n + FS_ROWS - 1) / FS_ROWS);
+  uint32_t* fsums = (uint32_t*)w;
+  k_flag_sums<<<fs, FS_THREADS, 0, st>>>(n, flags, fsums);
+  SSR_TRY(check_launch("k_flag_sums"));
+  k_flag_scan<<<fs, FS_THREADS, 0, st>>>(n, flags, fsums, offs[0], offs[1], offs[2]);
+  SSR_TRY(check_launch("k_flag_scan"));
   const unsigned kb = (unsigned)((n + 255) / 256);
   switch (K) {
     case 1: k_densify_keep<1><<<kb, 256, 0, st>>>(n, n_new, params, m, v, flags, offs[0], new_params, new_m, new_v); break;
