@@ -417,7 +417,8 @@ def main():
     def step(k, target=None, values_out=None):
         cam_i = (k * world + rank) % len(cams)
         cam = cams[cam_i]
-        out = render(state.field, cam)
+        # soft counts only when the objective reads them (load weight > 0, losses.py:155-160)
+        out = render(state.field, cam, soft_count=state.weights.load > 0)
         br = total_loss(out.image, targets[cam_i] if target is None else target, out, state.weights,
                         values_out=values_out)
         if world > 1:

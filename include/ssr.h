@@ -247,7 +247,8 @@ int ssr_ply_unpack(int64_t n, int32_t sh_degree, const double* records, float* p
  * target: H x W x 3 float32 in [0, 1], or 8-bit (target_u8 != 0; value / 255,
  * like the reference's image loader io/images.py).
  * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,
- * total, hard_count_std) as float64 in device memory. */
+ * total, hard_count_std) as float64 in device memory.  soft_count may be NULL
+ * when w_load == 0 and d_soft == NULL (a render without soft counts). */
 int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes);
 int ssr_loss(int32_t width, int32_t height, const float* image, const void* target, int32_t target_u8,
              const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim,

@@ -212,13 +212,13 @@ __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* 
     __syncthreads();
   }
   double sd = 0.0, sd2 = 0.0, hd = 0.0, hd2 = 0.0;
-  const double s0 = soft[0];
+  const double s0 = soft ? soft[0] : 0.0;  // soft == NULL: the render computed no soft counts (load weight 0)
   const int32_t h0 = hard[0];
   for (int e = tid; e < LT * LT; e += blockDim.x) {
     const int gr = r0 + e / LT, gc = c0 + e % LT;
     if (gr >= H || gc >= W) continue;
     const size_t pi = (size_t)gr * W + gc;
-    const double d = soft[pi] - s0;
+    const double d = soft ? soft[pi] - s0 : 0.0;
     sd += d;
     sd2 += d * d;
     const double dh = (double)(hard[pi] - h0);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_loss_finalize(int W, int H, dou
   double sd = var > 0.0 ? sqrt(var) : 0.0;
   const double mh = acc->hard_d / n;
   double varh = acc->hard_d2 / n - mh * mh;
-  acc->mean_soft = soft[0] + md;
+  acc->mean_soft = (soft ? soft[0] : 0.0) + md;
   acc->std_soft = sd;
   const double load = w_load > 0.0 ? sd : 0.0;
   out[0] = l1;
@@ -468,6 +468,10 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   ssr_loss_workspace(width, height, &need);
   if (workspace_bytes < need) {
     set_error("ssr_loss: workspace too small");
+    return SSR_ERR_INVALID;
+  }
+  if (!soft_count && (w_load > 0.0 || d_soft)) {
+    set_error("ssr_loss: soft_count is required for a load term or a d_soft output");
     return SSR_ERR_INVALID;
   }
   SSR_TRY(ensure_window());

@@ -82,19 +82,23 @@ struct FwdState {
 // small-alpha soft deviation, or the large path (exact sigmoid, guard bands,
 // blend).  w100 = staged +-100 opacity (sign: fragile).  Returns false once
 // the pixel terminated or was flagged.
-template <bool FRAGILE>
+template <bool FRAGILE, bool SOFT>
 __device__ __forceinline__ bool fwd_slot(FwdState& q, float p2, float qpos, float w100, const float4* sB, int j,
                                          int k0, float band, float band_t) {
-  if (FRAGILE && w100 < 0.f) {
-    // only near-singular conics can round to power > 0: flag near that decision
-    if (p2 > 1e-6f * qpos && qpos != 0.f) {
-      q.flag = true;
-      q.nwk = k0 + j;  // flagged: the slot of the ambiguous decision
-      return false;
-    }
-    if (p2 > 0.f) {
-      q.nbig++;  // skipped: no soft term (counted out of the S0 total)
-      return true;
+  if (FRAGILE) {
+    // SOFT = false stages the signed opacity in sB[j].w instead of +-100 opacity
+    const bool fragile = SOFT ? w100 < 0.f : sB[j].w < 0.f;
+    if (fragile) {
+      // only near-singular conics can round to power > 0: flag near that decision
+      if (p2 > 1e-6f * qpos && qpos != 0.f) {
+        q.flag = true;
+        q.nwk = k0 + j;  // flagged: the slot of the ambiguous decision
+        return false;
+      }
+      if (p2 > 0.f) {
+        q.nbig++;  // skipped: no soft term (counted out of the S0 total)
+        return true;
+      }
     }
   }
   // y = 100 alpha costs one product; alpha itself (= opacity * 2^p2, the
@@ -102,17 +106,21 @@ __device__ __forceinline__ bool fwd_slot(FwdState& q, float p2, float qpos, floa
   // fl(alpha * 100) in the last bit: that only moves a pair between the
   // deviation fit and the exact sigmoid (|diff| < 2e-10).
   const float e2 = ex2_approx(p2);
-  const float y = __fmul_rn(fabsf(w100), e2);
-  if (y < SOFT_Y0) {
-    q.sdev = soft_dev_acc(y, q.sdev);
-    return true;
+  if (SOFT) {
+    const float y = __fmul_rn(fabsf(w100), e2);
+    if (y < SOFT_Y0) {
+      q.sdev = soft_dev_acc(y, q.sdev);
+      return true;
+    }
   }
   const float4 B = sB[j];
-  float alpha = __fmul_rn(B.w, e2);
+  float alpha = __fmul_rn(SOFT ? B.w : fabsf(B.w), e2);
   const bool fa = (fabsf(alpha - ALPHA_MIN_F) < ALPHA_MIN_F * band) | (fabsf(alpha - ALPHA_CAP_F) < ALPHA_CAP_F * band);
   alpha = fminf(alpha, ALPHA_CAP_F);
-  q.nbig++;  // (also for a slot flagged here: the fix-up recomputes a flagged pixel)
-  q.sbig += (double)soft_sigmoid_accurate(alpha);
+  if (SOFT) {
+    q.nbig++;  // (also for a slot flagged here: the fix-up recomputes a flagged pixel)
+    q.sbig += (double)soft_sigmoid_accurate(alpha);
+  }
   // blend without a branch (most large-path lanes blend): a lane below
   // 1/255 runs it with alpha = 0, i.e. T * 1 and colour + B * 0
   const bool bl = alpha >= ALPHA_MIN_F;
@@ -147,7 +155,11 @@ __device__ __forceinline__ bool fwd_slot(FwdState& q, float p2, float qpos, floa
 // near-singular conic (negative staged opacity), so the power > 0 guard band
 // is tested; batches without one (the common case) skip that test entirely.
 // Returns false once the pixel terminated or was flagged.
-template <bool FRAGILE, bool FULL>
+// SOFT = false (no soft-count output): the far test uses each splat's own
+// cut (D.z / D.w = log2(0.999 / (255 opacity)), clamped to the soft far
+// power): a pair below it has alpha < 1/255 and, without soft counts,
+// contributes nothing -- the same bound the backward's non-soft path uses.
+template <bool FRAGILE, bool FULL, bool SOFT>
 __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sP, const float4* sB, int j0, int jend, int k0,
                                          float fpx, float fpy, float band, float band_t) {
   // FULL: a whole 32-slot bucket, constant trip count (no per-slot bound test)
@@ -164,9 +176,10 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sP, const fl
     const float2 qp = f2_fma(make_float2(D.x, D.y), dyy, f2_mul(make_float2(C.x, C.y), dxx));
     const float2 p2 = f2_fma(make_float2(C.z, C.w), dxy, qp);
     // far (power < -25): soft term S0 only, nothing else
-    if (!(p2.x < FAR_POWER2) && !fwd_slot<FRAGILE>(q, p2.x, qp.x, D.z, sB, j, k0, band, band_t)) return false;
-    if ((FULL || jj + 1 < nj) && !(p2.y < FAR_POWER2) &&
-        !fwd_slot<FRAGILE>(q, p2.y, qp.y, D.w, sB, j + 1, k0, band, band_t))
+    const float cut_x = SOFT ? FAR_POWER2 : D.z, cut_y = SOFT ? FAR_POWER2 : D.w;
+    if (!(p2.x < cut_x) && !fwd_slot<FRAGILE, SOFT>(q, p2.x, qp.x, D.z, sB, j, k0, band, band_t)) return false;
+    if ((FULL || jj + 1 < nj) && !(p2.y < cut_y) &&
+        !fwd_slot<FRAGILE, SOFT>(q, p2.y, qp.y, D.w, sB, j + 1, k0, band, band_t))
       return false;
   }
   return true;
@@ -177,7 +190,7 @@ constexpr int FWD_BATCH = 2 * TILE_PX;
 
 // CK = false: render-only (view_psnr, pipeline.py:180-182): no bucket
 // checkpoints are written (the backward's seeds, ~16 B per live pixel-bucket).
-template <bool CK>
+template <bool CK, bool SOFT>
 __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
@@ -234,8 +247,13 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         P[8] = sc.a2;
         P[10] = sc.b2;
         P[12] = sc.c2;
-        P[14] = __fmul_rn(co.w, 100.f);  // < 0 marks a fragile conic
-        sB[e] = make_float4(col.x, col.y, col.z, fabsf(co.w));
+        if (SOFT) {
+          P[14] = __fmul_rn(co.w, 100.f);  // < 0 marks a fragile conic
+          sB[e] = make_float4(col.x, col.y, col.z, fabsf(co.w));
+        } else {  // the pair's far cut; the staged opacity keeps the fragile sign
+          P[14] = fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / fabsf(co.w)));
+          sB[e] = make_float4(col.x, col.y, col.z, co.w);
+        }
         fragile |= co.w < 0.f;
       }
     }
@@ -252,11 +270,11 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
         const int jend = min(j0 + BUCKET, n);
         bool go;
         if (jend - j0 == BUCKET)
-          go = batch_fragile ? fwd_walk<true, true>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
-                             : fwd_walk<false, true>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
+          go = batch_fragile ? fwd_walk<true, true, SOFT>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, true, SOFT>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
         else
-          go = batch_fragile ? fwd_walk<true, false>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
-                             : fwd_walk<false, false>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
+          go = batch_fragile ? fwd_walk<true, false, SOFT>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t)
+                             : fwd_walk<false, false, SOFT>(q, sP, sB, j0, jend, k0, fpx, fpy, band, band_t);
         if (!go) {
           done = true;
           break;
@@ -277,7 +295,7 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
     a.n_walk[pix] = nwk;
     a.term[pix] = term ? 1 : 0;
     a.hard[pix] = hard;
-    a.soft[pix] = (double)(nwk - nbig) * SOFT_S0 + (sbig + (double)sdev);
+    if (SOFT) a.soft[pix] = (double)(nwk - nbig) * SOFT_S0 + (sbig + (double)sdev);
     a.flagged[pix] = flag ? 1 : 0;
     // every decision before the flagged slot was unambiguous, so the fp32
     // backward handles those slots of a flagged pixel and the fp64 fix-up the rest
@@ -526,7 +544,7 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
       a.n_walk[pix] = r.nw;
       a.term[pix] = (uint8_t)r.term;
       a.hard[pix] = r.hard;
-      a.soft[pix] = r.soft;
+      if (a.soft) a.soft[pix] = r.soft;
       // tile_info.x stays an upper bound of the tile's n_walk (buckets to visit);
       // .z bounds the buckets the backward fix-up visits for this tile
       atomicMax(&a.tile_info[t].x, r.nw);
@@ -1191,10 +1209,17 @@ extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_ga
   if (cudaMemsetAsync(frame.fix_list, 0, FIX_HEAD * sizeof(int32_t), st) != cudaSuccess)
     return check_launch("fix_list reset");
   // frame.ckpt == NULL: render-only (no backward state beyond the per-pixel outputs)
+  // frame.soft_count == NULL: no soft-count output (the caller's loss does not
+  // read it); the walk then culls pairs below 1/255 at the packed far test
   if (frame.ckpt)
-    k_forward<true><<<n_tiles, TILE_PX, 0, st>>>(a);
+    if (frame.soft_count)
+      k_forward<true, true><<<n_tiles, TILE_PX, 0, st>>>(a);
+    else
+      k_forward<true, false><<<n_tiles, TILE_PX, 0, st>>>(a);
+  else if (frame.soft_count)
+    k_forward<false, true><<<n_tiles, TILE_PX, 0, st>>>(a);
   else
-    k_forward<false><<<n_tiles, TILE_PX, 0, st>>>(a);
+    k_forward<false, false><<<n_tiles, TILE_PX, 0, st>>>(a);
   SSR_TRY(check_launch("k_forward"));
   k_forward_fixup<<<num_sms() * 4, 256, 0, st>>>(a);
   return check_launch("k_forward_fixup");

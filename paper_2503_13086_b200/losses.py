@@ -86,10 +86,16 @@ def total_loss(rendered, target, output, weights: LossWeights, values_out: torch
     # an 8-bit target (the reference's image files; value / 255) is read as is
     u8 = target.dtype == torch.uint8
     y = target.to(device=dev).contiguous() if u8 else target.to(device=dev, dtype=torch.float32).contiguous()
-    soft = output.soft_count.to(dtype=torch.float64).contiguous()
+    if output.soft_count is None:
+        # render(soft_count=False): only a loss without the load term can use it
+        if weights.load > 0:
+            raise InvalidParameter("the load-balance term needs soft counts; render with soft_count=True")
+        soft = None
+    else:
+        soft = output.soft_count.to(dtype=torch.float64).contiguous()
     hard = output.hard_count.to(dtype=torch.int32).contiguous()
     d_image = torch.empty_like(x)
-    d_soft = torch.empty(soft.shape, dtype=torch.float32, device=dev)
+    d_soft = None if soft is None else torch.empty(soft.shape, dtype=torch.float32, device=dev)
     if values_out is not None:
         if values_out.device.type != "cpu" or not values_out.is_pinned() or values_out.dtype != torch.float64 \
                 or values_out.numel() < 5 or not values_out.is_contiguous():
@@ -98,9 +104,9 @@ def total_loss(rendered, target, output, weights: LossWeights, values_out: torch
     else:
         vals = torch.empty(5, dtype=torch.float64, device=dev)
     ws = _Workspace.get(w, h, dev)
-    _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), 1 if u8 else 0, soft.data_ptr(), hard.data_ptr(),
+    _lib.call("ssr_loss", w, h, x.data_ptr(), y.data_ptr(), 1 if u8 else 0, _lib.ptr(soft), hard.data_ptr(),
               float(weights.l1),
-              float(weights.ssim), float(weights.load), d_image.data_ptr(), d_soft.data_ptr(), vals.data_ptr(),
+              float(weights.ssim), float(weights.load), d_image.data_ptr(), _lib.ptr(d_soft), vals.data_ptr(),
               ws.data_ptr(), ws.numel(), _lib.stream_ptr())
     ready = None
     if values_out is not None:

@@ -305,7 +305,7 @@ class DeviceSession:
 
     def view_psnr(self, frame) -> float:
         """pipeline.py:180-182."""
-        out = render(self.field, frame, workers=self.cfg.workers, for_backward=False)
+        out = render(self.field, frame, workers=self.cfg.workers, for_backward=False, soft_count=False)
         return psnr(out.image, self._target(frame.image_id))
 
     def _target(self, image_id):

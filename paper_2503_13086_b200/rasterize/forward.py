@@ -29,7 +29,7 @@ class RenderOutput:
     n_walk: torch.Tensor  # (H, W) int32
     terminated: torch.Tensor  # (H, W) uint8
     hard_count: torch.Tensor  # (H, W) int32
-    soft_count: torch.Tensor  # (H, W) float64
+    soft_count: torch.Tensor  # (H, W) float64; None for render(soft_count=False)
     splats: ProjectedSplats
     cam: CameraFrame
     bg: np.ndarray
@@ -53,18 +53,24 @@ class RenderOutput:
         for k in ("image", "t_final", "n_walk", "terminated", "hard_count", "soft_count", "flagged", "tile_info",
                   "ckpt", "fix_list"):
             t = getattr(self, k)
-            setattr(f, k, t.data_ptr() if t.numel() else None)
+            setattr(f, k, t.data_ptr() if t is not None and t.numel() else None)
         return f
 
 
 def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: float = None,
-           band_t: float = None, *, for_backward: bool = True) -> RenderOutput:
+           band_t: float = None, *, for_backward: bool = True, soft_count: bool = True) -> RenderOutput:
     """Render the field from ``cam`` over a constant background colour.
 
     ``for_backward=False`` is the render-only path (view_psnr, pipeline.py:180-182):
     identical outputs, but the bucket checkpoints the backward seeds from are not
     written (~16 B per live pixel-bucket, ~320 MB at 1M Gaussians / 1080p), so the
-    result cannot be passed to ``backward``."""
+    result cannot be passed to ``backward``.
+
+    ``soft_count=False`` skips the soft blend count (``RenderOutput.soft_count``
+    is None): a loss whose load weight is 0 never reads it (losses.py:155-160),
+    and without it the walk culls pairs certain to stay below 1/255 at the
+    packed far test.  Every other output is identical; such a render feeds
+    ``total_loss`` only with ``weights.load == 0``."""
     if workers < 1:
         raise InvalidParameter(f"workers must be >= 1, got {workers}")
     band = GUARD_BAND if band is None else float(band)
@@ -78,7 +84,8 @@ def render(field, cam: CameraFrame, bg=(0.0, 0.0, 0.0), workers: int = 1, band: 
     n_tiles = splats.tiles_x * splats.tiles_y
     e = lambda *s, dt=torch.float32: torch.empty(s, dtype=dt, device=dev)
     image, t_final, n_walk = e(h, w, 3), e(h, w), e(h, w, dt=torch.int32)
-    terminated, hard, soft = e(h, w, dt=torch.uint8), e(h, w, dt=torch.int32), e(h, w, dt=torch.float64)
+    terminated, hard = e(h, w, dt=torch.uint8), e(h, w, dt=torch.int32)
+    soft = e(h, w, dt=torch.float64) if soft_count else None
     flagged, tile_info = e(h, w, dt=torch.uint8), e(n_tiles, 4, dt=torch.int32)
     fix_list = e(int(_lib.load().ssr_fix_list_ints(w, h, n_tiles)), dt=torch.int32)
     project_end(splats, ctx, field)

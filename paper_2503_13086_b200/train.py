@@ -77,7 +77,8 @@ def train_iteration(state: TrainState, cam, target, position_rate: float, bg=(0.
     checks the two agree).  ``fused=False`` goes through FieldGrads exactly like
     the reference's backward + step calls.
     """
-    out = render(state.field, cam, bg=bg)
+    # soft counts only when the objective reads them (load weight > 0)
+    out = render(state.field, cam, bg=bg, soft_count=state.weights.load > 0)
     br = total_loss(out.image, target, out, state.weights)
     if fused:
         backward_and_step(state.field, out, br.d_image, br.d_soft, state.optimizer, position_rate,
@@ -238,7 +239,7 @@ class SemiGlobalBatch:
         grads = self._buffer()
         losses = []
         for i in idx:
-            out = render(f, cams[i], bg=bg)
+            out = render(f, cams[i], bg=bg, soft_count=st.weights.load > 0)
             br = total_loss(out.image, targets[i], out, st.weights)
             backward(f, out, br.d_image, br.d_soft, layout=st.layout, grads=grads, accumulate=True)
             losses.append(br)

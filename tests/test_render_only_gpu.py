@@ -31,3 +31,57 @@ def test_render_only_matches_training_render(cfg, n, w, h):
     g = backward(f, full, torch.full_like(full.image, 1e-3))
     assert bool(torch.isfinite(g.flat).all())
     np.testing.assert_array_less(0.0, float(g.positions.abs().sum()))
+
+
+@pytest.mark.parametrize("cfg,n,w,h", [(1, 30000, 320, 240), (2, 60000, 480, 270)])
+def test_render_without_soft_counts(cfg, n, w, h, oracle_lib):
+    """render(soft_count=False): every output but the soft count identical to
+    the full render and to the oracle; total_loss without the load term gives
+    the same scalars and d_image; a training iteration moves the parameters
+    bit-identically (d_soft is zero either way when the load weight is 0)."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.errors import InvalidParameter
+    from paper_2503_13086_b200.losses import LossWeights, total_loss
+    from paper_2503_13086_b200.optim import FieldOptimizer
+    from paper_2503_13086_b200.rasterize import render
+    from paper_2503_13086_b200.train import TrainState, train_iteration
+    from parity import GRAD_CLASSES, forward_report
+
+    hp = scenes.make_params(cfg, seed=4, n=n)
+    f = GaussianField.from_host(hp)
+    cam = scenes.camera(cfg, view=6, width=w, height=h)
+    full = render(f, cam)
+    lite = render(f, cam, soft_count=False)
+    torch.cuda.synchronize()
+    assert lite.soft_count is None
+    for k in ("image", "t_final", "n_walk", "terminated", "hard_count", "flagged"):
+        assert torch.equal(getattr(full, k), getattr(lite, k)), k
+    ref = oracle_lib.render(oracle_lib.Params(*(getattr(hp, k).astype(np.float64) for k in GRAD_CLASSES)), cam)
+    r = forward_report(full, ref)
+    assert r["image_max_abs"] <= 1e-4 and r["n_walk_mismatch"] == 0 and r["hard_count_mismatch"] == 0, r
+    tgt = torch.rand((h, w, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    bw = LossWeights(l1=1.0, ssim=0.2, load=0.0)
+    a, b = total_loss(full.image, tgt, full, bw), total_loss(lite.image, tgt, lite, bw)
+    assert (a.l1, a.ssim_loss, a.load, a.total) == (b.l1, b.ssim_loss, b.load, b.total)
+    assert torch.equal(a.d_image, b.d_image) and b.d_soft is None and float(a.d_soft.abs().max()) == 0.0
+    with pytest.raises(InvalidParameter):
+        total_loss(lite.image, tgt, lite, LossWeights())
+    flats = []
+    for soft in (True, False):
+        g = GaussianField.from_host(hp)
+        st = TrainState(field=g, optimizer=FieldOptimizer(g, 3.0), weights=bw, densify_enabled=False)
+        for _ in range(3):
+            if soft:  # the reference's call sequence: soft counts computed, d_soft all zero
+                out = render(g, cam)
+                br = total_loss(out.image, tgt, out, bw)
+                from paper_2503_13086_b200.rasterize.backward import backward_and_step
+
+                backward_and_step(g, out, br.d_image, br.d_soft, st.optimizer, 1e-4, stats=st.stats)
+            else:
+                train_iteration(st, cam, tgt, 1e-4)
+        torch.cuda.synchronize()
+        flats.append((g.flat.clone(), st.optimizer.m.clone(), st.stats.clone()))
+    for x, y in zip(*flats):
+        assert torch.equal(x, y)
