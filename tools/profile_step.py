@@ -24,8 +24,8 @@ f = GaussianField.from_host(hp)
 opt = FieldOptimizer(f, scene_extent=6.6)
 target = torch.full((cam.height, cam.width, 3), 0.5, device="cuda")
 for _ in range(iters):
-    out = render(f, cam)
     w = LossWeights() if os.environ.get("SSR_WEIGHTS") == "paper" else LossWeights(l1=1.0, ssim=0.2, load=0.0)
+    out = render(f, cam, soft_count=w.load > 0)  # as train.train_iteration does
     br = total_loss(out.image, target, out, w)
     if os.environ.get("SSR_FUSED") == "1":
         from paper_2503_13086_b200.rasterize.backward import backward_and_step
