@@ -560,11 +560,15 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   float* shrow = sh + ii * W;
   float* grow = grads + 11 * ns + ii * W;
 
-  // the lane's coefficients: c[ch][j] = sh[ch*K + q*KL + j]
+  // the lane's coefficients: c[ch][j] = sh[ch*K + q*KL + j] (an invisible
+  // row's gradient is zero: no coefficient or position is read for it)
   float cf[3][KL];
 #pragma unroll
   for (int ch = 0; ch < 3; ch++) {
-    if (VEC) {
+    if (!vis) {
+#pragma unroll
+      for (int j = 0; j < KL; j++) cf[ch][j] = 0.f;
+    } else if (VEC) {
       const float4 v4 = *reinterpret_cast<const float4*>(shrow + ch * K + q * 4);
       cf[ch][0] = v4.x;
       cf[ch][1] = v4.y;
@@ -579,8 +583,8 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
     }
   }
   // direction (sh.py:114-124), recomputed by each lane
-  const float ox = pos[ii * 3] - cam.center[0], oy = pos[ii * 3 + 1] - cam.center[1],
-              oz = pos[ii * 3 + 2] - cam.center[2];
+  const float ox = vis ? pos[ii * 3] - cam.center[0] : 1.f, oy = vis ? pos[ii * 3 + 1] - cam.center[1] : 0.f,
+              oz = vis ? pos[ii * 3 + 2] - cam.center[2] : 0.f;
   const float r = sqrtf(ox * ox + oy * oy + oz * oz);
   const float rs = fmaxf(r, 1e-12f);
   const float irs = 1.f / rs;
@@ -624,7 +628,9 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   }
   const float radial = gd[0] * dx + gd[1] * dy + gd[2] * dz;
   const float dpos_sh[3] = {(gd[0] - radial * dx) * irs, (gd[1] - radial * dy) * irs, (gd[2] - radial * dz) * irs};
-  if (!row_ok) return;
+  // accumulating (view batches): an invisible row adds exact zeros -- skip
+  // its read-modify-write of the gradient rows
+  if (!row_ok || (accumulate && !vis)) return;
   if (q == 0 && vis) {
     float* g_pos = grads + i * 3;
 #pragma unroll
