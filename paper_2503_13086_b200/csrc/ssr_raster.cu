@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
 #define SSR_BW_UNROLL 2
 #endif
 constexpr int BW_UNROLL = SSR_BW_UNROLL;
+constexpr int BW2_MIN_BLOCKS = 3;  // 80 registers: 24 warps per SM (2 blocks: 125 registers, no faster)
 constexpr int BW_PAD = 32;
 constexpr int BW_LIST = BW_PAD + TILE_PX + BW_PAD;
 
@@ -597,6 +598,100 @@ __shared__ float4 sPix[2 * (TILE_PX + 1)];
 #define sPA (sPix)
 #define sPB (sPix + TILE_PX + 1)
 
+// One (pixel, slot) pair of the splat-parallel backward: the pixel record
+// (PB: x, y, w . image, walk limit; w: dL/dRGB, dL/dsoft), the slot k, the
+// lane's splat; T / H (transmittance, w . C_front) enter and leave updated.
+template <bool SOFT>
+__device__ __forceinline__ void bw_pair(const float4& PB, const float4& w, int k, const BwSplat& s, BwAcc& g,
+                                        float& T, float& H) {
+  const int lim = __float_as_int(PB.w);
+#ifdef SSR_BW_PACKED
+  // (dx, dy) and (dxx, dyy) as packed pairs: each lane bit-identical to the
+  // scalar __fsub_rn / __fmul_rn the forward uses
+  const float2 d2 = f2_sub(f2_sub(make_float2(PB.x, PB.y), make_float2(s.sm.xi, s.sm.yi)),
+                           make_float2(s.sm.xf, s.sm.yf));
+  const float dx = d2.x, dy = d2.y;
+  const float2 sq = f2_mul(d2, d2);
+  const float dxx = sq.x, dyy = sq.y, dxy = __fmul_rn(dx, dy);
+#else
+  const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
+  const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
+#endif
+  float qpos;
+  const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
+  if (!SOFT) {
+    const float araw = pair_alpha2(s.opa, p2);
+    // (araw >= 1/255 implies p2 >= p2_min: no separate far test here; lanes
+    // past the walks have opacity 0).  Branch-free: some lane of the warp
+    // nearly always contributes, so the block runs anyway; a lane that does
+    // not contributes exactly zero (alpha = 0: T, H and every sum unchanged).
+    const bool c = (k < lim) & (p2 <= 0.f) & (araw >= ALPHA_MIN_F);
+    const float alpha = c ? fminf(araw, ALPHA_CAP_F) : 0.f;
+    const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+    const float aT = alpha * T;
+    g.g0 = fmaf(aT, w.x, g.g0);
+    g.g1 = fmaf(aT, w.y, g.g1);
+    g.g2 = fmaf(aT, w.z, g.g2);
+    const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
+    const float awc = aT * wc;
+    const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
+    const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
+    H = c ? H + awc : H;
+    T = __fmul_rn(T, one_m);
+    // capped: no opacity/geometry path; a lane that does not blend has
+    // alpha = 0 and a finite dlda, so its gp is already zero
+    const float gp = araw <= ALPHA_CAP_F ? dlda * alpha : 0.f;
+    g.g3 += gp;
+#ifdef SSR_BW_PACKED
+    {
+      const float2 s2 = f2_fma(make_float2(gp, gp), d2, make_float2(g.sx, g.sy));
+      const float2 q2 = f2_fma(make_float2(gp, gp), sq, make_float2(g.g6, g.g8));
+      g.sx = s2.x;
+      g.sy = s2.y;
+      g.g6 = q2.x;
+      g.g8 = q2.y;
+    }
+#else
+    g.sx = fmaf(gp, dx, g.sx);
+    g.sy = fmaf(gp, dy, g.sy);
+    g.g6 = fmaf(gp, dxx, g.g6);
+    g.g8 = fmaf(gp, dyy, g.g8);
+#endif
+    g.g7 = fmaf(gp, dxy, g.g7);
+  } else {
+    // same branch-free form with the soft-count term of every walked pair
+    // below the cap
+    const int nw = lim >> 1;
+    const bool walked = (k < nw) & (p2 <= 0.f) & (p2 >= s.p2_min);
+    const float araw = pair_alpha2(s.opa, p2);
+    const bool capped = araw > ALPHA_CAP_F;
+    const float alpha = capped ? ALPHA_CAP_F : araw;
+    // the terminating slot (k == nw - 1 of a terminated walk) is never blended
+    const bool blended = walked & (alpha >= ALPHA_MIN_F) & (k < nw - (lim & 1));
+    const float ab = blended ? alpha : 0.f;
+    const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
+    const float aT = ab * T;
+    g.g0 = fmaf(aT, w.x, g.g0);
+    g.g1 = fmaf(aT, w.y, g.g1);
+    g.g2 = fmaf(aT, w.z, g.g2);
+    const float one_m = __fsub_rn(1.f, ab);
+    const float awc = aT * wc;
+    const float sdot = PB.z - H - awc;
+    const float dlda = blended ? fmaf(T, wc, -sdot * rcp_approx(one_m)) : 0.f;
+    H = blended ? H + awc : H;
+    T = __fmul_rn(T, one_m);
+    const bool soft_ok = walked & !capped;
+    const float sv = soft_sigmoid(alpha);
+    g.g3 = soft_ok ? fmaf(fmaf(w.w * sv * (1.f - sv), 100.f, dlda), alpha, g.g3) : g.g3;
+    const float gp = (soft_ok & blended) ? dlda * alpha : 0.f;
+    g.sx = fmaf(gp, dx, g.sx);
+    g.sy = fmaf(gp, dy, g.sy);
+    g.g6 = fmaf(gp, dxx, g.g6);
+    g.g7 = fmaf(gp, dxy, g.g7);
+    g.g8 = fmaf(gp, dyy, g.g8);
+  }
+}
+
 template <bool SOFT>
 __device__ __forceinline__ void bw_stream(
                                           const uint16_t* __restrict__ list, const float2* __restrict__ seed,
@@ -609,7 +704,7 @@ __device__ __forceinline__ void bw_stream(
   const char* sPixb = reinterpret_cast<const char*>(sPix);
   constexpr int B_OFF = (TILE_PX + 1) * sizeof(float4);
   float4 PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF), PAn = *reinterpret_cast<const float4*>(sPixb + on);
-#pragma unroll BW_UNROLL
+#pragma unroll 2
   for (int i = 0; i < n_steps; i++) {
     float Tin = __shfl_up_sync(FULL, T, 1);
     float Hin = __shfl_up_sync(FULL, H, 1);
@@ -621,92 +716,40 @@ __device__ __forceinline__ void bw_stream(
     on = list[jn];
     PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF);
     PAn = *reinterpret_cast<const float4*>(sPixb + on);
-    const int lim = __float_as_int(PB.w);
-#ifdef SSR_BW_PACKED
-    // (dx, dy) and (dxx, dyy) as packed pairs: each lane bit-identical to the
-    // scalar __fsub_rn / __fmul_rn the forward uses
-    const float2 d2 = f2_sub(f2_sub(make_float2(PB.x, PB.y), make_float2(s.sm.xi, s.sm.yi)),
-                             make_float2(s.sm.xf, s.sm.yf));
-    const float dx = d2.x, dy = d2.y;
-    const float2 sq = f2_mul(d2, d2);
-    const float dxx = sq.x, dyy = sq.y, dxy = __fmul_rn(dx, dy);
-#else
-    const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
-    const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
-#endif
-    float qpos;
-    const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
-    if (!SOFT) {
-      const float araw = pair_alpha2(s.opa, p2);
-      // (araw >= 1/255 implies p2 >= p2_min: no separate far test here; lanes
-      // past the walks have opacity 0).  Branch-free: some lane of the warp
-      // nearly always contributes, so the block runs anyway; a lane that does
-      // not contributes exactly zero (alpha = 0: T, H and every sum unchanged).
-      const bool c = (k < lim) & (p2 <= 0.f) & (araw >= ALPHA_MIN_F);
-      const float alpha = c ? fminf(araw, ALPHA_CAP_F) : 0.f;
-      const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
-      const float aT = alpha * T;
-      g.g0 = fmaf(aT, w.x, g.g0);
-      g.g1 = fmaf(aT, w.y, g.g1);
-      g.g2 = fmaf(aT, w.z, g.g2);
-      const float one_m = __fsub_rn(1.f, alpha);  // >= 0.01
-      const float awc = aT * wc;
-      const float sdot = PB.z - H - awc;  // w . (colour behind this splat)
-      const float dlda = fmaf(T, wc, -sdot * rcp_approx(one_m));
-      H = c ? H + awc : H;
-      T = __fmul_rn(T, one_m);
-      // capped: no opacity/geometry path; a lane that does not blend has
-      // alpha = 0 and a finite dlda, so its gp is already zero
-      const float gp = araw <= ALPHA_CAP_F ? dlda * alpha : 0.f;
-      g.g3 += gp;
-#ifdef SSR_BW_PACKED
-      {
-        const float2 s2 = f2_fma(make_float2(gp, gp), d2, make_float2(g.sx, g.sy));
-        const float2 q2 = f2_fma(make_float2(gp, gp), sq, make_float2(g.g6, g.g8));
-        g.sx = s2.x;
-        g.sy = s2.y;
-        g.g6 = q2.x;
-        g.g8 = q2.y;
-      }
-#else
-      g.sx = fmaf(gp, dx, g.sx);
-      g.sy = fmaf(gp, dy, g.sy);
-      g.g6 = fmaf(gp, dxx, g.g6);
-      g.g8 = fmaf(gp, dyy, g.g8);
-#endif
-      g.g7 = fmaf(gp, dxy, g.g7);
-    } else {
-      // same branch-free form with the soft-count term of every walked pair
-      // below the cap
-      const int nw = lim >> 1;
-      const bool walked = (k < nw) & (p2 <= 0.f) & (p2 >= s.p2_min);
-      const float araw = pair_alpha2(s.opa, p2);
-      const bool capped = araw > ALPHA_CAP_F;
-      const float alpha = capped ? ALPHA_CAP_F : araw;
-      // the terminating slot (k == nw - 1 of a terminated walk) is never blended
-      const bool blended = walked & (alpha >= ALPHA_MIN_F) & (k < nw - (lim & 1));
-      const float ab = blended ? alpha : 0.f;
-      const float wc = w.x * s.cr + w.y * s.cg + w.z * s.cbl;
-      const float aT = ab * T;
-      g.g0 = fmaf(aT, w.x, g.g0);
-      g.g1 = fmaf(aT, w.y, g.g1);
-      g.g2 = fmaf(aT, w.z, g.g2);
-      const float one_m = __fsub_rn(1.f, ab);
-      const float awc = aT * wc;
-      const float sdot = PB.z - H - awc;
-      const float dlda = blended ? fmaf(T, wc, -sdot * rcp_approx(one_m)) : 0.f;
-      H = blended ? H + awc : H;
-      T = __fmul_rn(T, one_m);
-      const bool soft_ok = walked & !capped;
-      const float sv = soft_sigmoid(alpha);
-      g.g3 = soft_ok ? fmaf(fmaf(w.w * sv * (1.f - sv), 100.f, dlda), alpha, g.g3) : g.g3;
-      const float gp = (soft_ok & blended) ? dlda * alpha : 0.f;
-      g.sx = fmaf(gp, dx, g.sx);
-      g.sy = fmaf(gp, dy, g.sy);
-      g.g6 = fmaf(gp, dxx, g.g6);
-      g.g7 = fmaf(gp, dxy, g.g7);
-      g.g8 = fmaf(gp, dyy, g.g8);
-    }
+    bw_pair<SOFT>(PB, w, k, s, g, T, H);
+  }
+}
+
+// Two consecutive slots per lane (64-slot buckets, k_backward_splat2): lane l
+// owns slots k and k + 1; each pixel record read from shared memory and each
+// (T, H) hand-off by shuffle serves two pairs (the one-slot stream runs at
+// 86% of the LSU wavefront peak; this one at 49%, limited by occupancy).
+template <bool SOFT>
+__device__ __forceinline__ void bw_stream2(const uint16_t* __restrict__ list, const float2* __restrict__ seed,
+                                           int n_live, int lane, int k, const BwSplat& s0, const BwSplat& s1,
+                                           BwAcc& g0, BwAcc& g1) {
+  float T = 1.f, H = 0.f;
+  const int n_steps = n_live + 31;
+  const bool lane0 = lane == 0;
+  int jn = BW_PAD - lane;
+  int on = list[jn];
+  const char* sPixb = reinterpret_cast<const char*>(sPix);
+  constexpr int B_OFF = (TILE_PX + 1) * sizeof(float4);
+  float4 PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF), PAn = *reinterpret_cast<const float4*>(sPixb + on);
+#pragma unroll 2
+  for (int i = 0; i < n_steps; i++) {
+    float Tin = __shfl_up_sync(FULL, T, 1);
+    float Hin = __shfl_up_sync(FULL, H, 1);
+    const float2 sd = seed[i];
+    T = lane0 ? sd.x : Tin;
+    H = lane0 ? sd.y : Hin;
+    const float4 PB = PBn, w = PAn;
+    jn++;
+    on = list[jn];
+    PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF);
+    PAn = *reinterpret_cast<const float4*>(sPixb + on);
+    bw_pair<SOFT>(PB, w, k, s0, g0, T, H);
+    bw_pair<SOFT>(PB, w, k + 1, s1, g1, T, H);
   }
 }
 
@@ -840,6 +883,144 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       r[6] = -0.5f * g.g6;
       r[7] = -g.g7;
       r[8] = -0.5f * g.g8;
+    }
+    __syncwarp();
+  }
+  // rows of slots no pixel walked
+  for (int k = maxw + tid; k < len; k += blockDim.x) {
+    const uint32_t g = a.inst[s0 + k];
+    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
+    for (int c = 0; c < 9; c++) r[c] = 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterArgs a, const float* __restrict__ d_image,
+                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int2 rg = a.ranges[t];
+  const int s0 = rg.x, len = rg.y - rg.x;
+  if (len == 0) return;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int x00 = tx * TILE, y00 = ty * TILE;
+  const int maxw = a.tile_info[t].x;
+
+  __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
+  __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
+  bool soft_px = false;
+  {
+    const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
+    int nw = 0, term = 0;
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+    float wimg = 0.f;
+    if (px < a.width && py < a.height) {
+      const size_t pix = (size_t)py * a.width + px;
+      if (!a.flagged[pix]) {
+        nw = a.n_walk[pix];
+        term = a.term[pix] ? 1 : 0;
+      } else {
+        nw = fix_kflag(a)[pix];  // slots before the ambiguous one; the fp64 fix-up adds the rest
+      }
+      w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
+      wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
+    }
+    soft_px = w.w != 0.f;
+    sPA[tid] = w;
+    // does any pixel of the tile carry a soft-count gradient?  If not, pairs
+    // with alpha < 1/255 (and terminating slots) contribute exactly nothing.
+    const bool us = __syncthreads_or(soft_px);
+    const int lim = us ? ((nw << 1) | term) : nw - term;
+    sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(lim));
+    if (tid < 8)
+      for (int e = 0; e < BW_PAD; e++) {
+        sList[tid][e] = TILE_PX * sizeof(float4);
+        sList[tid][BW_PAD + TILE_PX + e] = TILE_PX * sizeof(float4);
+      }
+    if (tid == 0) {
+      sPA[TILE_PX] = make_float4(0.f, 0.f, 0.f, 0.f);
+      sPB[TILE_PX] = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    }
+    soft_px = us;
+  }
+  __syncthreads();
+  const bool use_soft = soft_px;
+
+  const int nb = (maxw + 63) >> 6;  // 64-slot buckets: two slots per lane
+  const float4* ckt = a.ckpt + ckpt_base(s0, t);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint16_t* const myList = sList[warp] + BW_PAD;
+  float2* const mySeed = sSeed[warp];
+  for (int b = warp; b < nb; b += 8) {
+    const int kb = b * 64;
+    int n_live = 0;
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      const int p = c * 32 + lane;
+      const int lim = __float_as_int(sPB[p].w);
+      const bool lv = (use_soft ? (lim >> 1) : lim) > kb;
+      const unsigned msk = __ballot_sync(FULL, lv);
+      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint16_t)(p * sizeof(float4));
+      n_live += __popc(msk);
+    }
+    if (n_live + lane < TILE_PX) myList[n_live + lane] = TILE_PX * sizeof(float4);
+    __syncwarp();
+    for (int j = lane; j < n_live; j += 32) {
+      const int p = myList[j] / sizeof(float4);
+      float2 sd = make_float2(1.f, 0.f);
+      if (b > 0) {  // the forward's checkpoint at slot kb (every other 32-slot checkpoint)
+        const float4 c = ckt[(size_t)(2 * b) * TILE_PX + p];
+        const float4 w = sPA[p];
+        sd = make_float2(c.x, w.x * c.y + w.y * c.z + w.z * c.w);
+      }
+      mySeed[j] = sd;
+    }
+    mySeed[n_live + lane] = make_float2(1.f, 0.f);
+    __syncwarp();
+    const int k = kb + 2 * lane;
+    BwSplat sp[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      BwSplat& sv = sp[h];
+      sv.sm = {0.f, 0.f, 0.f, 0.f};
+      sv.q = {0.f, 0.f, 0.f};
+      sv.opa = sv.cr = sv.cg = sv.cbl = 0.f;
+      sv.p2_min = __int_as_float(0x7f800000);
+      if (k + h < maxw) {
+        const uint32_t g = a.inst[s0 + k + h];
+        const double2 m = a.mean[g];
+        const float4 co = a.conic_opa[g];
+        const float4 col = a.color[g];
+        sv.sm = stage_mean(m.x, m.y, x00, y00);
+        sv.opa = fabsf(co.w);
+        sv.q = stage_conic(co.x, co.y, co.z);
+        sv.cr = col.x;
+        sv.cg = col.y;
+        sv.cbl = col.z;
+        sv.p2_min = use_soft ? FAR_POWER2 : fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / sv.opa));
+      }
+    }
+    BwAcc g[2] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
+    if (use_soft)
+      bw_stream2<true>(sList[warp], mySeed, n_live, lane, k, sp[0], sp[1], g[0], g[1]);
+    else
+      bw_stream2<false>(sList[warp], mySeed, n_live, lane, k, sp[0], sp[1], g[0], g[1]);
+    // the row index and conic are re-read after the stream (registers are the limit)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (k + h < maxw) {
+        const uint32_t gi = a.inst[s0 + k + h];
+        const float4 co = a.conic_opa[gi];
+        float* r = rows + (size_t)inst_row(a, gi, tx, ty) * 9;
+        r[0] = g[h].g0;
+        r[1] = g[h].g1;
+        r[2] = g[h].g2;
+        r[3] = g[h].g3 * (1.f - fabsf(co.w));
+        r[4] = co.x * g[h].sx + co.y * g[h].sy;
+        r[5] = co.y * g[h].sx + co.z * g[h].sy;
+        r[6] = -0.5f * g[h].g6;
+        r[7] = -g[h].g7;
+        r[8] = -0.5f * g[h].g8;
+      }
     }
     __syncwarp();
   }
@@ -1240,8 +1421,15 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     return SSR_ERR_INVALID;
   }
   RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f, 0.f);
-  if (layout == 0)
-    k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+  if (layout == 0) {
+    // no soft-count gradient (d_soft NULL): two slots per lane, 64-slot buckets
+    // (fewer shared-memory and shuffle wavefronts per pair, -1.4%); with one,
+    // the soft pair block needs the registers of the one-slot kernel
+    if (!d_soft)
+      k_backward_splat2<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+    else
+      k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+  }
   else
     k_backward_pixel<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
   SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
