@@ -37,8 +37,9 @@ def test_render_only_matches_training_render(cfg, n, w, h):
 def test_render_without_soft_counts(cfg, n, w, h, oracle_lib):
     """render(soft_count=False): every output but the soft count identical to
     the full render and to the oracle; total_loss without the load term gives
-    the same scalars and d_image; a training iteration moves the parameters
-    bit-identically (d_soft is zero either way when the load weight is 0)."""
+    the same scalars and d_image; the gradients agree to rounding (d_soft is
+    zero either way when the load weight is 0; without a d_soft the two-slot
+    backward runs, whose rounding of w . C_front differs)."""
     import torch
 
     from paper_2503_13086_b200 import GaussianField, scenes
@@ -68,23 +69,25 @@ def test_render_without_soft_counts(cfg, n, w, h, oracle_lib):
     assert torch.equal(a.d_image, b.d_image) and b.d_soft is None and float(a.d_soft.abs().max()) == 0.0
     with pytest.raises(InvalidParameter):
         total_loss(lite.image, tgt, lite, LossWeights())
-    flats = []
-    for soft in (True, False):
-        g = GaussianField.from_host(hp)
-        st = TrainState(field=g, optimizer=FieldOptimizer(g, 3.0), weights=bw, densify_enabled=False)
-        for _ in range(3):
-            if soft:  # the reference's call sequence: soft counts computed, d_soft all zero
-                out = render(g, cam)
-                br = total_loss(out.image, tgt, out, bw)
-                from paper_2503_13086_b200.rasterize.backward import backward_and_step
+    # the training iteration itself runs without soft counts (load weight 0)
+    st = TrainState(field=GaussianField.from_host(hp), optimizer=None, weights=bw, densify_enabled=False)
+    st.optimizer = FieldOptimizer(st.field, 3.0)
+    assert np.isfinite(train_iteration(st, cam, tgt, 1e-4).total)
+    # d_soft all zero (one-slot backward) vs d_soft None (two-slot backward):
+    # the same decisions and contributions, summed with a different rounding of
+    # the carried w . C_front (Adam's per-element normalisation would amplify
+    # that on near-zero gradients, so the gradients are compared, not trajectories)
+    from paper_2503_13086_b200.rasterize import backward
 
-                backward_and_step(g, out, br.d_image, br.d_soft, st.optimizer, 1e-4, stats=st.stats)
-            else:
-                train_iteration(st, cam, tgt, 1e-4)
-        torch.cuda.synchronize()
-        flats.append((g.flat.clone(), st.optimizer.m.clone(), st.stats.clone()))
-    for x, y in zip(*flats):
-        assert torch.equal(x, y)
+    f2 = GaussianField.from_host(hp)
+    o2 = render(f2, cam, soft_count=False)
+    d = torch.randn(o2.image.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(5)) * 1e-3
+    g1 = backward(f2, o2, d, torch.zeros(o2.image.shape[:2], device="cuda"))  # one-slot kernel
+    g2 = backward(f2, o2, d, None)  # two-slot kernel
+    for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh", "screen_norms"):
+        a1, a2 = getattr(g1, k).double(), getattr(g2, k).double()
+        assert float((a1 - a2).norm() / a1.norm().clamp_min(1e-30)) <= 1e-5, k
+    assert torch.equal(g1.visible, g2.visible)
 
 
 def _same_backward(f, full, lite):
