@@ -140,7 +140,9 @@ int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tiles_y, ssr_sp
  * instances (ssr_bin_workspace(capacity, ...)).  Returns SSR_ERR_CAPACITY
  * without launching when M > capacity (the caller then sizes the buffers for
  * *m_out and calls ssr_bin_tiles).  Lets the binning start without a round
- * trip through the host language after the path's one synchronisation. */
+ * trip through the host language after the path's one synchronisation.
+ * `stream` must be the stream of the preceding ssr_scan_tiles: the binning reads
+ * its depth order and offsets, ordered after them by that stream only. */
 int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y, ssr_splats splats,
                            const uint64_t* total_dev, int64_t* m_out, uint32_t* inst_gauss, int32_t* tile_ranges,
                            void* workspace, int64_t workspace_bytes, void* stream);
