@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_up(int64_t n, int shift, c
                                                          const double* __restrict__ depth,
                                                          uint32_t* __restrict__ counts,
                                                          uint32_t* __restrict__ hist, int n_ctas) {
+  griddep_wait();
   __shared__ uint32_t s_hist[RX_WARPS][256];  // one histogram per warp: no cross-warp contention
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < RX_WARPS * 256; i += RX_THREADS) (&s_hist[0][0])[i] = 0u;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_up(int64_t n, int shift, c
 __global__ void __launch_bounds__(RX_THREADS) k_digit_scan(const uint32_t* __restrict__ counts,
                                                            const uint32_t* __restrict__ hist, int n_ctas,
                                                            uint32_t* __restrict__ offsets) {
+  griddep_wait();
   __shared__ uint32_t s_red[RX_WARPS];
   __shared__ uint32_t s_base;
   const int d = blockIdx.x;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2) k_radix_down(
     int64_t n, int shift, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     const uint32_t* __restrict__ tiles, const double* __restrict__ depth, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ offsets, int n_ctas) {
+  griddep_wait();
   __shared__ uint32_t s_keys[RX_TILE];
   __shared__ uint32_t s_vals[RX_TILE];
   __shared__ uint16_t s_whist[RX_WARPS][256];  // per-warp digit counts, then warp offsets (< 4096)
@@ -276,6 +279,7 @@ __device__ __noinline__ void tiefix_long_run(int64_t s, int64_t n, uint32_t key,
 __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t* __restrict__ keys,
                                                       uint32_t* __restrict__ order, const double* __restrict__ depth,
                                                       const uint32_t* __restrict__ tiles, uint32_t* __restrict__ cnt) {
+  griddep_wait();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t key = keys[s];
@@ -335,6 +339,7 @@ __global__ void __launch_bounds__(256) k_depth_tiefix(int64_t n, const uint32_t*
 __global__ void __launch_bounds__(RX_THREADS) k_tile_sums(int64_t n, const uint32_t* __restrict__ src,
                                                           uint64_t* __restrict__ sums,
                                                           unsigned long long* __restrict__ total) {
+  griddep_wait();
   __shared__ uint64_t s_red[RX_WARPS];
   const int64_t base = (int64_t)blockIdx.x * RX_TILE + threadIdx.x;
   uint64_t v = 0;
@@ -361,6 +366,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_scan2(int64_t n, const uint32_t*
                                                       const uint32_t* __restrict__ tiles,
                                                       uint32_t* __restrict__ offset, uint32_t* __restrict__ row_offset,
                                                       const uint64_t* __restrict__ sums, int n_per) {
+  griddep_wait();
   __shared__ uint64_t s_red[RX_WARPS];
   __shared__ uint64_t s_pre[RX_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -430,6 +436,7 @@ __global__ void __launch_bounds__(256) k_duplicate(int64_t n, int tiles_x, const
                                                    const uint32_t* __restrict__ offset, const int4* __restrict__ rect,
                                                    const uint32_t* __restrict__ order, uint32_t* __restrict__ keys,
                                                    uint32_t* __restrict__ vals) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   {
     const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -511,6 +518,7 @@ constexpr int RANGE_KEYS = 8;
 
 __global__ void __launch_bounds__(256) k_ranges(int64_t m, int n_tiles, const uint32_t* __restrict__ keys,
                                                 int32_t* __restrict__ ranges) {
+  griddep_wait();
   const int64_t s0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RANGE_KEYS;
   if (s0 >= m) return;
   int prev = s0 > 0 ? (int)keys[s0 - 1] : -1;
@@ -587,13 +595,12 @@ static int radix_pass(int64_t n, int shift, const uint32_t* keys_in, const uint3
                       const double* depth, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts,
                       uint32_t* offsets, uint32_t* hist, cudaStream_t st) {
   const int ctas = (int)rx_ctas(n);
-  k_radix_up<MODE><<<ctas, RX_THREADS, 0, st>>>(n, shift, keys_in, tiles, depth, counts, hist, ctas);
-  SSR_TRY(check_launch("k_radix_up"));
-  k_digit_scan<<<256, RX_THREADS, 0, st>>>(counts, hist, ctas, offsets);
-  SSR_TRY(check_launch("k_digit_scan"));
-  k_radix_down<MODE><<<ctas, RX_THREADS, 0, st>>>(n, shift, keys_in, vals_in, tiles, depth, keys_out, vals_out,
-                                                  offsets, ctas);
-  return check_launch("k_radix_down");
+  SSR_TRY(launch_pdl("k_radix_up", k_radix_up<MODE>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in, tiles,
+                     depth, counts, hist, ctas));
+  SSR_TRY(launch_pdl("k_digit_scan", k_digit_scan, dim3(256), dim3(RX_THREADS), 0, st, (const uint32_t*)counts,
+                     (const uint32_t*)hist, ctas, offsets));
+  return launch_pdl("k_radix_down", k_radix_down<MODE>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in,
+                    vals_in, tiles, depth, keys_out, vals_out, (const uint32_t*)offsets, ctas);
 }
 
 // scan workspace: [zeroed: hist 3 x 256 u32] [counts 256 x ctas | offsets 256 x ctas u32 | sums 2 x ctas u64]
@@ -671,14 +678,15 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   uint32_t* vals_a = (uint32_t*)(w + L.vals_a);
   uint32_t* keys_b = (uint32_t*)(w + L.keys_b);
   uint32_t* cnt = (uint32_t*)(w + L.cnt);
-  SSR_TRY(check_cuda(cudaMemsetAsync(w, 0, L.zero_bytes, st), "scan workspace memset"));
-  SSR_TRY(check_cuda(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), st), "total memset"));
+  SSR_TRY(launch_pdl("scan workspace zero", k_zero_words, dim3(1), dim3(256), 0, st, (uint32_t*)w,
+                     (int64_t)(L.zero_bytes / 4)));
+  SSR_TRY(launch_pdl("total zero", k_zero_words, dim3(1), dim3(32), 0, st, (uint32_t*)total_dev, (int64_t)2));
   const int ctas = (int)L.ctas;
   // M first (field-row tile sums, summed into *total_dev), then its copy to
   // the host and an event: the host waits for M (ssr_bin_tiles_capacity) while
   // the device runs the depth sort queued behind the event
-  k_tile_sums<<<ctas, RX_THREADS, 0, st>>>(n, splats.tiles, sums + ctas, (unsigned long long*)total_dev);
-  SSR_TRY(check_launch("k_tile_sums rows"));
+  SSR_TRY(launch_pdl("k_tile_sums rows", k_tile_sums, dim3(ctas), dim3(RX_THREADS), 0, st, n,
+                     (const uint32_t*)splats.tiles, sums + ctas, (unsigned long long*)total_dev));
   SSR_TRY(arm_pending_total(total_dev, st));
   // pass 0: keys from (tiles, depth) -> (keys_a, vals_a); pass 1 -> (keys_b, cnt as scratch);
   // pass 2 -> (keys_a, depth_order); the tie-fix then fixes depth_order in place and fills cnt
@@ -687,14 +695,14 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   SSR_TRY(radix_pass<0>(n, 8, keys_a, vals_a, nullptr, nullptr, keys_b, cnt, counts, offsets, hist + 256, st));
   SSR_TRY(radix_pass<0>(n, 16, keys_b, cnt, nullptr, nullptr, keys_a, splats.depth_order, counts, offsets,
                         hist + 512, st));
-  k_depth_tiefix<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, keys_a, splats.depth_order, splats.depth,
-                                                              splats.tiles, cnt);
-  SSR_TRY(check_launch("k_depth_tiefix"));
-  k_tile_sums<<<ctas, RX_THREADS, 0, st>>>(n, cnt, sums, nullptr);
-  SSR_TRY(check_launch("k_tile_sums depth"));
-  k_scan2<<<2 * ctas, RX_THREADS, 0, st>>>(n, cnt, splats.depth_order, splats.tiles, splats.offset,
-                                           splats.row_offset, sums, ctas);
-  return check_launch("k_scan2");
+  SSR_TRY(launch_pdl("k_depth_tiefix", k_depth_tiefix, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
+                     (const uint32_t*)keys_a, splats.depth_order, (const double*)splats.depth,
+                     (const uint32_t*)splats.tiles, cnt));
+  SSR_TRY(launch_pdl("k_tile_sums depth", k_tile_sums, dim3(ctas), dim3(RX_THREADS), 0, st, n, (const uint32_t*)cnt,
+                     sums, (unsigned long long*)nullptr));
+  return launch_pdl("k_scan2", k_scan2, dim3(2 * ctas), dim3(RX_THREADS), 0, st, n, (const uint32_t*)cnt,
+                    (const uint32_t*)splats.depth_order, (const uint32_t*)splats.tiles, splats.offset,
+                    splats.row_offset, (const uint64_t*)sums, ctas);
 }
 
 extern "C" int ssr_bin_workspace(int64_t m, int32_t n_tiles, int64_t* bytes) {
@@ -736,17 +744,17 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   uint32_t* vals_a = (uint32_t*)(w + L.vals_a);
   uint32_t* keys_b = (uint32_t*)(w + L.keys_b);
   uint32_t* vals_b = (uint32_t*)(w + L.vals_b);
-  SSR_TRY(check_cuda(cudaMemsetAsync(w, 0, L.zero_bytes, st), "bin workspace memset"));
-  k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, tiles_x, splats.tiles, splats.offset,
-                                                           (const int4*)splats.rect, splats.depth_order, keys_a,
-                                                           vals_a);
-  SSR_TRY(check_launch("k_duplicate"));
+  SSR_TRY(launch_pdl("bin workspace zero", k_zero_words, dim3(1), dim3(256), 0, st, (uint32_t*)w,
+                     (int64_t)(L.zero_bytes / 4)));
+  SSR_TRY(launch_pdl("k_duplicate", k_duplicate, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
+                     (int)tiles_x, (const uint32_t*)splats.tiles, (const uint32_t*)splats.offset,
+                     (const int4*)splats.rect, (const uint32_t*)splats.depth_order, keys_a, vals_a));
   SSR_TRY(radix_pass<0>(m, 0, keys_a, vals_a, nullptr, nullptr, keys_b, vals_b, counts, offsets, hist, st));
   SSR_TRY(radix_pass<0>(m, 8, keys_b, vals_b, nullptr, nullptr, keys_a, inst_gauss, counts, offsets, hist + 256,
                         st));
   const int64_t rthreads = (m + RANGE_KEYS - 1) / RANGE_KEYS;
-  k_ranges<<<(unsigned)((rthreads + 255) / 256), 256, 0, st>>>(m, (int)n_tiles, keys_a, tile_ranges);
-  return check_launch("k_ranges");
+  return launch_pdl("k_ranges", k_ranges, dim3((unsigned)((rthreads + 255) / 256)), dim3(256), 0, st, m,
+                    (int)n_tiles, (const uint32_t*)keys_a, tile_ranges);
 }
 
 extern "C" int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y,

@@ -142,6 +142,7 @@ __device__ __forceinline__ int64_t merge_find(const uint32_t* __restrict__ tiles
 __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
                                                                 const uint32_t* __restrict__ roff,
                                                                 float* __restrict__ rows) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * MERGE_WARPS;
   const int64_t w = (int64_t)blockIdx.x * MERGE_WARPS + (threadIdx.x >> 5);
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
                                                           const uint32_t* __restrict__ roff, float* __restrict__ rows,
                                                           float* __restrict__ grads, int S, int accumulate,
                                                           float* __restrict__ stats, AdamArgsF adam) {
+  griddep_wait();
   __shared__ __align__(16) float s_rows[CHAIN_STAGE_FLOATS + 4];
   __shared__ uint64_t mbar;
   const int64_t i0 = (int64_t)blockIdx.x * CHAIN_ROWS;
@@ -546,6 +548,7 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
                                                          const float4* __restrict__ color,
                                                          const float* __restrict__ rows, float* __restrict__ grads,
                                                          int accumulate) {
+  griddep_wait();
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
   constexpr int KL = (K + 3) / 4;
@@ -677,6 +680,7 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh_adam(CamF cam, int64
                                                               const uint32_t* __restrict__ roff,
                                                               const float4* __restrict__ color,
                                                               const float* __restrict__ rows, AdamArgsF adam) {
+  griddep_wait();
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
   constexpr int KL = (K + 3) / 4;
@@ -856,7 +860,8 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_merge_big, MERGE_WARPS * 32, 0);
     merge_blocks = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 4);  // one resident wave
   }
-  k_merge_big<<<merge_blocks, MERGE_WARPS * 32, 0, st>>>(n, splats.tiles, splats.row_offset, rows);
+  SSR_TRY(launch_pdl("k_merge_big", k_merge_big, dim3(merge_blocks), dim3(MERGE_WARPS * 32), 0, st, n,
+                     (const uint32_t*)splats.tiles, (const uint32_t*)splats.row_offset, rows));
   SSR_TRY(check_launch("k_merge_big"));
   const unsigned blocks = (unsigned)((n + CHAIN_ROWS - 1) / CHAIN_ROWS);
   const size_t geo_smem = FUSED ? 3 * 8 * CHAIN_ROWS * sizeof(float) : 0;
@@ -869,9 +874,9 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
       attr.set();
     }
   }
-  k_chain_geo<FUSED><<<blocks, CHAIN_ROWS, geo_smem, st>>>(c, n, positions, rotations, log_scales, logits, splats.tiles,
-                                                           splats.row_offset, rows, grads, 11 + 3 * K, accumulate,
-                                                           stats, adam);
+  SSR_TRY(launch_pdl("k_chain_geo", k_chain_geo<FUSED>, dim3(blocks), dim3(CHAIN_ROWS), geo_smem, st, c, n, positions,
+                     rotations, log_scales, logits, (const uint32_t*)splats.tiles, (const uint32_t*)splats.row_offset,
+                     rows, grads, 11 + 3 * K, (int)accumulate, stats, adam));
   SSR_TRY(check_launch("k_chain_geo"));
   if (FUSED) {
     const unsigned ablocks = (unsigned)((n + SHA_ROWS - 1) / SHA_ROWS);
@@ -885,8 +890,9 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
                          "k_chain_sh_adam smem"));                                                                \
       attr.set();                                                                                                \
     }                                                                                                             \
-    k_chain_sh_adam<D><<<ablocks, SH_THREADS, sm, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset,     \
-                                                        (const float4*)splats.color, rows, adam);                 \
+    SSR_TRY(launch_pdl("k_chain_sh_adam", k_chain_sh_adam<D>, dim3(ablocks), dim3(SH_THREADS), sm, st, c, n,     \
+                       positions, sh, (const uint32_t*)splats.tiles, (const uint32_t*)splats.row_offset,           \
+                       (const float4*)splats.color, (const float*)rows, adam));                                  \
   } while (0)
     switch (sh_degree) {
       case 0: SSR_SHA(0); break;
@@ -898,9 +904,10 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
     return check_launch("k_chain_sh_adam");
   }
   const unsigned sblocks = (unsigned)((n + SH_ROWS - 1) / SH_ROWS);
-#define SSR_SH(D)                                                                                       \
-  k_chain_sh<D><<<sblocks, SH_THREADS, 0, st>>>(c, n, positions, sh, splats.tiles, splats.row_offset, \
-                                                 (const float4*)splats.color, rows, grads, accumulate)
+#define SSR_SH(D)                                                                                         \
+  SSR_TRY(launch_pdl("k_chain_sh", k_chain_sh<D>, dim3(sblocks), dim3(SH_THREADS), 0, st, c, n, positions, sh, \
+                     (const uint32_t*)splats.tiles, (const uint32_t*)splats.row_offset,                       \
+                     (const float4*)splats.color, (const float*)rows, grads, (int)accumulate))
   switch (sh_degree) {
     case 0: SSR_SH(0); break;
     case 1: SSR_SH(1); break;

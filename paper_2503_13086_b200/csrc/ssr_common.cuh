@@ -14,6 +14,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "../../include/ssr.h"
 
@@ -495,6 +496,38 @@ __device__ __forceinline__ float adam_update(float p, float g, float& m, float& 
   m = __fmaf_rn(0.9f, m, 0.1f * g);
   v = __fmaf_rn(0.999f, v, 0.001f * g * g);
   return p - __fdividef(lr * (m * ib1), sqrt_approx(v * ib2) + 1e-15f);
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels launched with launch_pdl may be scheduled while their stream
+// predecessor drains (its launch latency hides behind the predecessor's
+// tail); each such kernel calls griddep_wait() before anything else, which
+// returns once the predecessor has completed and its writes are visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Zeroes n 32-bit words (a kernel rather than a memset: it keeps the launch
+// chain programmatic).
+static __global__ void k_zero_words(uint32_t* p, int64_t n) {
+  griddep_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+
+template <typename... KArgs, typename... Args>
+static inline int launch_pdl(const char* what, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args&&... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return SSR_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), what);
 }
 
 // ------------------------------------------------------------------ exclusive scan of uint32

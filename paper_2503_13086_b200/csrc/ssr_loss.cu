@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* 
                                                   const Target tgt, const double* __restrict__ soft,
                                                   const int32_t* __restrict__ hard, float* __restrict__ dmaps,
                                                   double* __restrict__ partials) {
+  griddep_wait();
   __shared__ float sx[LH][LH + 1], sy[LH][LH + 1];
   __shared__ float hz[5][LH][HZS];
   __shared__ double red[8];
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_loss_finalize(int W, int H, dou
                                                                double w_load, const double* soft,
                                                                const double* __restrict__ partials, int n_parts,
                                                                LossAcc* acc, double* out) {
+  griddep_wait();
   // fixed-order sums of the per-CTA partials: thread t adds parts t, t + 256,
   // ... in order, then a fixed shuffle / warp-order tree
   __shared__ double red[FIN_THREADS / 32][LOSS_TERMS];
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
                                                   const float* __restrict__ dmaps, const LossAcc* __restrict__ acc,
                                                   double w_l1, double w_ssim, double w_load,
                                                   float* __restrict__ d_image, float* __restrict__ d_soft) {
+  griddep_wait();
   __shared__ float sm[3][LH][LH + 1];
   __shared__ float hz[3][LH][HZS];
   const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
@@ -482,18 +485,20 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
   const Target tg{target, target_u8 ? 1 : 0};
   if (tg.u8)
-    k_ssim_fwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, partials);
+    SSR_TRY(launch_pdl("k_ssim_fwd", k_ssim_fwd<true>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
+                       hard_count, dmaps, partials));
   else
-    k_ssim_fwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, hard_count, dmaps, partials);
+    SSR_TRY(launch_pdl("k_ssim_fwd", k_ssim_fwd<false>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
+                       hard_count, dmaps, partials));
   SSR_TRY(check_launch("k_ssim_fwd"));
-  k_loss_finalize<<<1, FIN_THREADS, 0, st>>>(width, height, w_l1, w_ssim, w_load, soft_count, partials,
-                                             (int)loss_ctas(width, height), acc, out);
+  SSR_TRY(launch_pdl("k_loss_finalize", k_loss_finalize, dim3(1), dim3(FIN_THREADS), 0, st, width, height, w_l1,
+                     w_ssim, w_load, soft_count, (const double*)partials, (int)loss_ctas(width, height), acc, out));
   SSR_TRY(check_launch("k_loss_finalize"));
   if (tg.u8)
-    k_ssim_bwd<true><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
-                                           d_image, d_soft);
+    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<true>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
+                       (const float*)dmaps, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
   else
-    k_ssim_bwd<false><<<grid, 256, 0, st>>>(width, height, image, tg, soft_count, dmaps, acc, w_l1, w_ssim, w_load,
-                                            d_image, d_soft);
+    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<false>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
+                       (const float*)dmaps, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
   return check_launch("k_ssim_bwd");
 }

@@ -36,6 +36,7 @@ template <int K>
 __global__ void __launch_bounds__(ADAM_THREADS) k_adam(AdamPlan plan, float* __restrict__ p,
                                                        const float* __restrict__ g_base, int64_t goff,
                                                        float* __restrict__ m, float* __restrict__ v) {
+  griddep_wait();
   const float* __restrict__ g = g_base - goff;
   const int64_t bid = blockIdx.x;
   int ri = 0;
@@ -331,12 +332,15 @@ static int launch_adam(int64_t n, int32_t sh_degree, float* params, const float*
   }
   if (blocks == 0) return SSR_OK;
   switch (K) {
-    case 1: k_adam<1><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
-    case 4: k_adam<4><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
-    case 9: k_adam<9><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
-    default: k_adam<16><<<(unsigned)blocks, ADAM_THREADS, 0, st>>>(plan, params, grads, goff, m, v); break;
+    case 1: return launch_pdl("k_adam", k_adam<1>, dim3((unsigned)blocks), dim3(ADAM_THREADS), 0, st, plan, params,
+                          grads, goff, m, v);
+    case 4: return launch_pdl("k_adam", k_adam<4>, dim3((unsigned)blocks), dim3(ADAM_THREADS), 0, st, plan, params,
+                          grads, goff, m, v);
+    case 9: return launch_pdl("k_adam", k_adam<9>, dim3((unsigned)blocks), dim3(ADAM_THREADS), 0, st, plan, params,
+                          grads, goff, m, v);
+    default: return launch_pdl("k_adam", k_adam<16>, dim3((unsigned)blocks), dim3(ADAM_THREADS), 0, st, plan, params,
+                          grads, goff, m, v);
   }
-  return check_launch("k_adam");
 }
 
 

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(PRE_ROWS, 7) k_preprocess(Cam cam, int64_t n, 
                                                          const float* __restrict__ ls,
                                                          const float* __restrict__ logit,
                                                          const float* __restrict__ sh, ssr_splats o) {
+  griddep_wait();
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
   extern __shared__ __align__(16) float s_pre[];  // rot 4R | pos 3R | log-scale 3R | sh W R
@@ -165,11 +166,11 @@ extern "C" int ssr_preprocess(const ssr_camera* cam, int64_t n, int32_t sh_degre
             "k_preprocess smem"));                                                                                 \
         attr.set();                                                                                               \
       }                                                                                                            \
-      k_preprocess<D, true><<<(unsigned)blocks, PRE_ROWS, sm, st>>>(c, n, tx, ty, positions, rotations,           \
-                                                                    log_scales, opacity_logits, sh, splats);       \
+      SSR_TRY(launch_pdl("k_preprocess", k_preprocess<D, true>, dim3((unsigned)blocks), dim3(PRE_ROWS), sm, st, c, \
+                         n, tx, ty, positions, rotations, log_scales, opacity_logits, sh, splats));              \
     } else {                                                                                                       \
-      k_preprocess<D, false><<<(unsigned)blocks, PRE_ROWS, 0, st>>>(c, n, tx, ty, positions, rotations,           \
-                                                                    log_scales, opacity_logits, sh, splats);       \
+      SSR_TRY(launch_pdl("k_preprocess", k_preprocess<D, false>, dim3((unsigned)blocks), dim3(PRE_ROWS), 0, st, c, \
+                         n, tx, ty, positions, rotations, log_scales, opacity_logits, sh, splats));              \
     }                                                                                                              \
   } while (0)
   switch (sh_degree) {

@@ -192,6 +192,7 @@ constexpr int FWD_BATCH = 2 * TILE_PX;
 // checkpoints are written (the backward's seeds, ~16 B per live pixel-bucket).
 template <bool CK, bool SOFT>
 __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
+  griddep_wait();
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
@@ -523,6 +524,7 @@ __device__ void walk_pixel64(const RasterArgs& a, int s0, int s1, double xx, dou
 // Forward fix-up: persistent grid, one warp per flagged pixel of the compact
 // list k_forward built (pixels are independent).
 __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int nw_total = gridDim.x * 8, count = a.fix[0];
   const int* px_list = fix_pixels(a);
@@ -551,6 +553,12 @@ __global__ void __launch_bounds__(256) k_forward_fixup(RasterArgs a) {
       atomicMax(&a.tile_info[t].z, r.nw);
     }
   }
+}
+
+// Reset of the fix-up list heads (a kernel, so the launch chain stays programmatic).
+__global__ void k_fix_reset(int* fix) {
+  griddep_wait();
+  if (threadIdx.x < FIX_HEAD) fix[threadIdx.x] = 0;
 }
 
 // ------------------------------------------------------------------ backward, splat-parallel (fp32)
@@ -755,6 +763,7 @@ __device__ __forceinline__ void bw_stream2(const uint16_t* __restrict__ list, co
 
 __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
+  griddep_wait();
   const int t = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int2 rg = a.ranges[t];
@@ -896,6 +905,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
 
 __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
+  griddep_wait();
   const int t = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int2 rg = a.ranges[t];
@@ -1038,6 +1048,7 @@ __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterA
 // summed in a fixed order (deterministic), one row write per slot.
 __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
+  griddep_wait();
   const int t = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int2 rg = a.ranges[t];
@@ -1169,6 +1180,7 @@ __device__ __forceinline__ int fix_tile_buckets(const RasterArgs& a, int it) {
 // Bucket plan of the backward fix-up: exclusive prefix over the flagged tiles
 // of their bucket counts (one CTA; <= n_tiles entries), total in fix[2].
 __global__ void __launch_bounds__(1024) k_fix_plan(RasterArgs a) {
+  griddep_wait();
   __shared__ int s_part[32];
   const int n_ft = a.fix[1];
   const int per = (n_ft + 1023) / 1024;
@@ -1210,6 +1222,7 @@ __global__ void __launch_bounds__(1024) k_fix_plan(RasterArgs a) {
 // row with one plain add: every row is owned by exactly one item.
 __global__ void __launch_bounds__(256, 2) k_backward_fixup(RasterArgs a, const float* __restrict__ d_image,
                                                            const float* __restrict__ d_soft, float* __restrict__ rows) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int n_ft = a.fix[1];
   const int n_items = a.fix[2];
@@ -1387,23 +1400,21 @@ extern "C" int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_ga
     set_error("ssr_forward: frame.fix_list is required");
     return SSR_ERR_INVALID;
   }
-  if (cudaMemsetAsync(frame.fix_list, 0, FIX_HEAD * sizeof(int32_t), st) != cudaSuccess)
-    return check_launch("fix_list reset");
+  SSR_TRY(launch_pdl("k_fix_reset", k_fix_reset, dim3(1), dim3(32), 0, st, frame.fix_list));
   // frame.ckpt == NULL: render-only (no backward state beyond the per-pixel outputs)
   // frame.soft_count == NULL: no soft-count output (the caller's loss does not
   // read it); the walk then culls pairs below 1/255 at the packed far test
   if (frame.ckpt)
     if (frame.soft_count)
-      k_forward<true, true><<<n_tiles, TILE_PX, 0, st>>>(a);
+      SSR_TRY(launch_pdl("k_forward", k_forward<true, true>, dim3(n_tiles), dim3(TILE_PX), 0, st, a));
     else
-      k_forward<true, false><<<n_tiles, TILE_PX, 0, st>>>(a);
+      SSR_TRY(launch_pdl("k_forward", k_forward<true, false>, dim3(n_tiles), dim3(TILE_PX), 0, st, a));
   else if (frame.soft_count)
-    k_forward<false, true><<<n_tiles, TILE_PX, 0, st>>>(a);
+    SSR_TRY(launch_pdl("k_forward", k_forward<false, true>, dim3(n_tiles), dim3(TILE_PX), 0, st, a));
   else
-    k_forward<false, false><<<n_tiles, TILE_PX, 0, st>>>(a);
+    SSR_TRY(launch_pdl("k_forward", k_forward<false, false>, dim3(n_tiles), dim3(TILE_PX), 0, st, a));
   SSR_TRY(check_launch("k_forward"));
-  k_forward_fixup<<<num_sms() * 4, 256, 0, st>>>(a);
-  return check_launch("k_forward_fixup");
+  return launch_pdl("k_forward_fixup", k_forward_fixup, dim3(num_sms() * 4), dim3(256), 0, st, a);
 }
 
 extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
@@ -1426,19 +1437,21 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     // (fewer shared-memory and shuffle wavefronts per pair, -1.4%); with one,
     // the soft pair block needs the registers of the one-slot kernel
     if (!d_soft)
-      k_backward_splat2<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image,
+                         d_soft, inst_rows));
     else
-      k_backward_splat<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+      SSR_TRY(launch_pdl("k_backward_splat", k_backward_splat, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image,
+                         d_soft, inst_rows));
   }
   else
-    k_backward_pixel<<<n_tiles, TILE_PX, 0, st>>>(a, d_image, d_soft, inst_rows);
+    SSR_TRY(launch_pdl("k_backward_pixel", k_backward_pixel, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image, d_soft,
+                       inst_rows));
   SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
   if (!frame.fix_list) {
     set_error("ssr_backward: frame.fix_list is required");
     return SSR_ERR_INVALID;
   }
-  k_fix_plan<<<1, 1024, 0, st>>>(a);
-  SSR_TRY(check_launch("k_fix_plan"));
-  k_backward_fixup<<<num_sms() * 2, 256, 0, st>>>(a, d_image, d_soft, inst_rows);
-  return check_launch("k_backward_fixup");
+  SSR_TRY(launch_pdl("k_fix_plan", k_fix_plan, dim3(1), dim3(1024), 0, st, a));
+  return launch_pdl("k_backward_fixup", k_backward_fixup, dim3(num_sms() * 2), dim3(256), 0, st, a, d_image, d_soft,
+                    inst_rows);
 }
