@@ -167,7 +167,18 @@ int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
  * dconic abc] (9 floats) stored at the instance's splat-major position
  * (splats.row_offset[g] + local tile index).  layout 0 = splat-parallel
  * (Taming-style warp per 32-splat bucket), 1 = pixel-parallel.  Rows of
- * guard-band pixels are added by an fp64 pixel walk. */
+ * guard-band pixels are added by an fp64 pixel walk.
+ *
+ * inst_rows is a WORKSPACE of ssr_rows_floats(M) floats that the caller
+ * zero-fills once when it allocates it and then hands unchanged to every
+ * ssr_backward / ssr_chain pair (it may be regrown: zero-fill the new one).
+ * Word 0 holds a generation counter, then each instance has a 10-word row: the
+ * 9 terms and the generation that wrote it.  ssr_backward writes rows only for
+ * the slots some pixel walked (slot < tile_info.x); a row with a stale tag is
+ * zero to ssr_chain.  This skips the scattered zero-fill of unwalked slots
+ * (~30% of the rows at config 2, ~80% at config 4).  One buffer per stream. */
+int64_t ssr_rows_floats(int64_t m);
+
 int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
                  const int32_t* tile_ranges, ssr_frame frame, const float* d_image,
                  const float* d_soft, float* inst_rows, void* stream);
@@ -177,7 +188,8 @@ int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* i
  * FieldGrads buffer [pos 3N | rot 4N | logscale 3N | logit N | sh 3KN |
  * screen_norm N | visible N].  accumulate!=0 adds into it (view batches);
  * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible.
- * inst_rows is consumed (used as scratch between the two chain kernels). */
+ * inst_rows is the workspace ssr_backward just filled; it is consumed (the
+ * chain parks merged colour gradients in it between its kernels). */
 int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
               const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
               const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream);

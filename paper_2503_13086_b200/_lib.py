@@ -57,6 +57,7 @@ _SIGS = {
     "ssr_bin_tiles_capacity": [c_int64, c_int64, c_int32, c_int32, SsrSplats, c_void_p, ctypes.POINTER(c_int64),
                                c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "ssr_ckpt_floats": [c_int64, c_int32],
+    "ssr_rows_floats": [c_int64],
     "ssr_fix_list_ints": [c_int32, c_int32, c_int32],
     "ssr_forward": [c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_float, c_float, c_void_p],
     "ssr_backward": [c_int32, c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_void_p, c_void_p, c_void_p,
@@ -86,7 +87,7 @@ _SIGS = {
     "ssr_loss": [c_int32, c_int32, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_double, c_double, c_double,
                  c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
 }
-_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_fix_list_ints": c_int64,
+_RESTYPES = {"ssr_last_error": ctypes.c_char_p, "ssr_ckpt_floats": c_int64, "ssr_rows_floats": c_int64, "ssr_fix_list_ints": c_int64,
              "ssr_ply_properties": c_int32}
 
 EXPORTS = tuple(_SIGS)

@@ -78,29 +78,33 @@ constexpr uint32_t MERGE_BIG = 32;
 constexpr uint32_t MERGE_CHUNK = 256;
 constexpr int MERGE_WARPS = 8;
 
-// Sum of nr contiguous instance rows (9 floats each) over a warp: lane l
-// reads rows l, l + 32, ... (two rows, 18 loads, in flight), then a
+// Sum of nr contiguous instance rows (ROW_WORDS floats each) over a warp: lane l
+// reads rows l, l + 32, ... (two rows, 20 loads, in flight), then a
 // reduce-scatter butterfly over 16 zero-padded channels (16 shuffles instead
 // of 9 x 5).  Lanes 2c and 2c + 1 of the bit-reversed lane order end up with
 // channel c; the return value is the lane's channel sum, *ch its channel.
-__device__ __forceinline__ float merge_rows_warp(const float* __restrict__ rw, uint32_t nr, int lane, int* ch) {
+// Rows whose tag is not `gen` belong to slots no pixel walked: zero.
+__device__ __forceinline__ float merge_rows_warp(const float* __restrict__ rw, uint32_t nr, int lane, int* ch,
+                                                 uint32_t gen) {
   float acc[16];
 #pragma unroll
   for (int c = 0; c < 16; c++) acc[c] = 0.f;
   uint32_t j = lane;
   for (; j + 32 < nr; j += 64) {
-    float v0[9], v1[9];
+    float v0[ROW_WORDS], v1[ROW_WORDS];
+    load_row(rw + (int64_t)j * ROW_WORDS, v0);
+    load_row(rw + (int64_t)(j + 32) * ROW_WORDS, v1);
+    const bool w0 = __float_as_uint(v0[9]) == gen, w1 = __float_as_uint(v1[9]) == gen;
 #pragma unroll
-    for (int c = 0; c < 9; c++) {
-      v0[c] = rw[(int64_t)j * 9 + c];
-      v1[c] = rw[(int64_t)(j + 32) * 9 + c];
-    }
-#pragma unroll
-    for (int c = 0; c < 9; c++) acc[c] += v0[c] + v1[c];
+    for (int c = 0; c < 9; c++) acc[c] += (w0 ? v0[c] : 0.f) + (w1 ? v1[c] : 0.f);
   }
-  if (j < nr)
+  if (j < nr) {
+    float v[ROW_WORDS];
+    load_row(rw + (int64_t)j * ROW_WORDS, v);
+    const bool ok = __float_as_uint(v[9]) == gen;
 #pragma unroll
-    for (int c = 0; c < 9; c++) acc[c] += rw[(int64_t)j * 9 + c];
+    for (int c = 0; c < 9; c++) acc[c] += ok ? v[c] : 0.f;
+  }
   // level xor 16: keep half 8 channels, receive the partner's copy of them
 #pragma unroll
   for (int w = 8; w >= 1; w >>= 1) {
@@ -139,10 +143,12 @@ __device__ __forceinline__ int64_t merge_find(const uint32_t* __restrict__ tiles
   return a + (__ffs(m) - 1);
 }
 
-__global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
+__global__ void __launch_bounds__(MERGE_WARPS * 32, 4) k_merge_big(int64_t n, const uint32_t* __restrict__ tiles,
                                                                 const uint32_t* __restrict__ roff,
                                                                 float* __restrict__ rows) {
   griddep_wait();
+  const uint32_t gen = rows_generation(rows);
+  rows += ROWS_HEAD;
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * MERGE_WARPS;
   const int64_t w = (int64_t)blockIdx.x * MERGE_WARPS + (threadIdx.x >> 5);
@@ -169,9 +175,9 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, co
       uint32_t p0 = max(sl, lo0);
       while (p0 < min(el, hi1)) {
         const uint32_t p1 = min(min(el, hi1), (p0 / MERGE_CHUNK + 1) * MERGE_CHUNK);
-        float* rw = rows + (int64_t)p0 * 9;
+        float* rw = rows + (int64_t)p0 * ROW_WORDS;
         int ch;
-        const float v = merge_rows_warp(rw, p1 - p0, lane, &ch);
+        const float v = merge_rows_warp(rw, p1 - p0, lane, &ch, gen);
         __syncwarp();  // every lane's reads of the head row are done before it is overwritten
         if (!(lane & 1) && ch < 9) rw[ch] = v;
         p0 = p1;
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32, 5) k_merge_big(int64_t n, co
 
 // ------------------------------------------------------------------ geometry chain
 constexpr int CHAIN_ROWS = 64;
-constexpr int CHAIN_STAGE_FLOATS = 9 * 512;
+constexpr int CHAIN_STAGE_FLOATS = ROW_WORDS * 448;  // 17.5 KB: 10 CTAs per SM
 
 template <bool FUSED>
 __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, const float* __restrict__ pos,
@@ -195,6 +201,8 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
                                                           float* __restrict__ grads, int S, int accumulate,
                                                           float* __restrict__ stats, AdamArgsF adam) {
   griddep_wait();
+  const uint32_t gen = rows_generation(rows);
+  rows += ROWS_HEAD;
   __shared__ __align__(16) float s_rows[CHAIN_STAGE_FLOATS + 4];
   __shared__ uint64_t mbar;
   const int64_t i0 = (int64_t)blockIdx.x * CHAIN_ROWS;
@@ -205,8 +213,8 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   const uint32_t r_end = roff[i0 + rows_here - 1] + tiles[i0 + rows_here - 1];
   // the CTA's rows are one contiguous range: one 16-byte aligned TMA bulk
   // copy when it fits (inst_rows has >= 16 B slack), else direct reads
-  const int64_t n_floats = (int64_t)(r_end - r_begin) * 9;
-  const int64_t b0 = (int64_t)r_begin * 36, a0 = b0 & ~(int64_t)15;
+  const int64_t n_floats = (int64_t)(r_end - r_begin) * ROW_WORDS;
+  const int64_t b0 = (int64_t)r_begin * ROW_WORDS * 4 + ROWS_HEAD * 4, a0 = b0 & ~(int64_t)15;
   const int pad = (int)((b0 - a0) >> 2);
   const int64_t bytes = ((b0 + n_floats * 4 - a0) + 15) & ~(int64_t)15;
   const bool staged = n_floats > 0 && bytes <= (int64_t)sizeof(s_rows);
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
     if (threadIdx.x == 0) {
       const uint32_t rows4 = (uint32_t)min((int64_t)CHAIN_ROWS, ns - i0);
       mbar_expect_tx(&mbar, (staged ? (uint32_t)bytes : 0u) + (FUSED ? 3u * 32u * rows4 : 0u));
-      if (staged) bulk_g2s(s_rows, reinterpret_cast<const char*>(rows) + a0, (uint32_t)bytes, &mbar);
+      if (staged) bulk_g2s(s_rows, reinterpret_cast<const char*>(rows - ROWS_HEAD) + a0, (uint32_t)bytes, &mbar);
       if (FUSED) {
         const float* src[3] = {rot, adam.m + 3 * ns, adam.v + 3 * ns};
         for (int t = 0; t < 3; t++) {
@@ -254,11 +262,23 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   // more than MERGE_BIG rows were reduced into their first row by k_merge_big
   float pr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (nt > 0) {
-    const float* rw = staged ? s_rows + pad + (int64_t)(s0 - r_begin) * 9 : rows + (int64_t)s0 * 9;
+    const float* rw = staged ? s_rows + pad + (int64_t)(s0 - r_begin) * ROW_WORDS : rows + (int64_t)s0 * ROW_WORDS;
     if (nt <= MERGE_BIG) {
-      for (uint32_t j = 0; j < nt; j++)
+      // rows of slots no pixel walked carry a stale tag: zero.  Separate
+      // shared / global loops so the staged one compiles to LDS.64.
+      auto merge = [&](const float* r) {
+        for (uint32_t j = 0; j < nt; j++) {
+          float v[ROW_WORDS];
+          load_row(r + j * ROW_WORDS, v);
+          const bool ok = __float_as_uint(v[9]) == gen;
 #pragma unroll
-        for (int c = 0; c < 9; c++) pr[c] += rw[j * 9 + c];
+          for (int c = 0; c < 9; c++) pr[c] += ok ? v[c] : 0.f;
+        }
+      };
+      if (staged)
+        merge(s_rows + pad + (int64_t)(s0 - r_begin) * ROW_WORDS);
+      else
+        merge(rows + (int64_t)s0 * ROW_WORDS);
     } else {
       // k_merge_big left one partial sum per chunk the rows span: the first
       // row and every chunk boundary inside the range
@@ -266,7 +286,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
       for (int c = 0; c < 9; c++) pr[c] = rw[c];
       for (uint32_t h = (s0 / MERGE_CHUNK + 1) * MERGE_CHUNK; h < s0 + nt; h += MERGE_CHUNK)
 #pragma unroll
-        for (int c = 0; c < 9; c++) pr[c] += rw[(int64_t)(h - s0) * 9 + c];
+        for (int c = 0; c < 9; c++) pr[c] += rw[(int64_t)(h - s0) * ROW_WORDS + c];
     }
   }
   float* g_pos = grads;
@@ -282,7 +302,7 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
   const float4 q4 = FUSED ? *reinterpret_cast<const float4*>(s_p + tr * 4)
                           : *reinterpret_cast<const float4*>(rot + i * 4);
   float grot[4] = {0.f, 0.f, 0.f, 0.f}, dls[3] = {0.f, 0.f, 0.f}, dpos[3] = {0.f, 0.f, 0.f}, screen = 0.f;
-  float* dst = rows + (int64_t)roff[i] * 9;
+  float* dst = rows + (int64_t)roff[i] * ROW_WORDS;
   if (nt > 0) {
     dst[0] = pr[0];
     dst[1] = pr[1];
@@ -559,7 +579,7 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   const int64_t ii = row_ok ? i : n - 1;  // out-of-range lanes shadow the last row (shuffles need them)
   const int64_t ns = row_stride(n);
   const bool vis = row_ok && tiles[ii] != 0;
-  const float* rw = rows + (vis ? (int64_t)roff[ii] * 9 : 0);
+  const float* rw = rows + ROWS_HEAD + (vis ? (int64_t)roff[ii] * ROW_WORDS : 0);
   float* shrow = sh + ii * W;
   float* grow = grads + 11 * ns + ii * W;
 
@@ -714,7 +734,7 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh_adam(CamF cam, int64
   const bool row_ok = i < n;
   const int64_t ii = row_ok ? i : n - 1;  // out-of-range lanes shadow the last row (shuffles need them)
   const bool vis = row_ok && tiles[ii] != 0;
-  const float* rw = rows + (vis ? (int64_t)roff[ii] * 9 : 0);
+  const float* rw = rows + ROWS_HEAD + (vis ? (int64_t)roff[ii] * ROW_WORDS : 0);
   // colour gradient through the clamp (sh.py:128-131), masks from the fp64 preprocess
   float dcol[3] = {0.f, 0.f, 0.f}, gp_geo = 0.f;
   if (vis) {

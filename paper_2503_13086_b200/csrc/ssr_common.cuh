@@ -513,6 +513,43 @@ static __global__ void k_zero_words(uint32_t* p, int64_t n) {
     p[i] = 0u;
 }
 
+// ------------------------------------------------------------------ instance gradient rows
+// inst_rows workspace (ssr.h ssr_rows_floats): a 4-word header whose word 0 is
+// the generation of the last ssr_backward, then one 10-word row per instance
+// (9 gradient terms + the generation that wrote it).  Only instances some
+// pixel walked get a row; a row whose tag is not the current generation is
+// zero, so the rows of unwalked slots are never written nor zero-filled.
+constexpr int ROWS_HEAD = 4;
+constexpr int ROW_WORDS = 10;
+__device__ __forceinline__ uint32_t rows_generation(const float* rows) {
+  return *reinterpret_cast<const volatile uint32_t*>(rows);
+}
+// 5 x 8-byte loads (global or shared: every row starts 8-byte aligned)
+__device__ __forceinline__ void load_row(const float* r, float* v) {
+  const float2* p = reinterpret_cast<const float2*>(r);
+#pragma unroll
+  for (int i = 0; i < ROW_WORDS / 2; i++) {
+    const float2 x = p[i];
+    v[2 * i] = x.x;
+    v[2 * i + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void store_row(float* rows, size_t r, float v0, float v1, float v2, float v3, float v4,
+                                          float v5, float v6, float v7, float v8, uint32_t tag) {
+  // scalar stores: packing float2 pairs costs the backward 1% (registers)
+  float* p = rows + ROWS_HEAD + r * ROW_WORDS;
+  p[0] = v0;
+  p[1] = v1;
+  p[2] = v2;
+  p[3] = v3;
+  p[4] = v4;
+  p[5] = v5;
+  p[6] = v6;
+  p[7] = v7;
+  p[8] = v8;
+  p[9] = __uint_as_float(tag);
+}
+
 template <typename... KArgs, typename... Args>
 static inline int launch_pdl(const char* what, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                              cudaStream_t st, Args&&... args) {

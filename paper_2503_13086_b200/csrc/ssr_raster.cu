@@ -50,6 +50,7 @@ struct RasterArgs {
 };
 
 constexpr int FIX_HEAD = 4;
+
 __device__ __forceinline__ int* fix_tiles(const RasterArgs& a) { return a.fix + FIX_HEAD; }
 __device__ __forceinline__ int* fix_plan(const RasterArgs& a) { return a.fix + FIX_HEAD + a.n_tiles; }
 __device__ __forceinline__ int* fix_pixels(const RasterArgs& a) { return a.fix + FIX_HEAD + 2 * a.n_tiles; }
@@ -772,6 +773,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
+  const uint32_t gen = rows_generation(rows) + 1;  // k_fix_plan publishes it after this grid
 
   __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
   __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
@@ -881,26 +883,12 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
       bw_stream<true>(sList[warp], mySeed, n_live, lane, k, s, g);
     else
       bw_stream<false>(sList[warp], mySeed, n_live, lane, k, s, g);
-    if (live) {
-      float* r = rows + (size_t)orow * 9;
-      r[0] = g.g0;
-      r[1] = g.g1;
-      r[2] = g.g2;
-      r[3] = g.g3 * (1.f - s.opa);
-      r[4] = ca * g.sx + cb * g.sy;
-      r[5] = cb * g.sx + cc * g.sy;
-      r[6] = -0.5f * g.g6;
-      r[7] = -g.g7;
-      r[8] = -0.5f * g.g8;
-    }
+    if (live)
+      store_row(rows, orow, g.g0, g.g1, g.g2, g.g3 * (1.f - s.opa), ca * g.sx + cb * g.sy, cb * g.sx + cc * g.sy,
+                -0.5f * g.g6, -g.g7, -0.5f * g.g8, gen);
     __syncwarp();
   }
-  // rows of slots no pixel walked
-  for (int k = maxw + tid; k < len; k += blockDim.x) {
-    const uint32_t g = a.inst[s0 + k];
-    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
-    for (int c = 0; c < 9; c++) r[c] = 0.f;
-  }
+  // slots k >= maxw: no row (their tag stays stale, ssr_common.cuh)
 }
 
 __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterArgs a, const float* __restrict__ d_image,
@@ -914,6 +902,7 @@ __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterA
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
+  const uint32_t gen = rows_generation(rows) + 1;  // k_fix_plan publishes it after this grid
 
   __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
   __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
@@ -1020,26 +1009,14 @@ __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterA
       if (k + h < maxw) {
         const uint32_t gi = a.inst[s0 + k + h];
         const float4 co = a.conic_opa[gi];
-        float* r = rows + (size_t)inst_row(a, gi, tx, ty) * 9;
-        r[0] = g[h].g0;
-        r[1] = g[h].g1;
-        r[2] = g[h].g2;
-        r[3] = g[h].g3 * (1.f - fabsf(co.w));
-        r[4] = co.x * g[h].sx + co.y * g[h].sy;
-        r[5] = co.y * g[h].sx + co.z * g[h].sy;
-        r[6] = -0.5f * g[h].g6;
-        r[7] = -g[h].g7;
-        r[8] = -0.5f * g[h].g8;
+        store_row(rows, inst_row(a, gi, tx, ty), g[h].g0, g[h].g1, g[h].g2, g[h].g3 * (1.f - fabsf(co.w)),
+                  co.x * g[h].sx + co.y * g[h].sy, co.y * g[h].sx + co.z * g[h].sy, -0.5f * g[h].g6, -g[h].g7,
+                  -0.5f * g[h].g8, gen);
       }
     }
     __syncwarp();
   }
-  // rows of slots no pixel walked
-  for (int k = maxw + tid; k < len; k += blockDim.x) {
-    const uint32_t g = a.inst[s0 + k];
-    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
-    for (int c = 0; c < 9; c++) r[c] = 0.f;
-  }
+  // slots k >= maxw: no row (their tag stays stale, ssr_common.cuh)
 }
 
 // ------------------------------------------------------------------ backward, pixel-parallel (fp32)
@@ -1057,6 +1034,7 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int x00 = tx * TILE, y00 = ty * TILE;
   const int maxw = a.tile_info[t].x;
+  const uint32_t gen = rows_generation(rows) + 1;  // k_fix_plan publishes it after this grid
   __shared__ float4 sA[32], sB[32];
   __shared__ float4 sQ[32], sM[32];
   __shared__ uint32_t sRow[32];
@@ -1145,19 +1123,18 @@ __global__ void __launch_bounds__(256) k_backward_pixel(RasterArgs a, const floa
         for (int q = 0; q < 9; q++) part[warp][j][q] = c[q];
     }
     __syncthreads();
-    for (int e = tid; e < nc * 9; e += blockDim.x) {
-      const int j = e / 9, q = e % 9;
-      float v = 0.f;
-      for (int ww = 0; ww < 8; ww++) v += part[ww][j][q];
-      rows[(size_t)sRow[j] * 9 + q] = v;
+    for (int e = tid; e < nc * ROW_WORDS; e += blockDim.x) {
+      const int j = e / ROW_WORDS, q = e % ROW_WORDS;
+      float v = __uint_as_float(gen);
+      if (q < 9) {
+        v = 0.f;
+        for (int ww = 0; ww < 8; ww++) v += part[ww][j][q];
+      }
+      rows[ROWS_HEAD + (size_t)sRow[j] * ROW_WORDS + q] = v;
     }
     __syncthreads();
   }
-  for (int k = maxw + tid; k < len; k += blockDim.x) {
-    const uint32_t g = a.inst[s0 + k];
-    float* r = rows + (size_t)inst_row(a, g, tx, ty) * 9;
-    for (int c = 0; c < 9; c++) r[c] = 0.f;
-  }
+  // slots k >= maxw: no row (their tag stays stale, ssr_common.cuh)
 }
 
 // ------------------------------------------------------------------ backward fix-up (fp64)
@@ -1179,8 +1156,10 @@ __device__ __forceinline__ int fix_tile_buckets(const RasterArgs& a, int it) {
 
 // Bucket plan of the backward fix-up: exclusive prefix over the flagged tiles
 // of their bucket counts (one CTA; <= n_tiles entries), total in fix[2].
-__global__ void __launch_bounds__(1024) k_fix_plan(RasterArgs a) {
+__global__ void __launch_bounds__(1024) k_fix_plan(RasterArgs a, float* rows) {
   griddep_wait();
+  // the backward grid has finished reading the old generation: publish the new one
+  if (threadIdx.x == 0) *reinterpret_cast<uint32_t*>(rows) = rows_generation(rows) + 1;
   __shared__ int s_part[32];
   const int n_ft = a.fix[1];
   const int per = (n_ft + 1023) / 1024;
@@ -1329,7 +1308,7 @@ __global__ void __launch_bounds__(256, 2) k_backward_fixup(RasterArgs a, const f
       }
     }
     if (raw.valid) {
-      float* row = rows + (size_t)inst_row(a, raw.g, tx, ty) * 9;
+      float* row = rows + ROWS_HEAD + (size_t)inst_row(a, raw.g, tx, ty) * ROW_WORDS;
       for (int j = 0; j < 9; j++)
         if (acc[j] != 0.0) row[j] += (float)acc[j];
     }
@@ -1341,6 +1320,10 @@ static int num_sms() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n > 0 ? n : 148;
+}
+
+extern "C" int64_t ssr_rows_floats(int64_t m) {
+  return ROWS_HEAD + (m > 0 ? m : 1) * ROW_WORDS + 4;  // +4: the chain's 16-byte aligned TMA windows
 }
 
 extern "C" int64_t ssr_fix_list_ints(int32_t width, int32_t height, int32_t n_tiles) {
@@ -1431,6 +1414,10 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     set_error("ssr_backward: the frame was rendered without checkpoints (render-only)");
     return SSR_ERR_INVALID;
   }
+  if (!frame.fix_list || !inst_rows) {
+    set_error("ssr_backward: frame.fix_list and inst_rows are required");
+    return SSR_ERR_INVALID;
+  }
   RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f, 0.f);
   if (layout == 0) {
     // no soft-count gradient (d_soft NULL): two slots per lane, 64-slot buckets
@@ -1447,11 +1434,7 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     SSR_TRY(launch_pdl("k_backward_pixel", k_backward_pixel, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image, d_soft,
                        inst_rows));
   SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
-  if (!frame.fix_list) {
-    set_error("ssr_backward: frame.fix_list is required");
-    return SSR_ERR_INVALID;
-  }
-  SSR_TRY(launch_pdl("k_fix_plan", k_fix_plan, dim3(1), dim3(1024), 0, st, a));
+  SSR_TRY(launch_pdl("k_fix_plan", k_fix_plan, dim3(1), dim3(1024), 0, st, a, inst_rows));
   return launch_pdl("k_backward_fixup", k_backward_fixup, dim3(num_sms() * 2), dim3(256), 0, st, a, d_image, d_soft,
                     inst_rows);
 }

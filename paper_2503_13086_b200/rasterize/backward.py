@@ -12,6 +12,23 @@ from .forward import RenderOutput
 
 LAYOUTS = {"splat": 0, "pixel": 1}
 
+_ROWS: dict = {}
+
+
+def rows_workspace(dev, m: int) -> torch.Tensor:
+    """The ``inst_rows`` workspace of ssr_backward / ssr_chain (include/ssr.h)
+    for the current device and stream: zero-filled when (re)allocated, then
+    reused by every call -- its generation tags mark which rows the last
+    backward wrote, so rows of unwalked slots are never zero-filled."""
+    need = int(_lib.load().ssr_rows_floats(m))
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _lib.stream_ptr())
+    buf = _ROWS.get(key)
+    if buf is None or buf.numel() < need:
+        _ROWS.pop(key, None)
+        buf = torch.zeros(need + need // 8, dtype=torch.float32, device=dev)
+        _ROWS[key] = buf
+    return buf
+
 
 class FieldGrads:
     """Gradients aligned with the field's parameter arrays.
@@ -121,8 +138,7 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
     m = sp.n_instances
     st = _lib.stream_ptr()
     s = sp.struct()
-    # +4 floats of slack: the chain stages 16-byte aligned windows with TMA bulk copies
-    rows = torch.empty(max(m, 1) * 9 + 4, dtype=torch.float32, device=dev)
+    rows = rows_workspace(dev, m)
     if m:
         _lib.call("ssr_backward", LAYOUTS[layout], m, s, sp.inst_gauss.data_ptr(), sp.tile_ranges.data_ptr(),
                   out.frame_struct(), d_image.data_ptr(), _lib.ptr(d_soft), rows.data_ptr(), st)
@@ -162,7 +178,7 @@ def backward_and_step(field, out: RenderOutput, d_image, d_soft, optimizer, posi
     m = sp.n_instances
     st = _lib.stream_ptr()
     s = sp.struct()
-    rows = torch.empty(max(m, 1) * 9 + 4, dtype=torch.float32, device=dev)
+    rows = rows_workspace(dev, m)
     if m:
         _lib.call("ssr_backward", LAYOUTS[layout], m, s, sp.inst_gauss.data_ptr(), sp.tile_ranges.data_ptr(),
                   out.frame_struct(), d_image.data_ptr(), _lib.ptr(d_soft), rows.data_ptr(), st)
