@@ -60,8 +60,9 @@ def _args():
     ap.add_argument("--e2e-target", default="u8", choices=["u8", "f32"],
                     help="e2e upload of each step's target image: 8-bit like the reference's image files "
                          "(io/images.py; read natively by the loss kernels) or float32")
-    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "sharded"],
-                    help="N > 1: how the ranks' gradient sums meet (train.exchange_and_step)")
+    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "sharded", "p2p"],
+                    help="N > 1: how the ranks' gradient sums meet (train.exchange_and_step; p2p = the "
+                         "fused ssr_exchange_adam kernel over peer memory)")
     ap.add_argument("--batch-views", type=int, default=64, help="semi_global_batch: views per batch (config 4)")
     ap.add_argument("--batch-steps", type=int, default=2, help="semi_global_batch: timed batches (0 skips)")
     ap.add_argument("--extra-steps", type=int, default=10,
@@ -392,7 +393,7 @@ def main():
     from paper_2503_13086_b200.optim import FieldOptimizer
     from paper_2503_13086_b200.rasterize import backward, render
     from paper_2503_13086_b200.rasterize.backward import FieldGrads, backward_and_step
-    from paper_2503_13086_b200.train import TrainState, exchange_and_step
+    from paper_2503_13086_b200.train import PeerExchange, TrainState, exchange_and_step
 
     rank, world, local = _dist()
     torch.cuda.set_device(local)
@@ -413,6 +414,7 @@ def main():
 
     grads_buf = [None]
     layout = ["splat"]
+    exchanger = PeerExchange() if world > 1 and args.exchange == "p2p" else None
 
     def step(k, target=None, values_out=None):
         cam_i = (k * world + rank) % len(cams)
@@ -428,7 +430,7 @@ def main():
                 grads_buf[0] = FieldGrads.zeros(n, field.sh_degree, dev)
             grads = grads_buf[0]
             backward(state.field, out, br.d_image, br.d_soft, grads=grads, accumulate=False, layout=layout[0])
-            exchange_and_step(state.field, grads, state.optimizer, rate, mode=args.exchange)
+            exchange_and_step(state.field, grads, state.optimizer, rate, mode=args.exchange, exchanger=exchanger)
             state.stats[:n] += grads.screen_norms
             state.stats[n:] += grads.visible_count
         elif args.fused:

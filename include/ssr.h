@@ -220,6 +220,28 @@ int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const float* gra
                    float* m, float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest,
                    const double* bc1, const double* bc2, void* stream);
 
+/* The sharded view-batch exchange fused into one kernel per rank,
+ * over peer memory instead of reduce-scatter -> ssr_adam_range -> all-gather.
+ * grads / params: HOST arrays of `world` (<= 8) DEVICE pointers, entry q = rank
+ * q's FieldGrads flat buffer / field parameter buffer, mapped into this process
+ * (CUDA IPC over NVLink / NVSwitch; on one device, that device's memory).
+ * Rank `rank` owns the flat parameter elements ssr_exchange_chunk(P, world,
+ * rank) (P = (11+3K) * row_stride(n)): it sums their gradients over the ranks in
+ * rank order, runs Adam on params[rank] with its own m, v (current only in its
+ * chunk, like ssr_adam_range) and stores the result into every params[q]; the
+ * densify statistics [screen_norms | visible] are summed over the ranks the
+ * same way (its chunk of the 2 * row_stride(n) floats after P) and the sum is
+ * stored into every grads[q].  Caller contract: a barrier that orders every
+ * rank's gradient writes before any rank's call, and one after every rank's
+ * call before any replica is read (e.g. a 1-element NCCL all-reduce on the
+ * stream; the kernel ends with a system-scope fence).  lr, bc1, bc2 as ssr_adam. */
+int ssr_exchange_adam(int64_t n, int32_t sh_degree, int32_t world, int32_t rank, float* const* grads,
+                      float* const* params, float* m, float* v, const double* lr, double lr_sh_rest,
+                      const double* bc1, const double* bc2, void* stream);
+/* [lo, hi) of rank's chunk of `total` floats: 16-byte aligned equal chunks,
+ * the last rank also owning the remainder (used by ssr_exchange_adam). */
+int ssr_exchange_chunk(int64_t total, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+
 /* field.py:303-375: per-row flags (bit0 keep, bit1 clone, bit2 split) and
  * counts[3] = (n_clone, n_split, n_prune) in device memory. stats = the
  * already averaged grad_accum / max(count, 1) (pipeline.py:209-210). */

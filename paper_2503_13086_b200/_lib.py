@@ -67,6 +67,10 @@ _SIGS = {
     "ssr_chain_adam": [ctypes.POINTER(SsrCamera), c_int64, c_int32, c_void_p, c_void_p, c_void_p, SsrSplats,
                        c_void_p, c_void_p, ctypes.POINTER(c_double), c_double, ctypes.POINTER(c_double),
                        ctypes.POINTER(c_double), c_void_p],
+    "ssr_exchange_adam": [c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                          ctypes.POINTER(c_double), c_double, ctypes.POINTER(c_double), ctypes.POINTER(c_double),
+                          c_void_p],
+    "ssr_exchange_chunk": [c_int64, c_int32, c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64)],
     "ssr_adam": [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_double), c_double,
                  ctypes.POINTER(c_double), ctypes.POINTER(c_double), c_void_p],
     "ssr_adam_range": [c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64,

@@ -297,20 +297,123 @@ __global__ void k_densify_apply(int64_t n, int64_t n_new, int K, const float* __
   }
 }
 
+// ------------------------------------------------------------------ fused exchange + Adam over peer memory
+// The sharded step of a view batch as one kernel per rank instead
+// of reduce-scatter -> Adam -> all-gather: rank r owns the flat elements of
+// its chunk; each thread loads the gradients of its elements from every
+// rank's buffer (peer memory over NVLink / NVSwitch, mapped by CUDA IPC), sums
+// them in rank order, runs Adam on its own replica's element and stores the
+// new value into every rank's replica.  Reads and writes use the two link
+// directions at once, the reduced gradient is never written, and the Adam
+// pass over the chunk rides on the transfer.  The densify statistics
+// (screen_norms, visible) are summed the same way and the sum stored into
+// every rank's gradient buffer.  Ranks must not read their replicas until
+// every rank's kernel is done (a stream-ordered barrier after it), nor launch
+// it before every rank's gradients are final (one before it).
+constexpr int MAX_PEERS = 8;
+struct PeerSet {
+  const float* g[MAX_PEERS];
+  float* p[MAX_PEERS];
+  float* gs[MAX_PEERS];  // writable view of the same gradient buffers (statistics)
+  int world;
+};
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+template <int K>
+__global__ void __launch_bounds__(ADAM_THREADS) k_exchange_adam(AdamPlan plan, PeerSet ps, int own,
+                                                                float* __restrict__ m, float* __restrict__ v,
+                                                                int64_t s_lo, int64_t s_hi, int64_t s_block0) {
+  griddep_wait();
+  const int64_t bid = blockIdx.x;
+  const int W = ps.world;
+  if (bid >= s_block0) {
+    // statistics: sum over the ranks, stored into every rank's buffer
+    const int64_t e0 = s_lo + (bid - s_block0) * ADAM_PER_BLOCK;
+    for (int u = 0; u < ADAM_PER_THREAD; u++) {
+      const int64_t e = e0 + (int64_t)u * ADAM_THREADS + threadIdx.x;
+      if (e >= s_hi) break;
+      float g = ps.g[0][e];
+      for (int q = 1; q < W; q++) g += ps.g[q][e];
+      for (int q = 0; q < W; q++) ps.gs[q][e] = g;
+    }
+    __threadfence_system();
+    return;
+  }
+  int ri = 0;
+#pragma unroll
+  for (int i = 1; i < 5; i++)
+    if (bid >= plan.r[i].block0) ri = i;
+  const AdamRegion R = plan.r[ri];
+  const int64_t e0 = R.start + (bid - R.block0) * ADAM_PER_BLOCK;
+  const int64_t e_end = R.start + R.count;
+  float* __restrict__ p = ps.p[own];
+  if ((R.start & 3) == 0 && e0 + ADAM_PER_BLOCK <= e_end) {
+#pragma unroll
+    for (int u = 0; u < ADAM_PER_THREAD / 4; u++) {
+      const int64_t e = e0 + (int64_t)(u * ADAM_THREADS + threadIdx.x) * 4;
+      float4 gq[MAX_PEERS];
+#pragma unroll
+      for (int q = 0; q < MAX_PEERS; q++)  // all loads in flight before the sum
+        if (q < W) gq[q] = *reinterpret_cast<const float4*>(ps.g[q] + e);
+      float4 gg = gq[0];
+#pragma unroll
+      for (int q = 1; q < MAX_PEERS; q++)
+        if (q < W) gg = f4_add(gg, gq[q]);
+      float4 pp = *reinterpret_cast<const float4*>(p + e);
+      float4 mm = *reinterpret_cast<float4*>(m + e);
+      float4 vv = *reinterpret_cast<float4*>(v + e);
+      float lr0 = R.lr, lr1 = R.lr, lr2 = R.lr, lr3 = R.lr;
+      if (R.is_sh) {
+        const int64_t j = e - R.phase0;
+        lr0 = ((j + 0) % K) == 0 ? R.lr : R.lr_rest;
+        lr1 = ((j + 1) % K) == 0 ? R.lr : R.lr_rest;
+        lr2 = ((j + 2) % K) == 0 ? R.lr : R.lr_rest;
+        lr3 = ((j + 3) % K) == 0 ? R.lr : R.lr_rest;
+      }
+      pp.x = adam_one(pp.x, gg.x, mm.x, vv.x, lr0, R.inv_bc1, R.inv_bc2);
+      pp.y = adam_one(pp.y, gg.y, mm.y, vv.y, lr1, R.inv_bc1, R.inv_bc2);
+      pp.z = adam_one(pp.z, gg.z, mm.z, vv.z, lr2, R.inv_bc1, R.inv_bc2);
+      pp.w = adam_one(pp.w, gg.w, mm.w, vv.w, lr3, R.inv_bc1, R.inv_bc2);
+      *reinterpret_cast<float4*>(m + e) = mm;
+      *reinterpret_cast<float4*>(v + e) = vv;
+#pragma unroll
+      for (int q = 0; q < MAX_PEERS; q++)
+        if (q < W) *reinterpret_cast<float4*>(ps.p[q] + e) = pp;
+    }
+  } else {
+    for (int u = 0; u < ADAM_PER_THREAD; u++) {
+      const int64_t e = e0 + (int64_t)u * ADAM_THREADS + threadIdx.x;
+      if (e >= e_end) break;
+      float g = ps.g[0][e];
+      for (int q = 1; q < W; q++) g += ps.g[q][e];
+      const float lr = (R.is_sh && ((e - R.phase0) % K) != 0) ? R.lr_rest : R.lr;
+      float mm = m[e], vv = v[e];
+      const float np = adam_one(p[e], g, mm, vv, lr, R.inv_bc1, R.inv_bc2);
+      m[e] = mm;
+      v[e] = vv;
+      for (int q = 0; q < W; q++) ps.p[q][e] = np;
+    }
+  }
+  // the peer stores are visible system-wide before the kernel's completion
+  // releases the barrier that follows it
+  __threadfence_system();
+}
+
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace ssr
 
 using namespace ssr;
 
-// Adam over the flat elements [lo, hi) of the class-major buffers (padding
-// rows excluded); grads[e - goff] is the gradient of element e.
-static int launch_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, int64_t goff, float* m,
-                       float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest, const double* bc1,
-                       const double* bc2, cudaStream_t st) {
+// Region plan of Adam over the flat elements [lo, hi) (padding rows excluded);
+// returns the block count.
+static int64_t adam_plan(AdamPlan& plan, int64_t n, int32_t sh_degree, int64_t lo, int64_t hi, const double* lr,
+                         double lr_sh_rest, const double* bc1, const double* bc2) {
   const int K = (sh_degree + 1) * (sh_degree + 1);
   const int64_t widths[5] = {3, 4, 3, 1, 3 * (int64_t)K};
-  AdamPlan plan;
   int64_t start = 0, blocks = 0;
   const int64_t ns = row_stride(n);
   for (int c = 0; c < 5; c++) {
@@ -330,6 +433,17 @@ static int launch_adam(int64_t n, int32_t sh_degree, float* params, const float*
     start += widths[c] * ns;
     blocks += (R.count + ADAM_PER_BLOCK - 1) / ADAM_PER_BLOCK;
   }
+  return blocks;
+}
+
+// Adam over the flat elements [lo, hi) of the class-major buffers (padding
+// rows excluded); grads[e - goff] is the gradient of element e.
+static int launch_adam(int64_t n, int32_t sh_degree, float* params, const float* grads, int64_t goff, float* m,
+                       float* v, int64_t lo, int64_t hi, const double* lr, double lr_sh_rest, const double* bc1,
+                       const double* bc2, cudaStream_t st) {
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  AdamPlan plan;
+  const int64_t blocks = adam_plan(plan, n, sh_degree, lo, hi, lr, lr_sh_rest, bc1, bc2);
   if (blocks == 0) return SSR_OK;
   switch (K) {
     case 1: return launch_pdl("k_adam", k_adam<1>, dim3((unsigned)blocks), dim3(ADAM_THREADS), 0, st, plan, params,
@@ -365,6 +479,62 @@ extern "C" int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const
   if (n == 0 || hi == lo) return SSR_OK;
   return launch_adam(n, sh_degree, params, grads, grads_offset, m, v, lo, hi, lr, lr_sh_rest, bc1, bc2,
                      (cudaStream_t)stream);
+}
+
+extern "C" int ssr_exchange_chunk(int64_t total, int32_t world, int32_t rank, int64_t* lo, int64_t* hi) {
+  if (world < 1 || rank < 0 || rank >= world || total < 0 || !lo || !hi) {
+    set_error("ssr_exchange_chunk: invalid argument");
+    return SSR_ERR_INVALID;
+  }
+  const int64_t chunk = total / (4 * (int64_t)world) * 4;  // 16-byte aligned chunks
+  *lo = rank * chunk;
+  *hi = rank == world - 1 ? total : (rank + 1) * chunk;  // the last rank also owns the tail
+  return SSR_OK;
+}
+
+extern "C" int ssr_exchange_adam(int64_t n, int32_t sh_degree, int32_t world, int32_t rank, float* const* grads,
+                                 float* const* params, float* m, float* v, const double* lr, double lr_sh_rest,
+                                 const double* bc1, const double* bc2, void* stream) {
+  if (n < 0 || sh_degree < 0 || sh_degree > 3 || world < 1 || world > MAX_PEERS || rank < 0 || rank >= world ||
+      !grads || !params || !m || !v || !lr || !bc1 || !bc2) {
+    set_error("ssr_exchange_adam: invalid argument (world must be 1..8)");
+    return SSR_ERR_INVALID;
+  }
+  if (n == 0) return SSR_OK;
+  PeerSet ps = {};
+  ps.world = world;
+  for (int q = 0; q < world; q++) {
+    if (!grads[q] || !params[q]) {
+      set_error("ssr_exchange_adam: null peer pointer");
+      return SSR_ERR_INVALID;
+    }
+    ps.g[q] = grads[q];
+    ps.gs[q] = grads[q];
+    ps.p[q] = params[q];
+  }
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  const int64_t ns = row_stride(n);
+  const int64_t p_floats = (11 + 3 * (int64_t)K) * ns;
+  int64_t lo, hi, s_lo, s_hi;
+  SSR_TRY(ssr_exchange_chunk(p_floats, world, rank, &lo, &hi));
+  SSR_TRY(ssr_exchange_chunk(2 * ns, world, rank, &s_lo, &s_hi));
+  s_lo += p_floats;  // statistics: [screen_norms | visible] after the parameter classes
+  s_hi += p_floats;
+  AdamPlan plan;
+  const int64_t blocks = adam_plan(plan, n, sh_degree, lo, hi, lr, lr_sh_rest, bc1, bc2);
+  const int64_t total = blocks + (s_hi - s_lo + ADAM_PER_BLOCK - 1) / ADAM_PER_BLOCK;
+  if (total == 0) return SSR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (K) {
+    case 1: return launch_pdl("k_exchange_adam", k_exchange_adam<1>, dim3((unsigned)total), dim3(ADAM_THREADS), 0,
+                              st, plan, ps, (int)rank, m, v, s_lo, s_hi, blocks);
+    case 4: return launch_pdl("k_exchange_adam", k_exchange_adam<4>, dim3((unsigned)total), dim3(ADAM_THREADS), 0,
+                              st, plan, ps, (int)rank, m, v, s_lo, s_hi, blocks);
+    case 9: return launch_pdl("k_exchange_adam", k_exchange_adam<9>, dim3((unsigned)total), dim3(ADAM_THREADS), 0,
+                              st, plan, ps, (int)rank, m, v, s_lo, s_hi, blocks);
+    default: return launch_pdl("k_exchange_adam", k_exchange_adam<16>, dim3((unsigned)total), dim3(ADAM_THREADS), 0,
+                               st, plan, ps, (int)rank, m, v, s_lo, s_hi, blocks);
+  }
 }
 
 extern "C" int ssr_densify_masks(int64_t n, const float* params, int32_t sh_degree, const float* stats,

@@ -119,7 +119,7 @@ def shard_layout(param_floats: int, world: int):
 
 
 def exchange_and_step(field, grads, optimizer, position_rate: float, mode: str = "allreduce", group=None,
-                      adam_range=None):
+                      adam_range=None, exchanger=None):
     """Combine the ranks' gradient sums and apply the identical Adam step.
 
     ``mode="allreduce"``: one all-reduce of the whole 61-float-per-row buffer,
@@ -129,6 +129,9 @@ def exchange_and_step(field, grads, optimizer, position_rate: float, mode: str =
     all-reduce of the tail and the densify statistics.  Same bytes on the wire
     as the all-reduce, 1/world of the Adam traffic per rank; rank r's moments
     are current only inside its chunk (``gather_moments`` before a densify).
+
+    ``mode="p2p"``: the sharded step fused into one kernel per rank over peer
+    memory (``exchange_p2p``; ``exchanger`` keeps the peer mappings).
 
     ``adam_range(lo, hi, g, goff)`` overrides the CUDA Adam (host-logic tests).
     """
@@ -141,6 +144,11 @@ def exchange_and_step(field, grads, optimizer, position_rate: float, mode: str =
             optimizer.step(field, grads, position_rate=position_rate)
         else:
             adam_range(0, field.flat.numel(), grads.flat, 0)
+        return
+    if mode == "p2p":
+        if adam_range is not None:
+            raise ValueError("mode='p2p' runs the fused CUDA kernel; adam_range applies to 'sharded'")
+        exchange_p2p(field, grads, optimizer, position_rate, exchanger or PeerExchange(group))
         return
     if mode != "sharded":
         raise ValueError(f"unknown exchange mode {mode!r}")
@@ -171,19 +179,110 @@ def exchange_and_step(field, grads, optimizer, position_rate: float, mode: str =
     dist.all_gather_into_tensor(field.flat[:main], src, group=group)
 
 
-def gather_moments(field, optimizer, group=None):
+def gather_moments(field, optimizer, group=None, mode: str = "sharded"):
     """Make every rank's Adam moments complete after sharded steps (before a
-    densify remaps rows across chunk boundaries)."""
+    densify remaps rows across chunk boundaries).  ``mode="p2p"``: the last
+    rank also owns the tail past ``world * chunk`` (ssr_exchange_chunk)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    chunk, main = shard_layout(field.flat.numel(), world)
+    p_floats = field.flat.numel()
+    chunk, main = shard_layout(p_floats, world)
     for buf in (optimizer.m, optimizer.v):
         src = buf[rank * chunk:(rank + 1) * chunk]
         if dist.get_backend(group) != "nccl":
             src = src.clone()
         dist.all_gather_into_tensor(buf[:main], src, group=group)
+        if mode == "p2p" and main < p_floats:
+            tail = buf[main:p_floats]
+            if dist.get_backend(group) != "nccl":
+                t = tail.clone()
+                dist.broadcast(t, src=dist.get_global_rank(group, world - 1) if group is not None else world - 1,
+                               group=group)
+                tail.copy_(t)
+            else:
+                dist.broadcast(tail, src=dist.get_global_rank(group, world - 1) if group is not None else world - 1,
+                               group=group)
+
+
+class PeerExchange:
+    """Every rank's FieldGrads and parameter buffers mapped into this process
+    (CUDA IPC: peer memory over NVLink / NVSwitch, or the same device's memory
+    when the ranks share one GPU) for ``ssr_exchange_adam``.  The mapping is
+    re-done when any rank's buffers move (a densify reallocates them)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self._keys = None
+        self._maps = None
+        self._flag = None
+
+    def _gather(self, obj):
+        import torch.distributed as dist
+
+        out = [None] * dist.get_world_size(self.group)
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def _map(self, t, rank):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        shared = self._gather(reduce_tensor(t))
+        return [t if q == rank else fn(*args) for q, (fn, args) in enumerate(shared)]
+
+    def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
+        """(grads, params): per-rank device pointers, rank order."""
+        import torch.distributed as dist
+
+        rank = dist.get_rank(self.group)
+        key = (grads_flat.data_ptr(), grads_flat.numel(), params_flat.data_ptr(), params_flat.numel())
+        keys = self._gather(key)
+        if keys != self._keys:
+            self._maps = None  # drop the old mappings before opening new ones
+            self._maps = (self._map(grads_flat, rank), self._map(params_flat, rank))
+            self._keys = keys
+        return [t.data_ptr() for t in self._maps[0]], [t.data_ptr() for t in self._maps[1]]
+
+    def barrier(self, device) -> None:
+        """Stream-ordered barrier: a one-element NCCL all-reduce completes on a
+        rank only once every rank's stream has reached it (gloo: host barrier
+        after a device synchronise)."""
+        import torch.distributed as dist
+
+        if dist.get_backend(self.group) == "nccl":
+            if self._flag is None or self._flag.device != device:
+                self._flag = torch.zeros(1, dtype=torch.float32, device=device)
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize(device)
+            dist.barrier(group=self.group)
+
+
+def exchange_p2p(field, grads, optimizer, position_rate: float, exchanger: PeerExchange) -> None:
+    """The sharded exchange as one fused kernel per rank over peer memory
+    (``ssr_exchange_adam``): reduce-scatter, Adam on the rank's chunk and the
+    all-gather of the new parameters in one pass, plus the summed densify
+    statistics in every rank's ``grads``.  Moments as in ``mode="sharded"``
+    (``gather_moments(mode="p2p")`` before a densify)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from .optim import SH_REST_LR
+
+    group = exchanger.group
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    optimizer.check(field)
+    gp, pp = exchanger.pointers(grads.flat, field.flat)
+    arr = ctypes.c_void_p * world
+    dev = field.flat.device
+    exchanger.barrier(dev)  # every rank's gradient sums are final
+    lr, bc1, bc2 = optimizer.advance(position_rate)
+    field.version += 1
+    _lib.call("ssr_exchange_adam", len(field), field.sh_degree, world, rank, arr(*gp), arr(*pp), optimizer.m.data_ptr(),
+              optimizer.v.data_ptr(), lr, SH_REST_LR, bc1, bc2, _lib.stream_ptr())
+    exchanger.barrier(dev)  # every replica holds every rank's chunk
 
 
 def densify_top_fraction(state: TrainState, fraction: float) -> None:
@@ -223,6 +322,7 @@ class SemiGlobalBatch:
         self.densify_every = int(densify_every)
         self.densify_fraction = densify_fraction
         self._grads = None
+        self._exchanger = PeerExchange(group) if mode == "p2p" else None
 
     def _buffer(self):
         f = self.state.field
@@ -244,14 +344,14 @@ class SemiGlobalBatch:
             backward(f, out, br.d_image, br.d_soft, layout=st.layout, grads=grads, accumulate=True)
             losses.append(br)
         rate = float(np.mean(position_rates)) if len(position_rates) else 0.0
-        exchange_and_step(f, grads, st.optimizer, rate, mode=self.mode, group=self.group)
+        exchange_and_step(f, grads, st.optimizer, rate, mode=self.mode, group=self.group, exchanger=self._exchanger)
         n = len(f)
         st.stats[:n] += grads.screen_norms
         st.stats[n:] += grads.visible_count
         st.global_iteration += 1
         if self.densify_every and st.global_iteration % self.densify_every == 0:
-            if self.mode == "sharded" and world > 1:
-                gather_moments(f, st.optimizer, self.group)
+            if self.mode in ("sharded", "p2p") and world > 1:
+                gather_moments(f, st.optimizer, self.group, mode=self.mode)
             if self.densify_fraction:
                 densify_top_fraction(st, self.densify_fraction)
             else:

@@ -3,6 +3,7 @@ declares, host-side logic (camera, scenes, FieldGrads packing, view sharding,
 loss-weight validation), loud failure without a GPU, and the N>1 gradient
 all-reduce path over gloo with world_size 2."""
 
+import ctypes
 import os
 import re
 import socket
@@ -321,3 +322,56 @@ def test_sharded_batch_step_matches_allreduce_gloo_world2():
             np.testing.assert_allclose(b, a, rtol=1e-6, atol=1e-7)
     for i in range(4):
         np.testing.assert_array_equal(res[0]["sharded"][i], res[1]["sharded"][i])
+
+
+def _moments_worker(rank, world, port, q):
+    import types
+
+    import torch.distributed as dist
+
+    from paper_2503_13086_b200 import _lib
+    from paper_2503_13086_b200.train import gather_moments
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    total = 4 * 37 + 3  # a tail past world * chunk
+    truth = torch.arange(total, dtype=torch.float32)
+    lo, hi = ctypes.c_int64(0), ctypes.c_int64(0)
+    _lib.call("ssr_exchange_chunk", total, world, rank, ctypes.byref(lo), ctypes.byref(hi))
+    # each rank's moments are current only in its ssr_exchange_chunk range
+    m = torch.full((total,), -1.0)
+    m[lo.value:hi.value] = truth[lo.value:hi.value]
+    opt = types.SimpleNamespace(m=m, v=m.clone() * 2)
+    fld = types.SimpleNamespace(flat=torch.zeros(total))
+    gather_moments(fld, opt, mode="p2p")
+    q.put((rank, (lo.value, hi.value), opt.m.numpy().copy(), opt.v.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_gather_moments_gloo(world):
+    """After p2p exchange steps (ssr_exchange_adam: the last rank also owns the
+    tail past world * chunk), gather_moments leaves every rank complete moments;
+    the ranks' chunks (the C ABI's ssr_exchange_chunk) tile the buffer."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_moments_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, b, m, v = q.get(timeout=180)
+        res[r] = (b, m, v)
+    for p in procs:
+        p.join(timeout=60)
+    total = 4 * 37 + 3
+    bounds = [res[r][0] for r in range(world)]
+    assert bounds[0][0] == 0 and bounds[-1][1] == total
+    assert all(a[1] == b[0] and a[0] % 4 == 0 for a, b in zip(bounds, bounds[1:]))
+    truth = np.arange(total, dtype=np.float32)
+    for r in range(world):
+        np.testing.assert_array_equal(res[r][1], truth)
+        np.testing.assert_array_equal(res[r][2], 2 * truth)
