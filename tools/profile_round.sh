@@ -22,4 +22,10 @@ SSR_DIST_BACKEND=gloo SSR_FORCE_DEVICE0=1 timeout 900 python -m torch.distribute
   --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 --steps 3 --warmup 3 --exchange sharded \
   --batch-views 8 --batch-steps 1 --extra-steps 0 --progressive-events 0 --no-cpu-baseline \
   > $O/mg2_sharded_functional.json 2> $O/mg2_sharded_functional.err; echo "mg2_functional exit $?" >> $O/status.txt
+SSR_DIST_BACKEND=gloo SSR_FORCE_DEVICE0=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 --steps 3 --warmup 3 --exchange p2p \
+  --batch-views 8 --batch-steps 1 --extra-steps 0 --progressive-events 0 --no-cpu-baseline \
+  > $O/mg2_p2p_functional.json 2> $O/mg2_p2p_functional.err; echo "mg2_p2p_functional exit $?" >> $O/status.txt
+SSR_CFG=4 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv \
+  python tools/profile_step.py > $O/ncu_c4.log 2>&1; echo "ncu_launch_c4 exit $?" >> $O/status.txt
 cat $O/status.txt
