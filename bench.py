@@ -666,8 +666,8 @@ def main():
         elif stage_ms.get("ssr_chain_adam"):
             kname, kms = ("ssr_chain_adam (k_merge_big + k_chain_geo + k_chain_sh, fused Adam)",
                           stage_ms["ssr_chain_adam"])
-            kbytes = 6.0 * s_bytes * n_rows + 36.0 * M_mean
-            work = f"6 x {s_bytes} B x {n_rows:,} rows + 36 B x {M_mean:,.0f} instance rows"
+            kbytes = 6.0 * s_bytes * n_rows + 40.0 * M_mean  # 10-word tagged rows
+            work = f"6 x {s_bytes} B x {n_rows:,} rows + 40 B x {M_mean:,.0f} instance rows"
         if kms:
             hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
             ach = kbytes / (kms / 1e3) / 1e9
