@@ -116,9 +116,10 @@ int ssr_project_aux(const ssr_camera* cam, int64_t n, int32_t sh_degree, const f
  * decoupled-look-back scans of splats.tiles: in depth order into splats.offset
  * (each row's instances are emitted at depth-ordered positions) and in field-row
  * order into splats.row_offset.  *total_dev gets M, summed in 64 bits; M is
- * computed first and copied to pinned host memory ahead of the depth sort, so
- * a following ssr_bin_tiles_capacity on the same host thread waits for that
- * copy alone while the device still sorts. */
+ * computed first and stored by a kernel into mapped pinned host memory ahead of
+ * the depth sort (no copy engine: it cannot queue behind the caller's uploads),
+ * so a following ssr_bin_tiles_capacity on the same host thread waits for that
+ * store alone while the device still sorts. */
 int ssr_scan_workspace(int64_t n, int64_t* bytes);
 int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int64_t workspace_bytes,
                    uint64_t* total_dev, void* stream);

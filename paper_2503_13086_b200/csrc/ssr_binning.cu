@@ -555,10 +555,22 @@ static int sm_count() {
 
 static inline int64_t rx_ctas(int64_t n) { return (n + RX_TILE - 1) / RX_TILE; }
 
-// The instance total M of the last ssr_scan_tiles of this host thread: copied
-// into pinned memory right after it is computed, with an event behind the copy.
+// The instance total M of the last ssr_scan_tiles of this host thread: stored
+// by a one-thread kernel straight into mapped pinned host memory right after
+// it is computed, with an event behind it.  No copy engine is involved, so the
+// read cannot queue behind a caller's host-to-device uploads (an 8-bit target
+// frame in flight delayed a cudaMemcpyAsync of these 8 bytes by ~20 us).
+__global__ void k_publish_total(const uint64_t* __restrict__ total_dev, volatile uint64_t* host) {
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    *host = *total_dev;
+    __threadfence_system();
+  }
+}
+
 struct PendingTotal {
   uint64_t* host = nullptr;
+  uint64_t* host_dev = nullptr;  // device alias of the mapped host word
   cudaEvent_t ev = nullptr;
   const uint64_t* dev = nullptr;
   int device = -1;
@@ -574,15 +586,19 @@ static int arm_pending_total(const uint64_t* total_dev, cudaStream_t st) {
   PendingTotal& pt = pending_total();
   int dev = 0;
   SSR_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
-  if (!pt.host) SSR_TRY(check_cuda(cudaMallocHost(&pt.host, sizeof(uint64_t)), "pinned total"));
+  if (!pt.host) {
+    SSR_TRY(check_cuda(cudaHostAlloc(&pt.host, sizeof(uint64_t), cudaHostAllocMapped | cudaHostAllocPortable),
+                       "mapped total"));
+    SSR_TRY(check_cuda(cudaHostGetDevicePointer(&pt.host_dev, pt.host, 0), "mapped total"));
+  }
   if (pt.ev && pt.device != dev) {
     cudaEventDestroy(pt.ev);
     pt.ev = nullptr;
   }
   if (!pt.ev) SSR_TRY(check_cuda(cudaEventCreateWithFlags(&pt.ev, cudaEventDisableTiming), "total event"));
   pt.device = dev;
-  SSR_TRY(check_cuda(cudaMemcpyAsync(pt.host, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st),
-                     "instance total"));
+  SSR_TRY(launch_pdl("k_publish_total", k_publish_total, dim3(1), dim3(32), 0, st, total_dev,
+                     (volatile uint64_t*)pt.host_dev));
   SSR_TRY(check_cuda(cudaEventRecord(pt.ev, st), "total event record"));
   pt.dev = total_dev;
   pt.armed = true;
@@ -772,7 +788,7 @@ extern "C" int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles
     // the copy was queued by ssr_scan_tiles ahead of its depth sort: wait for
     // it alone, so the binning is launched while the device still sorts
     SSR_TRY(check_cuda(cudaEventSynchronize(pt.ev), "instance total"));
-    m = (int64_t)*pt.host;
+    m = (int64_t)*(volatile uint64_t*)pt.host;
     pt.armed = false;
   } else {
     static thread_local uint64_t* host_total = nullptr;
