@@ -52,7 +52,7 @@ def _args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--progressive-events", type=int, default=3,
+    ap.add_argument("--progressive-events", type=int, default=5,
                     help="also time the progressive loop (config 3, seconds per new image) over this many "
                          "events after one warm-up event; 0 skips it (single GPU only)")
     ap.add_argument("--fused", type=int, default=1,

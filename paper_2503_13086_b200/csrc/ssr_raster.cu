@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
       const int k0 = base - s0;
       for (int j0 = 0; j0 < n; j0 += BUCKET) {
         if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
-          if (CK) ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
+          // without soft counts only the two-slot backward (64-slot buckets)
+          // can follow: every other checkpoint, half the writes
+          if (CK && (SOFT || ((k0 + j0) & 63) == 0))
+            ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
           q.sbig += (double)q.sdev;
           q.sdev = 0.f;
         }
@@ -1412,6 +1415,11 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
   if (m == 0) return SSR_OK;
   if (!frame.ckpt) {
     set_error("ssr_backward: the frame was rendered without checkpoints (render-only)");
+    return SSR_ERR_INVALID;
+  }
+  if (d_soft && !frame.soft_count && layout == 0) {
+    set_error("ssr_backward: a soft-count gradient needs a frame rendered with soft counts "
+              "(without them the forward keeps 64-slot checkpoints only)");
     return SSR_ERR_INVALID;
   }
   if (!frame.fix_list || !inst_rows) {

@@ -80,10 +80,14 @@ def test_render_without_soft_counts(cfg, n, w, h, oracle_lib):
     from paper_2503_13086_b200.rasterize import backward
 
     f2 = GaussianField.from_host(hp)
+    o1 = render(f2, cam)
     o2 = render(f2, cam, soft_count=False)
     d = torch.randn(o2.image.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(5)) * 1e-3
-    g1 = backward(f2, o2, d, torch.zeros(o2.image.shape[:2], device="cuda"))  # one-slot kernel
+    g1 = backward(f2, o1, d, torch.zeros(o1.image.shape[:2], device="cuda"))  # one-slot kernel
     g2 = backward(f2, o2, d, None)  # two-slot kernel
+    # a frame without soft counts keeps 64-slot checkpoints only: no soft-count gradient
+    with pytest.raises(InvalidParameter):
+        backward(f2, o2, d, torch.zeros(o2.image.shape[:2], device="cuda"))
     for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh", "screen_norms"):
         a1, a2 = getattr(g1, k).double(), getattr(g2, k).double()
         assert float((a1 - a2).norm() / a1.norm().clamp_min(1e-30)) <= 1e-5, k
