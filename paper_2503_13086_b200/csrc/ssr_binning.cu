@@ -98,7 +98,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, u
   return wbase + incl - v;
 }
 
-template <int MODE>
+// NB: bits of this pass's digit (<= 8; the tile sort splits its key's bits
+// evenly over its passes, so no ballot or bucket is spent on bits that are
+// always zero).
+template <int MODE, int NB>
 __global__ void __launch_bounds__(RX_THREADS) k_radix_up(int64_t n, int shift, const uint32_t* __restrict__ keys_in,
                                                          const uint32_t* __restrict__ tiles,
                                                          const double* __restrict__ depth,
@@ -107,15 +110,15 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_up(int64_t n, int shift, c
   griddep_wait();
   __shared__ uint32_t s_hist[RX_WARPS][256];  // one histogram per warp: no cross-warp contention
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < RX_WARPS * 256; i += RX_THREADS) (&s_hist[0][0])[i] = 0u;
-  __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RX_TILE + (int64_t)warp * (RX_ITEMS * 32) + lane;
-  uint32_t key[RX_ITEMS];
+  uint32_t key[RX_ITEMS];  // requested before the histogram set-up (latency overlap)
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) key[i] = rx_key<MODE>(base + i * 32, n, keys_in, tiles, depth);
+  for (int i = threadIdx.x; i < RX_WARPS * 256; i += RX_THREADS) (&s_hist[0][0])[i] = 0u;
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++)
-    if (base + i * 32 < n) atomicAdd(&s_hist[warp][(key[i] >> shift) & 255u], 1u);
+    if (base + i * 32 < n) atomicAdd(&s_hist[warp][(key[i] >> shift) & ((1u << NB) - 1u)], 1u);
   __syncthreads();
   if (threadIdx.x < 256) {
     uint32_t c = 0;
@@ -152,12 +155,13 @@ __global__ void __launch_bounds__(RX_THREADS) k_digit_scan(const uint32_t* __res
   }
 }
 
-template <int MODE>
+template <int MODE, int NB>
 __global__ void __launch_bounds__(RX_THREADS, 2) k_radix_down(
     int64_t n, int shift, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     const uint32_t* __restrict__ tiles, const double* __restrict__ depth, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ offsets, int n_ctas) {
   griddep_wait();
+  constexpr uint32_t DMASK = (1u << NB) - 1u;
   __shared__ uint32_t s_keys[RX_TILE];
   __shared__ uint32_t s_vals[RX_TILE];
   __shared__ uint16_t s_whist[RX_WARPS][256];  // per-warp digit counts, then warp offsets (< 4096)
@@ -166,24 +170,25 @@ __global__ void __launch_bounds__(RX_THREADS, 2) k_radix_down(
   __shared__ uint32_t s_red[RX_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
-  for (int i = threadIdx.x; i < RX_WARPS * 256; i += RX_THREADS) (&s_whist[0][0])[i] = 0u;
-  const uint32_t goff = threadIdx.x < 256 ? offsets[(size_t)threadIdx.x * n_ctas + tile] : 0u;
-  __syncthreads();
+  // the tile's keys are requested first: their latency overlaps the setup
   const int64_t base = (int64_t)tile * RX_TILE + (int64_t)warp * (RX_ITEMS * 32) + lane;
   uint32_t key[RX_ITEMS];  // values are read again at staging time (cache hits), saving registers
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) key[i] = rx_key<MODE>(base + i * 32, n, keys_in, tiles, depth);
+  for (int i = threadIdx.x; i < RX_WARPS * 256; i += RX_THREADS) (&s_whist[0][0])[i] = 0u;
+  const uint32_t goff = threadIdx.x < 256 ? offsets[(size_t)threadIdx.x * n_ctas + tile] : 0u;
+  __syncthreads();
   // ---- stable per-warp ranking (items in input order: item-major, lane-minor)
   const unsigned lt = (1u << lane) - 1u;
   uint32_t rank[RX_ITEMS];
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) {
     const bool valid = base + i * 32 < n;
-    const uint32_t d = (key[i] >> shift) & 255u;
+    const uint32_t d = (key[i] >> shift) & DMASK;
     unsigned peers = __ballot_sync(FULLM, valid);
     if (!valid) peers = ~peers;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
+    for (int b = 0; b < NB; b++) {
       const unsigned bal = __ballot_sync(FULLM, (d >> b) & 1u);
       peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2) k_radix_down(
 #pragma unroll
   for (int i = 0; i < RX_ITEMS; i++) {
     if (base + i * 32 < n) {
-      const uint32_t d = (key[i] >> shift) & 255u;
+      const uint32_t d = (key[i] >> shift) & DMASK;
       const uint32_t pos = s_start[d] + s_whist[warp][d] + rank[i];
       s_keys[pos] = key[i];
       s_vals[pos] = (uint32_t)(warp * (RX_ITEMS * 32) + i * 32 + lane);
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2) k_radix_down(
   for (int i = 0; i < RX_ITEMS; i++) {
     const int j = i * RX_THREADS + threadIdx.x;
     if (j < valid_n) {
-      const uint32_t o = s_gbase[(kv[i] >> shift) & 255u] + (uint32_t)j;
+      const uint32_t o = s_gbase[(kv[i] >> shift) & DMASK] + (uint32_t)j;
       keys_out[o] = kv[i];
       vals_out[o] = vv[i];
     }
@@ -606,17 +611,38 @@ static int arm_pending_total(const uint64_t* total_dev, cudaStream_t st) {
 }
 
 // One stable radix pass: counts -> digit scan -> ranked scatter.
-template <int MODE>
+template <int MODE, int NB>
 static int radix_pass(int64_t n, int shift, const uint32_t* keys_in, const uint32_t* vals_in, const uint32_t* tiles,
                       const double* depth, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts,
                       uint32_t* offsets, uint32_t* hist, cudaStream_t st) {
   const int ctas = (int)rx_ctas(n);
-  SSR_TRY(launch_pdl("k_radix_up", k_radix_up<MODE>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in, tiles,
-                     depth, counts, hist, ctas));
-  SSR_TRY(launch_pdl("k_digit_scan", k_digit_scan, dim3(256), dim3(RX_THREADS), 0, st, (const uint32_t*)counts,
+  SSR_TRY(launch_pdl("k_radix_up", k_radix_up<MODE, NB>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in,
+                     tiles, depth, counts, hist, ctas));
+  SSR_TRY(launch_pdl("k_digit_scan", k_digit_scan, dim3(1u << NB), dim3(RX_THREADS), 0, st, (const uint32_t*)counts,
                      (const uint32_t*)hist, ctas, offsets));
-  return launch_pdl("k_radix_down", k_radix_down<MODE>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in,
+  return launch_pdl("k_radix_down", k_radix_down<MODE, NB>, dim3(ctas), dim3(RX_THREADS), 0, st, n, shift, keys_in,
                     vals_in, tiles, depth, keys_out, vals_out, (const uint32_t*)offsets, ctas);
+}
+
+// A tile-sort pass over nb (1..8) digit bits.
+static int tile_pass(int nb, int64_t m, int shift, const uint32_t* keys_in, const uint32_t* vals_in,
+                     uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts, uint32_t* offsets, uint32_t* hist,
+                     cudaStream_t st) {
+#define SSR_TP(B)                                                                                              \
+  case B:                                                                                                      \
+    return radix_pass<0, B>(m, shift, keys_in, vals_in, nullptr, nullptr, keys_out, vals_out, counts, offsets, \
+                            hist, st)
+  switch (nb) {
+    SSR_TP(1);
+    SSR_TP(2);
+    SSR_TP(3);
+    SSR_TP(4);
+    SSR_TP(5);
+    SSR_TP(6);
+    SSR_TP(7);
+    default: SSR_TP(8);
+  }
+#undef SSR_TP
 }
 
 // scan workspace: [zeroed: hist 3 x 256 u32] [counts 256 x ctas | offsets 256 x ctas u32 | sums 2 x ctas u64]
@@ -706,11 +732,11 @@ extern "C" int ssr_scan_tiles(int64_t n, ssr_splats splats, void* workspace, int
   SSR_TRY(arm_pending_total(total_dev, st));
   // pass 0: keys from (tiles, depth) -> (keys_a, vals_a); pass 1 -> (keys_b, cnt as scratch);
   // pass 2 -> (keys_a, depth_order); the tie-fix then fixes depth_order in place and fills cnt
-  SSR_TRY(radix_pass<1>(n, 0, nullptr, nullptr, splats.tiles, splats.depth, keys_a, vals_a, counts, offsets, hist,
-                        st));
-  SSR_TRY(radix_pass<0>(n, 8, keys_a, vals_a, nullptr, nullptr, keys_b, cnt, counts, offsets, hist + 256, st));
-  SSR_TRY(radix_pass<0>(n, 16, keys_b, cnt, nullptr, nullptr, keys_a, splats.depth_order, counts, offsets,
-                        hist + 512, st));
+  SSR_TRY((radix_pass<1, 8>(n, 0, nullptr, nullptr, splats.tiles, splats.depth, keys_a, vals_a, counts, offsets, hist,
+                        st)));
+  SSR_TRY((radix_pass<0, 8>(n, 8, keys_a, vals_a, nullptr, nullptr, keys_b, cnt, counts, offsets, hist + 256, st)));
+  SSR_TRY((radix_pass<0, 8>(n, 16, keys_b, cnt, nullptr, nullptr, keys_a, splats.depth_order, counts, offsets,
+                        hist + 512, st)));
   SSR_TRY(launch_pdl("k_depth_tiefix", k_depth_tiefix, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
                      (const uint32_t*)keys_a, splats.depth_order, (const double*)splats.depth,
                      (const uint32_t*)splats.tiles, cnt));
@@ -765,12 +791,23 @@ extern "C" int ssr_bin_tiles(int64_t n, int64_t m, int32_t tiles_x, int32_t tile
   SSR_TRY(launch_pdl("k_duplicate", k_duplicate, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
                      (int)tiles_x, (const uint32_t*)splats.tiles, (const uint32_t*)splats.offset,
                      (const int4*)splats.rect, (const uint32_t*)splats.depth_order, keys_a, vals_a));
-  SSR_TRY(radix_pass<0>(m, 0, keys_a, vals_a, nullptr, nullptr, keys_b, vals_b, counts, offsets, hist, st));
-  SSR_TRY(radix_pass<0>(m, 8, keys_b, vals_b, nullptr, nullptr, keys_a, inst_gauss, counts, offsets, hist + 256,
-                        st));
+  // stable LSD sort over the tile id's bits: one pass up to 256 tiles, else
+  // two passes splitting the bits evenly (7 + 6 for the 8160 tiles of 1080p)
+  int bits = 1;
+  while ((1 << bits) < n_tiles) bits++;
+  const uint32_t* sorted_keys;
+  if (bits <= 8) {
+    SSR_TRY(tile_pass(bits, m, 0, keys_a, vals_a, keys_b, inst_gauss, counts, offsets, hist, st));
+    sorted_keys = keys_b;
+  } else {
+    const int b0 = bits <= 14 ? (bits + 1) / 2 : bits - 8;  // high pass <= 8 bits
+    SSR_TRY(tile_pass(b0, m, 0, keys_a, vals_a, keys_b, vals_b, counts, offsets, hist, st));
+    SSR_TRY(tile_pass(bits - b0, m, b0, keys_b, vals_b, keys_a, inst_gauss, counts, offsets, hist + 256, st));
+    sorted_keys = keys_a;
+  }
   const int64_t rthreads = (m + RANGE_KEYS - 1) / RANGE_KEYS;
   return launch_pdl("k_ranges", k_ranges, dim3((unsigned)((rthreads + 255) / 256)), dim3(256), 0, st, m,
-                    (int)n_tiles, (const uint32_t*)keys_a, tile_ranges);
+                    (int)n_tiles, sorted_keys, tile_ranges);
 }
 
 extern "C" int ssr_bin_tiles_capacity(int64_t n, int64_t capacity, int32_t tiles_x, int32_t tiles_y,
