@@ -150,12 +150,17 @@ def _ipc_worker(rank, world, port, q):
         g = FieldGrads(_flat=grads[rank].to(dev).clone(), _n=n, _k=(deg + 1) ** 2)
         ex = PeerExchange()
         results = []
-        for it in range(2):  # the second step reuses the mappings
+        for it in range(3):  # step 2 reuses the mappings; step 3 follows reallocated buffers
             if it == 1:
                 fld.flat.copy_(p.to(dev))
                 opt.m.copy_(m.to(dev))
                 opt.v.copy_(v.to(dev))
                 g.flat.copy_(grads[rank].to(dev))
+            if it == 2:  # as after a densify: new parameter and gradient buffers
+                fld.flat = p.to(dev).clone()
+                opt.m.copy_(m.to(dev))
+                opt.v.copy_(v.to(dev))
+                g = FieldGrads(_flat=grads[rank].to(dev).clone(), _n=n, _k=(deg + 1) ** 2)
             exchange_and_step(fld, g, opt, 1.6e-4, mode="p2p", exchanger=ex)
             torch.cuda.synchronize()
             gather_moments(fld, opt, mode="p2p")
