@@ -3,8 +3,11 @@
  * ssr_preprocess -> ssr_scan_tiles -> (host reads M) -> ssr_bin_tiles ->
  * ssr_forward -- and writes the image and per-pixel walk lengths.
  *
- *   ssr_render in.bin out.bin      (in.bin: see read_inputs; out.bin: image
- *                                   H x W x 3 float32, then n_walk H x W int32)
+ *   ssr_render in.bin out.bin [--grad]
+ *       in.bin: see main; out.bin: image H x W x 3 float32, then n_walk H x W
+ *       int32; with --grad the render keeps the backward state (no soft
+ *       counts) and a backward of d_image = 1e-3 + ssr_chain follow, the flat
+ *       FieldGrads buffer appended to out.bin
  *   ssr_render --query             host-only entry points, no device needed
  *
  * Test infrastructure (tests/test_abi_c.py builds and runs it). */
@@ -71,8 +74,9 @@ static int query(void) {
 
 int main(int argc, char** argv) {
   if (argc == 2 && !strcmp(argv[1], "--query")) return query();
-  if (argc != 3) {
-    fprintf(stderr, "usage: ssr_render in.bin out.bin | --query\n");
+  const int grad = argc == 4 && !strcmp(argv[3], "--grad");
+  if (argc != 3 && !grad) {
+    fprintf(stderr, "usage: ssr_render in.bin out.bin [--grad] | --query\n");
     return 1;
   }
   FILE* f = fopen(argv[1], "rb");
@@ -142,10 +146,11 @@ int main(int argc, char** argv) {
   fr.n_walk = (int32_t*)dalloc(4 * HW);
   fr.terminated = (uint8_t*)dalloc(HW);
   fr.hard_count = (int32_t*)dalloc(4 * HW);
-  fr.soft_count = (double*)dalloc(8 * HW);
+  fr.soft_count = grad ? NULL : (double*)dalloc(8 * HW); /* training: no soft counts */
   fr.flagged = (uint8_t*)dalloc(HW);
   fr.tile_info = (int32_t*)dalloc(16 * (size_t)nt);
-  fr.ckpt = NULL; /* render only: no backward state */
+  /* render only: no backward state; training: the bucket checkpoints */
+  fr.ckpt = grad ? (float*)dalloc(4 * (size_t)ssr_ckpt_floats((int64_t)m, nt)) : NULL;
   fr.fix_list = (int32_t*)dalloc(4 * (size_t)ssr_fix_list_ints(W, H, nt));
   SSR(ssr_forward((int64_t)m, sp, inst, ranges, fr, 1e-5f, 1e-4f, st));
   CK(cudaStreamSynchronize(st));
@@ -158,6 +163,26 @@ int main(int argc, char** argv) {
   if (!o) return 1;
   fwrite(img, 4, 3 * HW, o);
   fwrite(nw, 4, HW, o);
+  if (grad) {
+    /* dL/d(image) = 1e-3 everywhere -> instance rows -> the chain */
+    float* dimg_h = (float*)malloc(12 * HW);
+    for (size_t i = 0; i < 3 * HW; i++) dimg_h[i] = 1e-3f;
+    float* dimg = (float*)dalloc(12 * HW);
+    CK(cudaMemcpy(dimg, dimg_h, 12 * HW, cudaMemcpyHostToDevice));
+    /* the rows workspace: zero-filled once, then reused by every backward */
+    const int64_t rows_n = ssr_rows_floats((int64_t)m);
+    float* rows = (float*)dalloc(4 * (size_t)rows_n);
+    CK(cudaMemset(rows, 0, 4 * (size_t)rows_n));
+    const int64_t ns = (n + 3) & ~(int64_t)3;
+    const size_t g_floats = (size_t)(11 + 3 * K + 2) * ns;
+    float* g = (float*)dalloc(4 * g_floats);
+    SSR(ssr_backward(0, (int64_t)m, sp, inst, ranges, fr, dimg, NULL, rows, st));
+    SSR(ssr_chain(&cam, n, deg, pos, rot, lsc, sh, sp, rows, g, 0, NULL, st));
+    CK(cudaStreamSynchronize(st));
+    float* gh = (float*)malloc(4 * g_floats);
+    CK(cudaMemcpy(gh, g, 4 * g_floats, cudaMemcpyDeviceToHost));
+    fwrite(gh, 4, g_floats, o);
+  }
   fclose(o);
   printf("rendered %dx%d, %lld instances\n", W, H, (long long)m);
   return 0;

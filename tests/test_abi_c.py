@@ -4,7 +4,8 @@ INTEGRATION.md section 2 tells a non-Python host to.
 
 * CPU: the host-only entry points (sizes, chunking, error reporting).
 * GPU: a whole render through caller-owned device buffers, bit-identical to
-  the package's render() of the same field and camera."""
+  the package's render() of the same field and camera; and a backward + chain
+  from C, bit-identical to backward()."""
 
 import ctypes
 import os
@@ -76,3 +77,40 @@ def test_c_host_render_matches_python(tmp_path, cfg, n, w, h):
     assert np.array_equal(img, ref.image.cpu().numpy())
     assert np.array_equal(nw, ref.n_walk.cpu().numpy())
     assert ctypes.sizeof(_lib.SsrCamera) == 9 * 8 + 3 * 8 + 4 * 8 + 3 * 8 + 2 * 4
+
+
+@pytest.mark.gpu
+def test_c_host_backward_matches_python(tmp_path):
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, _lib, scenes
+    from paper_2503_13086_b200.field import flat_size
+    from paper_2503_13086_b200.rasterize import backward, render
+
+    exe = _build(tmp_path)
+    n, w, h = 20000, 320, 240
+    hp = scenes.make_params(1, seed=22, n=n)
+    cam = scenes.camera(1, view=6, width=w, height=h)
+    bg = np.zeros(3)
+    f = GaussianField.from_host(hp)
+    out = render(f, cam, bg=bg, soft_count=False)
+    g = backward(f, out, torch.full_like(out.image, 1e-3))
+    torch.cuda.synchronize()
+    src = tmp_path / "in.bin"
+    with open(src, "wb") as fh:
+        fh.write(np.int64(n).tobytes() + np.int32(f.sh_degree).tobytes() + bg.astype(np.float64).tobytes())
+        fh.write(bytes(_lib.camera_struct(cam)))
+        for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh"):
+            fh.write(np.ascontiguousarray(getattr(hp, k), dtype=np.float32).tobytes())
+    dst = tmp_path / "out.bin"
+    run = subprocess.run([exe, str(src), str(dst), "--grad"], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stderr
+    raw = np.fromfile(dst, dtype=np.uint8)
+    img = raw[: 12 * h * w].view(np.float32).reshape(h, w, 3)
+    flat = raw[16 * h * w:].view(np.float32)
+    assert flat.size == flat_size(n, f.n_sh_coeffs, extra=2)
+    assert np.array_equal(img, out.image.cpu().numpy())
+    got = {k: getattr(type(g)(_flat=torch.from_numpy(flat.copy()), _n=n, _k=f.n_sh_coeffs), k).numpy()
+           for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh", "screen_norms")}
+    for k, v in got.items():
+        assert np.array_equal(v, getattr(g, k).cpu().numpy()), k
