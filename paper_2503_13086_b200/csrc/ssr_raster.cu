@@ -823,7 +823,9 @@ __global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const f
   const unsigned lt_mask = (1u << lane) - 1u;
   uint16_t* const myList = sList[warp] + BW_PAD;
   float2* const mySeed = sSeed[warp];
-  for (int b = warp; b < nb; b += 8) {
+  // buckets over the CTA's warps and, for images of few tiles, over gridDim.y
+  // CTAs of the same tile (each a copy of the pixel set-up)
+  for (int b = warp + 8 * (int)blockIdx.y; b < nb; b += 8 * (int)gridDim.y) {
     const int kb = b * 32;
     // live pixels of this bucket: the walk reaches slot kb (compacted, pixel order)
     int n_live = 0;
@@ -952,7 +954,9 @@ __global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterA
   const unsigned lt_mask = (1u << lane) - 1u;
   uint16_t* const myList = sList[warp] + BW_PAD;
   float2* const mySeed = sSeed[warp];
-  for (int b = warp; b < nb; b += 8) {
+  // buckets over the CTA's warps and, for images of few tiles, over gridDim.y
+  // CTAs of the same tile (each a copy of the pixel set-up)
+  for (int b = warp + 8 * (int)blockIdx.y; b < nb; b += 8 * (int)gridDim.y) {
     const int kb = b * 64;
     int n_live = 0;
 #pragma unroll
@@ -1427,16 +1431,19 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     return SSR_ERR_INVALID;
   }
   RasterArgs a = make_args(splats, inst_gauss, tile_ranges, frame, 0.f, 0.f);
+  // few tiles (small images): split each tile's buckets over up to 8 CTAs so
+  // the grid still fills the GPU (bucket rows are disjoint: no conflicts)
+  const int split = max(1, min(8, (num_sms() * 4 + n_tiles - 1) / n_tiles));
   if (layout == 0) {
     // no soft-count gradient (d_soft NULL): two slots per lane, 64-slot buckets
     // (fewer shared-memory and shuffle wavefronts per pair, -1.4%); with one,
     // the soft pair block needs the registers of the one-slot kernel
     if (!d_soft)
-      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image,
-                         d_soft, inst_rows));
+      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2, dim3(n_tiles, split), dim3(TILE_PX), 0, st, a,
+                         d_image, d_soft, inst_rows));
     else
-      SSR_TRY(launch_pdl("k_backward_splat", k_backward_splat, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image,
-                         d_soft, inst_rows));
+      SSR_TRY(launch_pdl("k_backward_splat", k_backward_splat, dim3(n_tiles, split), dim3(TILE_PX), 0, st, a,
+                         d_image, d_soft, inst_rows));
   }
   else
     SSR_TRY(launch_pdl("k_backward_pixel", k_backward_pixel, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image, d_soft,
