@@ -547,17 +547,6 @@ __global__ void __launch_bounds__(256) k_ranges(int64_t m, int n_tiles, const ui
   }
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 static inline int64_t rx_ctas(int64_t n) { return (n + RX_TILE - 1) / RX_TILE; }
 
 // The instance total M of the last ssr_scan_tiles of this host thread: stored

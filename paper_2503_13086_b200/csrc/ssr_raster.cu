@@ -577,10 +577,6 @@ __global__ void k_fix_reset(int* fix) {
 // (pixel 256: blend limit 0), so the stream needs no bounds checks.  The mean
 // gradient is accumulated as sum(gp dx), sum(gp dy) and mapped through the
 // conic once per row (linear), so a contributing pair costs ~30 instructions.
-#ifndef SSR_BW_UNROLL
-#define SSR_BW_UNROLL 2
-#endif
-constexpr int BW_UNROLL = SSR_BW_UNROLL;
 constexpr int BW2_MIN_BLOCKS = 3;  // 80 registers: 24 warps per SM (2 blocks: 125 registers, no faster)
 constexpr int BW_PAD = 32;
 constexpr int BW_LIST = BW_PAD + TILE_PX + BW_PAD;
