@@ -60,9 +60,10 @@ def _args():
     ap.add_argument("--e2e-target", default="u8", choices=["u8", "f32"],
                     help="e2e upload of each step's target image: 8-bit like the reference's image files "
                          "(io/images.py; read natively by the loss kernels) or float32")
-    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "sharded", "p2p"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "allreduce", "sharded", "p2p"],
                     help="N > 1: how the ranks' gradient sums meet (train.exchange_and_step; p2p = the "
-                         "fused ssr_exchange_adam kernel over peer memory)")
+                         "fused ssr_exchange_adam kernel over peer memory; auto = p2p when every rank "
+                         "can map every rank's buffers, else allreduce)")
     ap.add_argument("--batch-views", type=int, default=64, help="semi_global_batch: views per batch (config 4)")
     ap.add_argument("--batch-steps", type=int, default=2, help="semi_global_batch: timed batches (0 skips)")
     ap.add_argument("--extra-steps", type=int, default=10,
@@ -414,7 +415,21 @@ def main():
 
     grads_buf = [None]
     layout = ["splat"]
-    exchanger = PeerExchange() if world > 1 and args.exchange == "p2p" else None
+    exchanger = None
+    exchange_note = None
+    if world > 1 and args.exchange in ("auto", "p2p"):
+        # the fused peer-memory exchange when every rank can map every rank's
+        # buffers (decided collectively: all ranks take the same branch)
+        grads_buf[0] = FieldGrads.zeros(n, field.sh_degree, dev)
+        exchanger = PeerExchange()
+        ok, why = exchanger.probe(grads_buf[0].flat, field.flat)
+        if not ok:
+            if args.exchange == "p2p":
+                raise SystemExit(f"--exchange p2p: {why}")
+            exchanger, exchange_note = None, f"p2p unavailable ({why}); all-reduce"
+        args.exchange = "p2p" if exchanger is not None else "allreduce"
+    elif args.exchange == "auto":
+        args.exchange = "allreduce"
 
     def step(k, target=None, values_out=None):
         cam_i = (k * world + rank) % len(cams)
@@ -739,7 +754,8 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE config generator, seeded; targets = "
                                                       "renders of a second seed's field)",
         "config": {"workload": _workload(cfg), "n_gaussians": n, "width": cams[0].width, "height": cams[0].height,
-                   "views": len(cams), "parallelism": f"view-sharded dp{world} ({args.exchange})" if world > 1
+                   "views": len(cams), "parallelism": f"view-sharded dp{world} ({exchange_note or args.exchange})"
+                   if world > 1
                    else "single GPU",
                    "l2": "inputs larger than L2 (field + Adam moments 708 MB, per-step working set > 1 GB)",
                    "walked_pairs_per_view": P_mean},

@@ -226,10 +226,38 @@ class PeerExchange:
         return out
 
     def _map(self, t, rank):
+        """Every rank's copy of the buffer ``t`` (its own: ``t``).  A failure on
+        any rank raises RuntimeError on every rank (each step is a collective),
+        so the ranks never disagree about whether the mapping exists."""
         from torch.multiprocessing.reductions import reduce_tensor
 
-        shared = self._gather(reduce_tensor(t))
-        return [t if q == rank else fn(*args) for q, (fn, args) in enumerate(shared)]
+        try:
+            mine = (True, reduce_tensor(t))
+        except Exception as e:  # noqa: BLE001 - reported to every rank below
+            mine = (False, repr(e))
+        shared = self._gather(mine)
+        bad = [str(x) for ok, x in shared if not ok]
+        if bad:
+            raise RuntimeError(f"peer mapping unavailable: {bad[0]}")
+        out, err = [], None
+        try:
+            out = [t if q == rank else fn(*args) for q, (_, (fn, args)) in enumerate(shared)]
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)
+        errs = [x for x in self._gather(err) if x]
+        if errs:
+            raise RuntimeError(f"peer mapping unavailable: {errs[0]}")
+        return out
+
+    def probe(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
+        """(True, "") when every rank can map every rank's buffers, else
+        (False, reason) on every rank (a collective)."""
+        try:
+            self.pointers(grads_flat, params_flat)
+            return True, ""
+        except RuntimeError as e:
+            self._keys = self._maps = None
+            return False, str(e)
 
     def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
         """(grads, params): per-rank device pointers, rank order."""
