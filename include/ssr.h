@@ -241,6 +241,16 @@ int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const float* gra
 int ssr_exchange_adam(int64_t n, int32_t sh_degree, int32_t world, int32_t rank, float* const* grads,
                       float* const* params, float* m, float* v, const double* lr, double lr_sh_rest,
                       const double* bc1, const double* bc2, void* stream);
+/* Peer buffers for ssr_exchange_adam (CUDA IPC).  ssr_ipc_export: the
+ * SSR_IPC_HANDLE_BYTES-byte handle of the device allocation holding ptr and
+ * ptr's offset in it.  ssr_ipc_open (another process): maps that allocation on
+ * the CURRENT device with lazy peer access and returns the buffer's address;
+ * opening one allocation twice shares the mapping (reference-counted).
+ * ssr_ipc_close: drops one reference (unmapping at zero). */
+#define SSR_IPC_HANDLE_BYTES 64
+int ssr_ipc_export(const void* ptr, uint8_t* handle, int64_t* offset);
+int ssr_ipc_open(const uint8_t* handle, int64_t offset, void** ptr);
+int ssr_ipc_close(const uint8_t* handle);
 /* [lo, hi) of rank's chunk of `total` floats: 16-byte aligned equal chunks,
  * the last rank also owning the remainder (used by ssr_exchange_adam). */
 int ssr_exchange_chunk(int64_t total, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);

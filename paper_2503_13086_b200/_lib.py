@@ -71,6 +71,9 @@ _SIGS = {
                           ctypes.POINTER(c_double), c_double, ctypes.POINTER(c_double), ctypes.POINTER(c_double),
                           c_void_p],
     "ssr_exchange_chunk": [c_int64, c_int32, c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64)],
+    "ssr_ipc_export": [c_void_p, c_void_p, ctypes.POINTER(c_int64)],
+    "ssr_ipc_open": [c_void_p, c_int64, ctypes.POINTER(c_void_p)],
+    "ssr_ipc_close": [c_void_p],
     "ssr_adam": [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_double), c_double,
                  ctypes.POINTER(c_double), ctypes.POINTER(c_double), c_void_p],
     "ssr_adam_range": [c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64,

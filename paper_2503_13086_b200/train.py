@@ -208,14 +208,17 @@ def gather_moments(field, optimizer, group=None, mode: str = "sharded"):
 
 class PeerExchange:
     """Every rank's FieldGrads and parameter buffers mapped into this process
-    (CUDA IPC: peer memory over NVLink / NVSwitch, or the same device's memory
-    when the ranks share one GPU) for ``ssr_exchange_adam``.  The mapping is
+    for ``ssr_exchange_adam``: each rank exports its buffers' CUDA IPC handles
+    (``ssr_ipc_export``) and opens the others' on its own device with lazy
+    peer access (``ssr_ipc_open``), so the kernel addresses them over NVLink /
+    NVSwitch (or, ranks sharing one GPU, that GPU's memory).  The mapping is
     re-done when any rank's buffers move (a densify reallocates them)."""
 
     def __init__(self, group=None):
         self.group = group
         self._keys = None
-        self._maps = None
+        self._ptrs = None
+        self._opened = []  # handles this process opened (closed on re-mapping)
         self._flag = None
 
     def _gather(self, obj):
@@ -225,29 +228,56 @@ class PeerExchange:
         dist.all_gather_object(out, obj, group=self.group)
         return out
 
-    def _map(self, t, rank):
-        """Every rank's copy of the buffer ``t`` (its own: ``t``).  A failure on
-        any rank raises RuntimeError on every rank (each step is a collective),
-        so the ranks never disagree about whether the mapping exists."""
-        from torch.multiprocessing.reductions import reduce_tensor
+    def _close(self):
+        for h in self._opened:
+            _lib.call_rc("ssr_ipc_close", h)
+        self._opened = []
 
-        try:
-            mine = (True, reduce_tensor(t))
-        except Exception as e:  # noqa: BLE001 - reported to every rank below
-            mine = (False, repr(e))
+    def _map(self, t, rank):
+        """Every rank's address of its copy of the buffer ``t`` (this rank's:
+        ``t.data_ptr()``).  A failure on any rank raises RuntimeError on every
+        rank (each step is a collective), so the ranks never disagree about
+        whether the mapping exists."""
+        import ctypes
+
+        h = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64(0)
+        rc = _lib.call_rc("ssr_ipc_export", t.data_ptr(), h, ctypes.byref(off))
+        mine = (True, (bytes(h), off.value)) if rc == 0 else (False, _lib.load().ssr_last_error().decode())
         shared = self._gather(mine)
         bad = [str(x) for ok, x in shared if not ok]
         if bad:
             raise RuntimeError(f"peer mapping unavailable: {bad[0]}")
         out, err = [], None
-        try:
-            out = [t if q == rank else fn(*args) for q, (_, (fn, args)) in enumerate(shared)]
-        except Exception as e:  # noqa: BLE001
-            err = repr(e)
+        for q, (_, (handle, offset)) in enumerate(shared):
+            if q == rank:
+                out.append(t.data_ptr())
+                continue
+            p = ctypes.c_void_p(0)
+            hb = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+            if _lib.call_rc("ssr_ipc_open", hb, offset, ctypes.byref(p)) != 0:
+                err = _lib.load().ssr_last_error().decode()
+                break
+            self._opened.append(hb)
+            out.append(int(p.value))
         errs = [x for x in self._gather(err) if x]
         if errs:
             raise RuntimeError(f"peer mapping unavailable: {errs[0]}")
         return out
+
+    def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
+        """(grads, params): per-rank device addresses, rank order."""
+        import torch.distributed as dist
+
+        rank = dist.get_rank(self.group)
+        key = (grads_flat.data_ptr(), grads_flat.numel(), params_flat.data_ptr(), params_flat.numel())
+        keys = self._gather(key)
+        if keys != self._keys:
+            self._close()
+            self._ptrs = self._keys = None
+            self._ptrs = (self._map(grads_flat, rank), self._map(params_flat, rank))
+            self._keys = keys
+        return self._ptrs
 
     def probe(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
         """(True, "") when every rank can map every rank's buffers, else
@@ -256,21 +286,9 @@ class PeerExchange:
             self.pointers(grads_flat, params_flat)
             return True, ""
         except RuntimeError as e:
-            self._keys = self._maps = None
+            self._close()
+            self._keys = self._ptrs = None
             return False, str(e)
-
-    def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
-        """(grads, params): per-rank device pointers, rank order."""
-        import torch.distributed as dist
-
-        rank = dist.get_rank(self.group)
-        key = (grads_flat.data_ptr(), grads_flat.numel(), params_flat.data_ptr(), params_flat.numel())
-        keys = self._gather(key)
-        if keys != self._keys:
-            self._maps = None  # drop the old mappings before opening new ones
-            self._maps = (self._map(grads_flat, rank), self._map(params_flat, rank))
-            self._keys = keys
-        return [t.data_ptr() for t in self._maps[0]], [t.data_ptr() for t in self._maps[1]]
 
     def barrier(self, device) -> None:
         """Stream-ordered barrier: a one-element NCCL all-reduce completes on a
