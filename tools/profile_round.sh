@@ -8,8 +8,8 @@ O=gpurun_out/$TAG
 mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest_gpu exit $?" >> $O/status.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/status.txt
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/status.txt
-timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err; echo "bench_ref exit $?" >> $O/status.txt
+T0=$(date +%s); timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $? ($(( $(date +%s) - T0 )) s)" >> $O/status.txt
+T0=$(date +%s); timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err; echo "bench_ref exit $? ($(( $(date +%s) - T0 )) s)" >> $O/status.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv \
   python tools/profile_step.py > $O/ncu_c2.log 2>&1; echo "ncu_launch_c2 exit $?" >> $O/status.txt
 SSR_CFG=3 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
