@@ -741,7 +741,8 @@ def main():
                     summ = prog.main(["--events", str(args.progressive_events), "--warmup-events", "1"] + extra)
                 progressive[name] = {
                     "metric": "seconds per new image", "value": summ["value"], "unit": "s/image",
-                    "higher_is_better": False, "worst": summ["worst"], "events": summ["events"],
+                    "higher_is_better": False, "median": summ["median"], "worst": summ["worst"],
+                    "events": summ["events"],
                     "field_final": summ["field_final"], "objective": summ["objective"],
                     "value_with_reference_scheduler": summ["value_with_reference_scheduler"],
                     "config": "config 3: 1297x840, +20k Gaussians per image, T_I = 200, reference build_plan / "

@@ -158,6 +158,7 @@ def main(argv=None):
     secs = [p["seconds"] for p in per_event]
     sched = [p["reference_scheduler_s"] for p in per_event]
     summary = {"metric": "seconds per new image (config 3)", "value": float(np.mean(secs)), "unit": "s/image",
+               "median": float(np.median(secs)),
                "worst": float(np.max(secs)), "worst_image": per_event[int(np.argmax(secs))]["image"],
                "events": len(per_event), "field_final": len(sess.field),
                "objective": "paper LossWeights() (0.47, 0.12, 0.41)" if args.paper_weights
