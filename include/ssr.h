@@ -179,7 +179,8 @@ int ssr_forward(int64_t m, ssr_splats splats, const uint32_t* inst_gauss,
  * 9 terms and the generation that wrote it.  ssr_backward writes rows only for
  * the slots some pixel walked (slot < tile_info.x); a row with a stale tag is
  * zero to ssr_chain.  This skips the scattered zero-fill of unwalked slots
- * (~30% of the rows at config 2, ~80% at config 4).  One buffer per stream. */
+ * (~30% of the rows at config 2, ~80% at config 4).  One buffer per stream (and host
+ * thread issuing backward / chain pairs). */
 int64_t ssr_rows_floats(int64_t m);
 
 int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* inst_gauss,

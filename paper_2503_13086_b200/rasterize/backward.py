@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -17,11 +19,14 @@ _ROWS: dict = {}
 
 def rows_workspace(dev, m: int) -> torch.Tensor:
     """The ``inst_rows`` workspace of ssr_backward / ssr_chain (include/ssr.h)
-    for the current device and stream: zero-filled when (re)allocated, then
+    for the current device, stream and host thread: zero-filled when (re)allocated, then
     reused by every call -- its generation tags mark which rows the last
     backward wrote, so rows of unwalked slots are never zero-filled."""
     need = int(_lib.load().ssr_rows_floats(m))
-    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _lib.stream_ptr())
+    # one per device, stream and host thread: a backward and its chain are
+    # separate calls, so calls of two threads on one stream must not share it
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _lib.stream_ptr(),
+           threading.get_ident())
     buf = _ROWS.get(key)
     if buf is None or buf.numel() < need:
         _ROWS.pop(key, None)
