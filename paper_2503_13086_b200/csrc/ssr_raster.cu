@@ -3,8 +3,12 @@
 //
 // Forward: one CTA per tile, one thread per pixel, 512-splat batches staged in
 // shared memory, block-wide early exit on transmittance.  Every 32 walked
-// slots each live pixel checkpoints (T, C_front) so the splat-parallel
-// backward can start any 32-splat bucket without replaying the tile.
+// slots (64 without soft counts: only the two-slot backward can follow) each
+// live pixel checkpoints (T, C_front) so the splat-parallel backward can start
+// any bucket without replaying the tile.
+//
+// Backward: per-instance gradient rows (10 words: 9 terms + the generation
+// tag of ssr_common.cuh) written once each, for the walked slots only.
 //
 // Guard band: the fp32 walk flags a pixel when any discrete
 // decision (power>0 skip, alpha >= 1/255 gate, alpha > 0.99 cap, T(1-a) < 1e-4
