@@ -220,6 +220,7 @@ class PeerExchange:
         self._ptrs = None
         self._opened = []  # handles this process opened (closed on re-mapping)
         self._flag = None
+        self._epoch = self._local_key = None
 
     def _gather(self, obj):
         import torch.distributed as dist
@@ -265,18 +266,29 @@ class PeerExchange:
             raise RuntimeError(f"peer mapping unavailable: {errs[0]}")
         return out
 
-    def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
-        """(grads, params): per-rank device addresses, rank order."""
+    def pointers(self, grads_flat: torch.Tensor, params_flat: torch.Tensor, epoch=None):
+        """(grads, params): per-rank device addresses, rank order.
+
+        ``epoch``: a value every rank changes at the same step whenever its
+        buffers may have moved (exchange_p2p passes the field's identity,
+        generation and size); while it stays the same no collective runs here
+        (the mapping is reused), and a buffer that moved anyway raises.  Without
+        it, the ranks compare buffer addresses collectively on every call."""
         import torch.distributed as dist
 
         rank = dist.get_rank(self.group)
         key = (grads_flat.data_ptr(), grads_flat.numel(), params_flat.data_ptr(), params_flat.numel())
+        if epoch is not None and self._ptrs is not None and epoch == self._epoch:
+            if key != self._local_key:
+                raise RuntimeError("exchange buffers moved without a new epoch")
+            return self._ptrs
         keys = self._gather(key)
         if keys != self._keys:
             self._close()
             self._ptrs = self._keys = None
             self._ptrs = (self._map(grads_flat, rank), self._map(params_flat, rank))
             self._keys = keys
+        self._epoch, self._local_key = epoch, key
         return self._ptrs
 
     def probe(self, grads_flat: torch.Tensor, params_flat: torch.Tensor):
@@ -320,7 +332,10 @@ def exchange_p2p(field, grads, optimizer, position_rate: float, exchanger: PeerE
     group = exchanger.group
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     optimizer.check(field)
-    gp, pp = exchanger.pointers(grads.flat, field.flat)
+    # the field's generation moves with every reallocation (insert / densify),
+    # identically on every rank: the mapping is re-checked only then
+    gp, pp = exchanger.pointers(grads.flat, field.flat,
+                                epoch=(id(field), getattr(field, "generation", 0), len(field), grads.flat.numel()))
     arr = ctypes.c_void_p * world
     dev = field.flat.device
     exchanger.barrier(dev)  # every rank's gradient sums are final

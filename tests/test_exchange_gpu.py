@@ -121,7 +121,7 @@ def _free_port():
 
 class _FlatField:
     def __init__(self, flat, n, deg):
-        self.flat, self._n, self.sh_degree, self.version = flat, n, deg, 0
+        self.flat, self._n, self.sh_degree, self.version, self.generation = flat, n, deg, 0, 0
 
     def __len__(self):
         return self._n
@@ -156,8 +156,9 @@ def _ipc_worker(rank, world, port, q):
                 opt.m.copy_(m.to(dev))
                 opt.v.copy_(v.to(dev))
                 g.flat.copy_(grads[rank].to(dev))
-            if it == 2:  # as after a densify: new parameter and gradient buffers
+            if it == 2:  # as after a densify: new parameter and gradient buffers, a new generation
                 fld.flat = p.to(dev).clone()
+                fld.generation += 1
                 opt.m.copy_(m.to(dev))
                 opt.v.copy_(v.to(dev))
                 g = FieldGrads(_flat=grads[rank].to(dev).clone(), _n=n, _k=(deg + 1) ** 2)
