@@ -238,7 +238,7 @@ int ssr_adam_range(int64_t n, int32_t sh_degree, float* params, const float* gra
  * stored into every grads[q].  Caller contract: a barrier that orders every
  * rank's gradient writes before any rank's call, and one after every rank's
  * call before any replica is read (e.g. a 1-element NCCL all-reduce on the
- * stream; the kernel ends with a system-scope fence).  lr, bc1, bc2 as ssr_adam. */
+ * stream, which the kernel's stores precede by stream order).  lr, bc1, bc2 as ssr_adam. */
 int ssr_exchange_adam(int64_t n, int32_t sh_degree, int32_t world, int32_t rank, float* const* grads,
                       float* const* params, float* m, float* v, const double* lr, double lr_sh_rest,
                       const double* bc1, const double* bc2, void* stream);
