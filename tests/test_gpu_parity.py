@@ -489,3 +489,53 @@ def test_gradient_matches_finite_differences():
         g = backward(f, render(f, cam), wm)
         analytic = float((getattr(g, name).reshape(-1).double() * d[off: off + width * n].double()).sum())
         assert abs(fd - analytic) <= 2e-2 * abs(analytic) + 1e-2, (name, fd, analytic)
+
+
+@pytest.mark.parametrize("w,h", [(200, 120), (2048, 1280), (3840, 2176), (4096, 4096)])
+def test_tile_sort_all_tile_id_widths(w, h):
+    """The stable tile sort splits the tile id's bits over its passes (one pass
+    up to 256 tiles, 7 + 6 bits at 1080p, up to 8 + 8 at 65536 tiles): its
+    instance order and ranges equal a plain stable sort of the depth-ordered
+    duplicates by tile id (projection.py:184-191) at every id width."""
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.rasterize.projection import project_field
+
+    f = GaussianField.from_host(scenes.make_params(1, seed=31, n=40000))
+    cam = scenes.camera(1, view=2, width=w, height=h)
+    sp = project_field(f, cam)
+    tx, ty = sp.tiles_x, sp.tiles_y
+    b = sp.bufs
+    order = b["depth_order"][: sp.n].long()
+    tiles = b["tiles"][: sp.n].long()
+    rect = b["rect"][: sp.n].view(-1, 4).long()
+    vis = order[tiles[order] > 0]  # visible rows in depth order
+    # duplicates in depth order, each row's tiles ty-outer / tx-inner
+    r = rect[vis]
+    wd, cnt = r[:, 2] - r[:, 0], tiles[vis]
+    idx = torch.repeat_interleave(torch.arange(vis.numel(), device=vis.device), cnt)
+    first = torch.cumsum(cnt, 0) - cnt
+    local = torch.arange(idx.numel(), device=vis.device) - first[idx]
+    row, col = local // wd[idx], local % wd[idx]
+    keys = (r[idx, 1] + row) * tx + r[idx, 0] + col
+    vals = vis[idx].int()
+    sk, perm = torch.sort(keys, stable=True)
+    assert keys.numel() == sp.n_instances and int(tx * ty) > 0
+    assert torch.equal(sp.inst_gauss, vals[perm])
+    n_tiles = tx * ty
+    t_ids = torch.arange(n_tiles, device=sk.device)
+    starts = torch.searchsorted(sk, t_ids, right=False)
+    ends = torch.searchsorted(sk, t_ids, right=True)
+    ranges = sp.tile_ranges.long()
+    assert torch.equal(ranges[:, 0], starts) and torch.equal(ranges[:, 1], ends)
+
+
+def test_tile_sort_rejects_more_than_65536_tiles():
+    from paper_2503_13086_b200 import GaussianField, scenes
+    from paper_2503_13086_b200.errors import InvalidParameter
+    from paper_2503_13086_b200.rasterize.projection import project_field
+
+    f = GaussianField.from_host(scenes.make_params(1, seed=31, n=2000))
+    with pytest.raises(InvalidParameter):
+        project_field(f, scenes.camera(1, view=2, width=4112, height=4096))  # 257 x 256 tiles
