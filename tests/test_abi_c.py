@@ -4,8 +4,9 @@ INTEGRATION.md section 2 tells a non-Python host to.
 
 * CPU: the host-only entry points (sizes, chunking, error reporting).
 * GPU: a whole render through caller-owned device buffers, bit-identical to
-  the package's render() of the same field and camera; and a backward + chain
-  from C, bit-identical to backward()."""
+  the package's render() of the same field and camera; a backward + chain
+  from C, bit-identical to backward(); and K whole training iterations from C
+  (render, loss, backward, chain + Adam), bit-identical to train_iteration()."""
 
 import ctypes
 import os
@@ -27,7 +28,7 @@ def _build(tmp_path):
     exe = str(tmp_path / "ssr_render")
     cmd = ["gcc", "-O2", "-std=c11", f"-I{ROOT}/include", "-I/usr/local/cuda/include",
            os.path.join(ROOT, "tests", "abi", "ssr_render.c"), "-o", exe, f"-L{LIBDIR}", "-lssr",
-           "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64"]
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lm", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     return exe
 
@@ -114,3 +115,48 @@ def test_c_host_backward_matches_python(tmp_path):
            for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh", "screen_norms")}
     for k, v in got.items():
         assert np.array_equal(v, getattr(g, k).cpu().numpy()), k
+
+
+@pytest.mark.gpu
+def test_c_host_training_matches_python(tmp_path):
+    import torch
+
+    from paper_2503_13086_b200 import GaussianField, _lib, scenes
+    from paper_2503_13086_b200.losses import LossWeights
+    from paper_2503_13086_b200.optim import (BETA1, BETA2, OPACITY_LR, ROTATION_LR, SCALE_LR, SH_DC_LR,
+                                             SH_REST_LR, FieldOptimizer)
+    from paper_2503_13086_b200.rasterize import render
+    from paper_2503_13086_b200.train import TrainState, train_iteration
+
+    exe = _build(tmp_path)
+    n, w, h, iters, rate, extent = 20000, 320, 240, 4, 1.6e-4, 3.0
+    hp = scenes.make_params(1, seed=23, n=n)
+    cam = scenes.camera(1, view=5, width=w, height=h)
+    tf = GaussianField.from_host(scenes.make_params(1, seed=24, n=n))
+    tgt = (render(tf, cam, for_backward=False).image * 255.0).round().clamp(0, 255).to(torch.uint8)
+    f = GaussianField.from_host(hp)
+    st = TrainState(field=f, optimizer=FieldOptimizer(f, scene_extent=extent),
+                    weights=LossWeights(l1=1.0, ssim=0.2, load=0.0), scene_extent=extent)
+    st.densify_enabled = False
+    for _ in range(iters):
+        br = train_iteration(st, cam, tgt, rate)
+    torch.cuda.synchronize()
+    src = tmp_path / "in.bin"
+    with open(src, "wb") as fh:
+        fh.write(np.int64(n).tobytes() + np.int32(f.sh_degree).tobytes())
+        fh.write(np.zeros(3).tobytes())
+        fh.write(bytes(_lib.camera_struct(cam)))
+        for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh"):
+            fh.write(np.ascontiguousarray(getattr(hp, k), dtype=np.float32).tobytes())
+        fh.write(np.array([rate * extent, ROTATION_LR, SCALE_LR, OPACITY_LR, SH_DC_LR, SH_REST_LR, BETA1, BETA2,
+                           1.0, 0.2], dtype=np.float64).tobytes())
+        fh.write(np.int32(iters).tobytes())
+        fh.write(tgt.cpu().numpy().tobytes())
+    dst = tmp_path / "out.bin"
+    run = subprocess.run([exe, str(src), str(dst), "--train"], capture_output=True, text=True, timeout=300)
+    assert run.returncode == 0, run.stderr
+    raw = np.fromfile(dst, dtype=np.uint8)
+    flat = raw[: 4 * f.flat.numel()].view(np.float32)
+    loss = raw[4 * f.flat.numel():].view(np.float64)
+    assert np.array_equal(flat, f.flat.cpu().numpy())
+    assert np.array_equal(loss[:4], np.array([br.l1, br.ssim_loss, br.load, br.total]))
