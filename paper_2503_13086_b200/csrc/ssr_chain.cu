@@ -256,6 +256,19 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
       st1 = stats[n + i];
     }
   }
+  // accumulating (view batches): the gradient entries this row adds to are
+  // requested now, so their latency overlaps the staging wait and the chain
+  float acc[13];
+  if (!FUSED && accumulate && mine && nt > 0) {
+    const float* gb[6] = {grads + i * 3, grads + 3 * ns + i * 4, grads + 7 * ns + i * 3, grads + 10 * ns + i,
+                          grads + (int64_t)S * ns + i, grads + (int64_t)(S + 1) * ns + i};
+    const int cnt[6] = {3, 4, 3, 1, 1, 1};
+    int e = 0;
+#pragma unroll
+    for (int b = 0; b < 6; b++)
+#pragma unroll
+      for (int j = 0; j < cnt[b]; j++) acc[e++] = gb[b][j];
+  }
   if (staged || FUSED) mbar_wait(&mbar, 0);
   if (!mine) return;
   // bincount merge (backward.py:110-118): ascending tile order; Gaussians with
@@ -471,13 +484,16 @@ __global__ void __launch_bounds__(CHAIN_ROWS) k_chain_geo(CamF cam, int64_t n, c
       dst[5] = dpos[2];
     }
   } else if (accumulate) {
-    if (vis) {
-      for (int j = 0; j < 3; j++) g_pos[i * 3 + j] += dpos[j];
-      for (int j = 0; j < 4; j++) g_rot[i * 4 + j] += grot[j];
-      for (int j = 0; j < 3; j++) g_ls[i * 3 + j] += dls[j];
-      g_logit[i] += pr[3];
-      g_screen[i] += screen;
-      g_vis[i] += 1.f;
+    if (vis) {  // acc: the entries read at entry (same order as below)
+#pragma unroll
+      for (int j = 0; j < 3; j++) g_pos[i * 3 + j] = acc[j] + dpos[j];
+#pragma unroll
+      for (int j = 0; j < 4; j++) g_rot[i * 4 + j] = acc[3 + j] + grot[j];
+#pragma unroll
+      for (int j = 0; j < 3; j++) g_ls[i * 3 + j] = acc[7 + j] + dls[j];
+      g_logit[i] = acc[10] + pr[3];
+      g_screen[i] = acc[11] + screen;
+      g_vis[i] = acc[12] + 1.f;
     }
   } else {
     for (int j = 0; j < 3; j++) g_pos[i * 3 + j] = dpos[j];
@@ -582,7 +598,6 @@ __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n,
   const float* rw = rows + ROWS_HEAD + (vis ? (int64_t)roff[ii] * ROW_WORDS : 0);
   float* shrow = sh + ii * W;
   float* grow = grads + 11 * ns + ii * W;
-
   // the lane's coefficients: c[ch][j] = sh[ch*K + q*KL + j] (an invisible
   // row's gradient is zero: no coefficient or position is read for it)
   float cf[3][KL];
