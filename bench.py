@@ -145,8 +145,8 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_mhz_min": float(np.min(self.samples)),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 def _dist():
@@ -737,7 +737,7 @@ def main():
         for name, extra in (("bench_objective", []), ("paper_objective", ["--paper-weights"])):
             try:
                 torch.cuda.empty_cache()
-                with contextlib.redirect_stdout(io.StringIO()):
+                with contextlib.redirect_stdout(io.StringIO()), ClockSampler(local, period=0.05) as pclk:
                     summ = prog.main(["--events", str(args.progressive_events), "--warmup-events", "1"] + extra)
                 progressive[name] = {
                     "metric": "seconds per new image", "value": summ["value"], "unit": "s/image",
@@ -745,6 +745,7 @@ def main():
                     "events": summ["events"],
                     "field_final": summ["field_final"], "objective": summ["objective"],
                     "value_with_reference_scheduler": summ["value_with_reference_scheduler"],
+                    "clocks": pclk.summary(),
                     "config": "config 3: 1297x840, +20k Gaussians per image, T_I = 200, reference build_plan / "
                               "lr_blended replayed, expansion + 2 render-only PSNRs included, wall clock"}
             except Exception as ex:  # pragma: no cover
