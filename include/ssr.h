@@ -193,10 +193,13 @@ int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const uint32_t* i
  * screen_norm N | visible N].  accumulate!=0 adds into it (view batches);
  * stats (optional, 2N: grad_accum, grad_count) get += screen_norm/visible.
  * inst_rows is the workspace ssr_backward just filled; it is consumed (the
- * chain parks merged colour gradients in it between its kernels). */
+ * chain parks merged colour gradients in it between its kernels).  row_list
+ * (optional, N + 1 uint32 of scratch; used with accumulate != 0): the SH pass
+ * then runs over the rows this view sees only (full warps), listed there. */
 int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
               const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
-              const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream);
+              const float* inst_rows, float* grads, int32_t accumulate, float* stats, uint32_t* row_list,
+              void* stream);
 
 /* backward.py:110-259 fused with optim.py:40-47,113-130: the chain of ssr_chain
  * followed by the dense Adam step of ssr_adam, without materialising

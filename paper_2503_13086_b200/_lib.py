@@ -63,7 +63,7 @@ _SIGS = {
     "ssr_backward": [c_int32, c_int64, SsrSplats, c_void_p, c_void_p, SsrFrame, c_void_p, c_void_p, c_void_p,
                      c_void_p],
     "ssr_chain": [ctypes.POINTER(SsrCamera), c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
-                  SsrSplats, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],
+                  SsrSplats, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p],
     "ssr_chain_adam": [ctypes.POINTER(SsrCamera), c_int64, c_int32, c_void_p, c_void_p, c_void_p, SsrSplats,
                        c_void_p, c_void_p, ctypes.POINTER(c_double), c_double, ctypes.POINTER(c_double),
                        ctypes.POINTER(c_double), c_void_p],

@@ -575,21 +575,53 @@ constexpr int SH_LANES = 4;
 constexpr int SH_THREADS = 256;
 constexpr int SH_ROWS = SH_THREADS / SH_LANES;
 
+// Accumulating (view batches): the field rows the view sees, listed (any
+// order: every row's update is independent), so the SH pass runs full warps
+// over them alone.  list[0] = count (zeroed beforehand), rows from list[1].
+constexpr int LIST_THREADS = 1024;
+__global__ void __launch_bounds__(LIST_THREADS) k_list_visible(int64_t n, const uint32_t* __restrict__ tiles,
+                                                               uint32_t* __restrict__ list) {
+  griddep_wait();
+  __shared__ uint32_t s_cnt[LIST_THREADS / 32];
+  __shared__ uint32_t s_base;
+  const int64_t i = (int64_t)blockIdx.x * LIST_THREADS + threadIdx.x;
+  const bool vis = i < n && tiles[i] != 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(FULLMASK, vis);
+  if (lane == 0) s_cnt[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one counter update per CTA, the warps' offsets in order
+    uint32_t run = 0;
+    for (int w = 0; w < LIST_THREADS / 32; w++) {
+      const uint32_t c = s_cnt[w];
+      s_cnt[w] = run;
+      run += c;
+    }
+    s_base = run ? atomicAdd(list, run) : 0u;
+  }
+  __syncthreads();
+  if (vis) list[1 + s_base + s_cnt[warp] + __popc(b & ((1u << lane) - 1u))] = (uint32_t)i;
+}
+
 // Lane q of a row owns coefficients k = q*KL + j (j < KL, k < K) of every
 // channel; at SH3 that is one float4 per channel, read and written directly.
+// list (optional, accumulating): the rows to process, from k_list_visible.
 template <int DEG>
 __global__ void __launch_bounds__(SH_THREADS, 4) k_chain_sh(CamF cam, int64_t n, float* __restrict__ pos,
                                                          float* __restrict__ sh, const uint32_t* __restrict__ tiles,
                                                          const uint32_t* __restrict__ roff,
                                                          const float4* __restrict__ color,
                                                          const float* __restrict__ rows, float* __restrict__ grads,
-                                                         int accumulate) {
+                                                         int accumulate, const uint32_t* __restrict__ list) {
   griddep_wait();
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int W = 3 * K;
   constexpr int KL = (K + 3) / 4;
   constexpr bool VEC = (K == 16);
-  const int64_t i = (int64_t)blockIdx.x * SH_ROWS + (threadIdx.x >> 2);
+  const int64_t slot = (int64_t)blockIdx.x * SH_ROWS + (threadIdx.x >> 2);
+  const int64_t n_slots = list ? (int64_t)list[0] : n;
+  if ((int64_t)blockIdx.x * SH_ROWS >= n_slots) return;  // the whole CTA is past the listed rows
+  const int64_t i = list ? (slot < n_slots ? (int64_t)list[1 + slot] : n) : slot;
   const int q = threadIdx.x & 3;
   const bool row_ok = i < n;
   const int64_t ii = row_ok ? i : n - 1;  // out-of-range lanes shadow the last row (shuffles need them)
@@ -883,7 +915,8 @@ using namespace ssr;
 template <bool FUSED>
 static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* positions, float* rotations,
                         float* log_scales, float* logits, float* sh, ssr_splats splats, float* rows, float* grads,
-                        int32_t accumulate, float* stats, const AdamArgsF& adam, cudaStream_t st) {
+                        int32_t accumulate, float* stats, const AdamArgsF& adam, cudaStream_t st,
+                        uint32_t* row_list = nullptr) {
   const CamF c = to_camf(*cam);
   const int K = (sh_degree + 1) * (sh_degree + 1);
   static int merge_blocks = 0;
@@ -939,10 +972,17 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
     return check_launch("k_chain_sh_adam");
   }
   const unsigned sblocks = (unsigned)((n + SH_ROWS - 1) / SH_ROWS);
+  const uint32_t* list = nullptr;
+  if (accumulate && row_list) {  // the view's visible rows only (full warps)
+    SSR_TRY(launch_pdl("row list zero", k_zero_words, dim3(1), dim3(32), 0, st, row_list, (int64_t)1));
+    SSR_TRY(launch_pdl("k_list_visible", k_list_visible, dim3((unsigned)((n + LIST_THREADS - 1) / LIST_THREADS)),
+                       dim3(LIST_THREADS), 0, st, n, (const uint32_t*)splats.tiles, row_list));
+    list = row_list;
+  }
 #define SSR_SH(D)                                                                                         \
   SSR_TRY(launch_pdl("k_chain_sh", k_chain_sh<D>, dim3(sblocks), dim3(SH_THREADS), 0, st, c, n, positions, sh, \
                      (const uint32_t*)splats.tiles, (const uint32_t*)splats.row_offset,                       \
-                     (const float4*)splats.color, (const float*)rows, grads, (int)accumulate))
+                     (const float4*)splats.color, (const float*)rows, grads, (int)accumulate, list))
   switch (sh_degree) {
     case 0: SSR_SH(0); break;
     case 1: SSR_SH(1); break;
@@ -955,7 +995,8 @@ static int launch_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, flo
 
 extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, const float* positions,
                          const float* rotations, const float* log_scales, const float* sh, ssr_splats splats,
-                         const float* inst_rows, float* grads, int32_t accumulate, float* stats, void* stream) {
+                         const float* inst_rows, float* grads, int32_t accumulate, float* stats, uint32_t* row_list,
+                         void* stream) {
   if (!cam || n < 0 || sh_degree < 0 || sh_degree > 3 || !grads) {
     set_error("ssr_chain: invalid argument");
     return SSR_ERR_INVALID;
@@ -966,7 +1007,8 @@ extern "C" int ssr_chain(const ssr_camera* cam, int64_t n, int32_t sh_degree, co
   // merged colour gradient in its own first row for the SH pass
   return launch_chain<false>(cam, n, sh_degree, const_cast<float*>(positions), const_cast<float*>(rotations),
                              const_cast<float*>(log_scales), nullptr, const_cast<float*>(sh), splats,
-                             const_cast<float*>(inst_rows), grads, accumulate, stats, none, (cudaStream_t)stream);
+                             const_cast<float*>(inst_rows), grads, accumulate, stats, none, (cudaStream_t)stream,
+                             row_list);
 }
 
 extern "C" int ssr_chain_adam(const ssr_camera* cam, int64_t n, int32_t sh_degree, float* params, float* m, float* v,

@@ -17,6 +17,21 @@ LAYOUTS = {"splat": 0, "pixel": 1}
 _ROWS: dict = {}
 
 
+_LISTS: dict = {}
+
+
+def _row_list(dev, n: int) -> torch.Tensor:
+    """N + 1 uint32 of scratch for ssr_chain's visible-row list (per device,
+    stream and host thread, like the rows workspace; grown on demand)."""
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _lib.stream_ptr(),
+           threading.get_ident())
+    buf = _LISTS.get(key)
+    if buf is None or buf.numel() < n + 1:
+        buf = torch.empty(n + 1 + (n + 1) // 8, dtype=torch.int32, device=dev)
+        _LISTS[key] = buf
+    return buf
+
+
 def rows_workspace(dev, m: int) -> torch.Tensor:
     """The ``inst_rows`` workspace of ssr_backward / ssr_chain (include/ssr.h)
     for the current device, stream and host thread: zero-filled when (re)allocated, then
@@ -150,9 +165,12 @@ def backward(field, out: RenderOutput, d_image, d_soft=None, layout: str = "spla
     if n:
         flat = field.flat
         sl = class_slices(n, k)
+        # accumulating (view batches): scratch for the list of the rows this view sees
+        row_list = _row_list(dev, n) if accumulate else None
         _lib.call("ssr_chain", _lib.camera_struct(cam), n, field.sh_degree, flat[sl[0][0]:].data_ptr(),
                   flat[sl[1][0]:].data_ptr(), flat[sl[2][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(), s,
-                  rows.data_ptr(), grads.flat.data_ptr(), 1 if accumulate else 0, _lib.ptr(stats), st)
+                  rows.data_ptr(), grads.flat.data_ptr(), 1 if accumulate else 0, _lib.ptr(stats),
+                  _lib.ptr(row_list), st)
     return grads
 
 

@@ -320,7 +320,7 @@ int main(int argc, char** argv) {
     const size_t g_floats = (size_t)(11 + 3 * K + 2) * ns;
     float* g = (float*)dalloc(4 * g_floats);
     SSR(ssr_backward(0, (int64_t)m, sp, inst, ranges, fr, dimg, NULL, rows, st));
-    SSR(ssr_chain(&cam, n, deg, pos, rot, lsc, sh, sp, rows, g, 0, NULL, st));
+    SSR(ssr_chain(&cam, n, deg, pos, rot, lsc, sh, sp, rows, g, 0, NULL, NULL, st));
     CK(cudaStreamSynchronize(st));
     float* gh = (float*)malloc(4 * g_floats);
     CK(cudaMemcpy(gh, g, 4 * g_floats, cudaMemcpyDeviceToHost));

@@ -98,7 +98,7 @@ def test_two_backwards_before_one_chain_abi():
     flat, sl = f.flat, class_slices(n, k)
     _lib.call("ssr_chain", _lib.camera_struct(cb), n, f.sh_degree, flat[sl[0][0]:].data_ptr(),
               flat[sl[1][0]:].data_ptr(), flat[sl[2][0]:].data_ptr(), flat[sl[4][0]:].data_ptr(), out_b.splats.struct(),
-              rows.data_ptr(), grads.flat.data_ptr(), 0, None, st)
+              rows.data_ptr(), grads.flat.data_ptr(), 0, None, None, st)
     torch.cuda.synchronize()
     assert torch.equal(grads.flat, ref)
 
