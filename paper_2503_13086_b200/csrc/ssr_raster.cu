@@ -617,18 +617,8 @@ template <bool SOFT>
 __device__ __forceinline__ void bw_pair(const float4& PB, const float4& w, int k, const BwSplat& s, BwAcc& g,
                                         float& T, float& H) {
   const int lim = __float_as_int(PB.w);
-#ifdef SSR_BW_PACKED
-  // (dx, dy) and (dxx, dyy) as packed pairs: each lane bit-identical to the
-  // scalar __fsub_rn / __fmul_rn the forward uses
-  const float2 d2 = f2_sub(f2_sub(make_float2(PB.x, PB.y), make_float2(s.sm.xi, s.sm.yi)),
-                           make_float2(s.sm.xf, s.sm.yf));
-  const float dx = d2.x, dy = d2.y;
-  const float2 sq = f2_mul(d2, d2);
-  const float dxx = sq.x, dyy = sq.y, dxy = __fmul_rn(dx, dy);
-#else
   const float dx = pair_d(PB.x, s.sm.xi, s.sm.xf), dy = pair_d(PB.y, s.sm.yi, s.sm.yf);
   const float dxx = __fmul_rn(dx, dx), dxy = __fmul_rn(dx, dy), dyy = __fmul_rn(dy, dy);
-#endif
   float qpos;
   const float p2 = pair_power2(dxx, dxy, dyy, s.q.a2, s.q.b2, s.q.c2, qpos);
   if (!SOFT) {
@@ -654,21 +644,10 @@ __device__ __forceinline__ void bw_pair(const float4& PB, const float4& w, int k
     // alpha = 0 and a finite dlda, so its gp is already zero
     const float gp = araw <= ALPHA_CAP_F ? dlda * alpha : 0.f;
     g.g3 += gp;
-#ifdef SSR_BW_PACKED
-    {
-      const float2 s2 = f2_fma(make_float2(gp, gp), d2, make_float2(g.sx, g.sy));
-      const float2 q2 = f2_fma(make_float2(gp, gp), sq, make_float2(g.g6, g.g8));
-      g.sx = s2.x;
-      g.sy = s2.y;
-      g.g6 = q2.x;
-      g.g8 = q2.y;
-    }
-#else
     g.sx = fmaf(gp, dx, g.sx);
     g.sy = fmaf(gp, dy, g.sy);
     g.g6 = fmaf(gp, dxx, g.g6);
     g.g8 = fmaf(gp, dyy, g.g8);
-#endif
     g.g7 = fmaf(gp, dxy, g.g7);
   } else {
     // same branch-free form with the soft-count term of every walked pair
