@@ -1195,12 +1195,16 @@ __global__ void __launch_bounds__(256, 2) k_backward_fixup(RasterArgs a, const f
   const bool soft_grad = d_soft != nullptr;
   const int* plan = fix_plan(a);
   for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_items; item += n_warps) {
-    // tile of this item: last plan entry <= item
-    int lo = 0, hi = n_ft - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (plan[mid] <= item) lo = mid;
-      else hi = mid - 1;
+    // tile of this item: the last plan entry <= item (the plan is
+    // non-decreasing), by a 32-way warp search: each level narrows the range
+    // 32x with one load per lane (3 dependent loads at 8160 tiles, not 13)
+    int lo = 0, hi = n_ft;
+    while (hi - lo > 1) {
+      const int step = (hi - lo + 31) >> 5;
+      const int idx = lo + lane * step;
+      const unsigned ok = __ballot_sync(FULL, idx < hi && plan[idx] <= item);  // lane 0 always
+      lo += (31 - __clz(ok)) * step;
+      hi = min(hi, lo + step);
     }
     const int it = lo;
     const int start = fix_tiles(a)[it];
