@@ -301,7 +301,9 @@ int ssr_ply_unpack(int64_t n, int32_t sh_degree, const double* records, float* p
  * like the reference's image loader io/images.py).
  * Writes d_image (HxWx3), d_soft (HxW) and out[5] = (l1, ssim_loss, load,
  * total, hard_count_std) as float64 in device memory.  soft_count may be NULL
- * when w_load == 0 and d_soft == NULL (a render without soft counts). */
+ * when w_load == 0 and d_soft == NULL (a render without soft counts).
+ * workspace: ssr_loss_workspace() bytes of device memory, 16-byte aligned
+ * (its adjoint maps are read back by TMA). */
 int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes);
 int ssr_loss(int32_t width, int32_t height, const float* image, const void* target, int32_t target_u8,
              const double* soft_count, const int32_t* hard_count, double w_l1, double w_ssim,

@@ -10,6 +10,8 @@
 // fixed order (so the scalars and d_soft are bit-identical run to run) and
 // turns them into the scalars.  k_ssim_bwd blurs the adjoint maps (the window is self-adjoint)
 // and writes d_image and d_soft.
+#include <cuda.h>
+
 #include "ssr_common.cuh"
 
 namespace ssr {
@@ -60,6 +62,19 @@ constexpr int HITEMS = LH * (LT / HSEG);  // 168
 constexpr int VSEG = 4;                 // vertical outputs per thread (32 x 8 = 256 items)
 constexpr int HZS = LT + 1;             // padded row stride of the horizontal results
 
+// The adjoint maps are stored with a zero border of HALO columns on the left
+// and HALO rows on top (written by the forward) and rows padded to 4 floats
+// (16-byte TMA global strides).  The backward loads each channel's three halo
+// tiles with one 3-D TMA copy at non-negative coordinates (a negative tile
+// origin faults on this hardware), its rows BP floats apart (16-byte multiple;
+// the columns past LH are loaded and not read); past the right and bottom edges
+// the copy fills zeros.  Both are the SSIM window's zero padding.
+__host__ __device__ __forceinline__ int map_pitch(int W) { return (W + HALO + 3) & ~3; }
+__host__ __device__ __forceinline__ size_t map_stride(int W, int H) { return (size_t)map_pitch(W) * (H + HALO); }
+constexpr int BP = 44;
+constexpr uint32_t BW_TILE_BYTES = 3 * LH * BP * 4;
+constexpr uint32_t BW_BUF_BYTES = (BW_TILE_BYTES + 127) & ~127u;  // TMA destinations: 128-byte aligned
+
 template <bool U8>
 __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* __restrict__ img,
                                                   const Target tgt, const double* __restrict__ soft,
@@ -71,8 +86,24 @@ __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* 
   __shared__ double red[8];
   const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
   const int tid = threadIdx.x;
-  const size_t HW = (size_t)W * H;
+  const int Wp = map_pitch(W);
+  const size_t MS = map_stride(W, H);
   const int n_crop_w = W - 2 * HALO, n_crop_h = H - 2 * HALO;
+  // the maps' zero borders: top rows by the first CTA row, left columns by the
+  // first CTA column
+  if (blockIdx.y == 0) {
+    for (int e = tid; e < 9 * HALO * (LT + HALO); e += blockDim.x) {
+      const int k = e / (HALO * (LT + HALO)), rr = (e / (LT + HALO)) % HALO, cc = e % (LT + HALO);
+      const int col = cc < HALO ? (blockIdx.x == 0 ? cc : -1) : (c0 + cc - HALO < W ? c0 + cc : -1);
+      if (col >= 0) dmaps[k * MS + (size_t)rr * Wp + col] = 0.f;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < 9 * LT * HALO; e += blockDim.x) {
+      const int k = e / (LT * HALO), rr = (e / HALO) % LT, cc = e % HALO;
+      if (r0 + rr < H) dmaps[k * MS + (size_t)(r0 + rr + HALO) * Wp + cc] = 0.f;
+    }
+  }
   const double mw = 1.0 / ((double)n_crop_w * n_crop_h * 3.0);
   const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
   float wv[11];
@@ -85,9 +116,9 @@ __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* 
   const bool ina = gca >= 0 && gca < W, inb = cb < LH && gcb >= 0 && gcb < W;
   for (int ch = 0; ch < 3; ch++) {
     const float* imc = img + ch;
-    float* dm0 = dmaps + (size_t)(ch * 3 + 0) * HW;
-    float* dm1 = dmaps + (size_t)(ch * 3 + 1) * HW;
-    float* dm2 = dmaps + (size_t)(ch * 3 + 2) * HW;
+    float* dm0 = dmaps + (size_t)(ch * 3 + 0) * MS + HALO * Wp + HALO;  // pixel (0, 0)
+    float* dm1 = dmaps + (size_t)(ch * 3 + 1) * MS + HALO * Wp + HALO;
+    float* dm2 = dmaps + (size_t)(ch * 3 + 2) * MS + HALO * Wp + HALO;
     // two rows per pass, all eight loads issued before the stores
     for (int r = tid >> 5; r < LH; r += 16) {
       float v[2][4];
@@ -193,7 +224,7 @@ __global__ void __launch_bounds__(256, 4) k_ssim_fwd(int W, int H, const float* 
         const float i1 = __frcp_rn(b1), i2 = __frcp_rn(b2), i12 = i1 * i2;
         const float smap = (a1 * a2) * i12;
         const bool crop = gr >= HALO && gr < H - HALO && gc >= HALO && gc < W - HALO;
-        const int pi = gr * W + gc;
+        const int pi = gr * Wp + gc;
         float dmu = 0.f, dg2 = 0.f, dxy = 0.f;
         if (crop) {
           ssf += smap;
@@ -290,62 +321,83 @@ __global__ void __launch_bounds__(FIN_THREADS) k_loss_finalize(int W, int H, dou
   out[4] = varh > 0.0 ? sqrt(varh) : 0.0;
 }
 
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar))
+      : "memory");
+}
+
+// Dynamic shared memory of k_ssim_bwd: two channel buffers of the three halo
+// tiles (TMA destinations, 128-byte aligned), the horizontal results, two
+// mbarriers.
+constexpr size_t BW_SMEM = 2 * (size_t)BW_BUF_BYTES + sizeof(float) * 3 * LH * HZS + 16;
+
+// One elected thread loads channel 0 and 1's adjoint tiles by TMA at entry
+// and channel 2's into the first buffer once channel 0's horizontal pass has
+// read it, so every tile load overlaps the blur of the previous channel.
 template <bool U8>
-__global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __restrict__ img,
-                                                  const Target tgt, const double* __restrict__ soft,
-                                                  const float* __restrict__ dmaps, const LossAcc* __restrict__ acc,
+__global__ void __launch_bounds__(256) k_ssim_bwd(const __grid_constant__ CUtensorMap tmap, int W, int H,
+                                                  const float* __restrict__ img, const Target tgt,
+                                                  const double* __restrict__ soft, const LossAcc* __restrict__ acc,
                                                   double w_l1, double w_ssim, double w_load,
                                                   float* __restrict__ d_image, float* __restrict__ d_soft) {
-  griddep_wait();
-  __shared__ float sm[3][LH][LH + 1];
-  __shared__ float hz[3][LH][HZS];
+  extern __shared__ __align__(128) unsigned char smem[];
+  float(*buf[2])[LH][BP] = {reinterpret_cast<float(*)[LH][BP]>(smem),
+                            reinterpret_cast<float(*)[LH][BP]>(smem + BW_BUF_BYTES)};
+  float(*hz)[LH][HZS] = reinterpret_cast<float(*)[LH][HZS]>(smem + 2 * BW_BUF_BYTES);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * BW_BUF_BYTES + sizeof(float) * 3 * LH * HZS);
   const int c0 = blockIdx.x * LT, r0 = blockIdx.y * LT;
   const int tid = threadIdx.x;
   const size_t HW = (size_t)W * H;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+  }
+  __syncthreads();
+  griddep_wait();  // the maps are the forward's output
+  if (tid == 0) {
+#pragma unroll
+    for (int ch = 0; ch < 2; ch++) {
+      mbar_expect_tx(&mbar[ch], BW_TILE_BYTES);
+      tma_load_3d(&buf[ch][0][0][0], &tmap, c0, r0, ch * 3, &mbar[ch]);  // padded coordinates
+    }
+  }
   const float gl1 = (float)(w_l1 / (double)(HW * 3));
   const float gss = (float)w_ssim;
   float wv[11];
 #pragma unroll
   for (int t = 0; t < 11; t++) wv[t] = c_win[t];
-  const int ca = tid & 31, cb = ca + 32;
-  const int gca = c0 - HALO + ca, gcb = c0 - HALO + cb;
-  const bool ina = gca >= 0 && gca < W, inb = cb < LH && gcb >= 0 && gcb < W;
   for (int ch = 0; ch < 3; ch++) {
-    const float* dm[3] = {dmaps + (size_t)(ch * 3 + 0) * HW, dmaps + (size_t)(ch * 3 + 1) * HW,
-                          dmaps + (size_t)(ch * 3 + 2) * HW};
-    // two rows per pass, all twelve loads issued before the stores
-    for (int r = tid >> 5; r < LH; r += 16) {
-      float v[2][3][2];
-#pragma unroll
-      for (int u = 0; u < 2; u++) {
-        const int rr = r + 8 * u;
-        const int gr = r0 - HALO + rr;
-        const bool rin = rr < LH && gr >= 0 && gr < H;
-        const int row = gr * W;
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-          v[u][k][0] = rin && ina ? dm[k][row + gca] : 0.f;
-          v[u][k][1] = rin && inb ? dm[k][row + gcb] : 0.f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 2; u++) {
-        const int rr = r + 8 * u;
-        if (rr >= LH) break;
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-          sm[k][rr][ca] = v[u][k][0];
-          if (cb < LH) sm[k][rr][cb] = v[u][k][1];
-        }
-      }
-    }
-    __syncthreads();
+    const int b = ch & 1;
+    mbar_wait(&mbar[b], ch >> 1);
+    float(*sm)[LH][BP] = buf[b];
     if (tid < HITEMS) {
       const int r = tid / (LT / HSEG), cs = (tid % (LT / HSEG)) * HSEG;
+      // 18 consecutive floats of a row: four 16-byte and one 8-byte load
+      // (conflict-free: the rows are 44 floats apart)
+      float row[3][HSEG + 10];
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        const float4* q = reinterpret_cast<const float4*>(&sm[k][r][cs]);
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const float4 x = q[v];
+          row[k][4 * v] = x.x;
+          row[k][4 * v + 1] = x.y;
+          row[k][4 * v + 2] = x.z;
+          row[k][4 * v + 3] = x.w;
+        }
+        const float2 x = *reinterpret_cast<const float2*>(&sm[k][r][cs + 16]);
+        row[k][16] = x.x;
+        row[k][17] = x.y;
+      }
       {  // maps 0 and 1 as lane pairs, then map 2
         float2 xv[HSEG + 10];
 #pragma unroll
-        for (int j = 0; j < HSEG + 10; j++) xv[j] = make_float2(sm[0][r][cs + j], sm[1][r][cs + j]);
+        for (int j = 0; j < HSEG + 10; j++) xv[j] = make_float2(row[0][j], row[1][j]);
 #pragma unroll
         for (int o = 0; o < HSEG; o++) {
           float2 v = make_float2(0.f, 0.f);
@@ -355,20 +407,19 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(int W, int H, const float* __r
           hz[1][r][cs + o] = v.y;
         }
       }
-      {
-        float xv[HSEG + 10];
 #pragma unroll
-        for (int j = 0; j < HSEG + 10; j++) xv[j] = sm[2][r][cs + j];
+      for (int o = 0; o < HSEG; o++) {
+        float v = 0.f;
 #pragma unroll
-        for (int o = 0; o < HSEG; o++) {
-          float v = 0.f;
-#pragma unroll
-          for (int t = 0; t < 11; t++) v = fmaf(wv[t], xv[o + t], v);
-          hz[2][r][cs + o] = v;
-        }
+        for (int t = 0; t < 11; t++) v = fmaf(wv[t], row[2][o + t], v);
+        hz[2][r][cs + o] = v;
       }
     }
     __syncthreads();
+    if (ch == 0 && tid == 0) {  // buffer 0 is free: channel 2's tiles
+      mbar_expect_tx(&mbar[0], BW_TILE_BYTES);
+      tma_load_3d(&buf[0][0][0][0], &tmap, c0, r0, 6, &mbar[0]);
+    }
     {
       const int c = tid % LT, rs = (tid / LT) * VSEG;
       float bm[3][VSEG];
@@ -449,8 +500,45 @@ static int64_t loss_ctas(int32_t width, int32_t height) {
   return (int64_t)((width + LT - 1) / LT) * ((height + LT - 1) / LT);
 }
 
+static int64_t maps_bytes(int32_t width, int32_t height) {
+  return align_up((int64_t)9 * map_stride(width, height) * 4, 256);
+}
+
+// The 3-D tensor map over the nine adjoint maps (x: column, y: row, z: map),
+// box = one channel's three halo tiles.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int maps_tensor_map(CUtensorMap* m, float* dmaps, int32_t width, int32_t height) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SSR_TRY(check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+                       "cuTensorMapEncodeTiled entry point"));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("ssr_loss: cuTensorMapEncodeTiled unavailable");
+      return SSR_ERR_CUDA;
+    }
+    encode = (EncodeTiledFn)fn;
+  }
+  const cuuint64_t pitch = (cuuint64_t)map_pitch(width) * 4;
+  const cuuint64_t dims[3] = {(cuuint64_t)width + HALO, (cuuint64_t)height + HALO, 9};
+  const cuuint64_t strides[2] = {pitch, (cuuint64_t)map_stride(width, height) * 4};
+  const cuuint32_t box[3] = {BP, LH, 3};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dmaps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("ssr_loss: cuTensorMapEncodeTiled failed");
+    return SSR_ERR_CUDA;
+  }
+  return SSR_OK;
+}
+
 extern "C" int ssr_loss_workspace(int32_t width, int32_t height, int64_t* bytes) {
-  *bytes = align_up((int64_t)9 * width * height * 4, 256) + align_up(sizeof(LossAcc), 256) +
+  *bytes = maps_bytes(width, height) + align_up(sizeof(LossAcc), 256) +
            align_up(loss_ctas(width, height) * LOSS_TERMS * 8, 256);
   return SSR_OK;
 }
@@ -469,8 +557,8 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   }
   int64_t need = 0;
   ssr_loss_workspace(width, height, &need);
-  if (workspace_bytes < need) {
-    set_error("ssr_loss: workspace too small");
+  if (workspace_bytes < need || ((uintptr_t)workspace & 15)) {
+    set_error("ssr_loss: workspace too small or not 16-byte aligned");
     return SSR_ERR_INVALID;
   }
   if (!soft_count && (w_load > 0.0 || d_soft)) {
@@ -480,7 +568,7 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   SSR_TRY(ensure_window());
   cudaStream_t st = (cudaStream_t)stream;
   float* dmaps = (float*)workspace;
-  LossAcc* acc = (LossAcc*)((char*)workspace + align_up((int64_t)9 * width * height * 4, 256));
+  LossAcc* acc = (LossAcc*)((char*)workspace + maps_bytes(width, height));
   double* partials = (double*)((char*)acc + align_up(sizeof(LossAcc), 256));
   dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
   const Target tg{target, target_u8 ? 1 : 0};
@@ -494,11 +582,23 @@ extern "C" int ssr_loss(int32_t width, int32_t height, const float* image, const
   SSR_TRY(launch_pdl("k_loss_finalize", k_loss_finalize, dim3(1), dim3(FIN_THREADS), 0, st, width, height, w_l1,
                      w_ssim, w_load, soft_count, (const double*)partials, (int)loss_ctas(width, height), acc, out));
   SSR_TRY(check_launch("k_loss_finalize"));
+  CUtensorMap tmap;
+  SSR_TRY(maps_tensor_map(&tmap, dmaps, width, height));
+  static DeviceOnce attr;
+  if (!attr.done()) {
+    SSR_TRY(check_cuda(cudaFuncSetAttribute(k_ssim_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)BW_SMEM),
+                       "k_ssim_bwd smem"));
+    SSR_TRY(check_cuda(cudaFuncSetAttribute(k_ssim_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)BW_SMEM),
+                       "k_ssim_bwd smem"));
+    attr.set();
+  }
   if (tg.u8)
-    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<true>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
-                       (const float*)dmaps, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
+    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<true>, grid, dim3(256), BW_SMEM, st, tmap, width, height, image, tg,
+                       soft_count, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
   else
-    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<false>, grid, dim3(256), 0, st, width, height, image, tg, soft_count,
-                       (const float*)dmaps, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
+    SSR_TRY(launch_pdl("k_ssim_bwd", k_ssim_bwd<false>, grid, dim3(256), BW_SMEM, st, tmap, width, height, image, tg,
+                       soft_count, (const LossAcc*)acc, w_l1, w_ssim, w_load, d_image, d_soft));
   return check_launch("k_ssim_bwd");
 }
