@@ -652,7 +652,7 @@ def main():
         fwd_ms = stage_ms.get("ssr_forward", 0.0)
         bwd_ms = stage_ms.get("ssr_backward", 0.0)
         if bwd_ms >= fwd_ms:
-            dom, flops, dms = ("ssr_backward (k_backward_splat2 + k_backward_fixup; k_backward_splat when d_soft != 0)",
+            dom, flops, dms = ("ssr_backward (k_backward_splat2 + k_backward_fixup)",
                                FLOP_BWD_PER_PAIR * P_mean, bwd_ms)
         else:
             dom, flops, dms = "ssr_forward (k_forward + k_forward_fixup)", FLOP_FWD_PER_PAIR * P_mean, fwd_ms

@@ -78,8 +78,8 @@ typedef struct ssr_frame {
   uint8_t* terminated; /* H x W */
   int32_t* hard_count; /* H x W */
   double* soft_count;  /* H x W  float64: counts reach 10^4, the bar is 1e-4 absolute.  NULL:
-                        * no soft counts (the walk culls pairs below 1/255); the frame then
-                        * keeps 64-slot checkpoints and ssr_backward layout 0 takes no d_soft */
+                        * no soft counts (the walk culls pairs below 1/255); ssr_backward
+                        * layout 0 then takes no d_soft */
   uint8_t* flagged;    /* H x W  1 = pixel re-walked in fp64 (guard band) */
   int32_t* tile_info;  /* n_tiles x 4  (max n_walk, flagged pixel count, max n_walk of a flagged pixel, 0) */
   float* ckpt;         /* ssr_ckpt_floats(M, n_tiles) floats: (T, C_front rgb) per bucket/pixel */

@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(256) k_forward(RasterArgs a) {
       const int n = min(FWD_BATCH, s1 - base);
       const int k0 = base - s0;
       for (int j0 = 0; j0 < n; j0 += BUCKET) {
-        if (k0 + j0) {  // bucket checkpoint for the splat-parallel backward
-          // without soft counts only the two-slot backward (64-slot buckets)
-          // can follow: every other checkpoint, half the writes
-          if (CK && (SOFT || ((k0 + j0) & 63) == 0))
+        if (k0 + j0) {  // checkpoint for the splat-parallel backward: its
+          // buckets hold 64 slots, so every other 32-slot boundary (the fp64
+          // fix-up writes its flagged pixels' own at every 32)
+          if (CK && ((k0 + j0) & 63) == 0)
             ck[(size_t)((k0 + j0) >> 5) * TILE_PX] = make_float4(q.T, q.c0, q.c1, q.c2);
           q.sbig += (double)q.sdev;
           q.sdev = 0.f;
@@ -570,18 +570,25 @@ __global__ void k_fix_reset(int* fix) {
 }
 
 // ------------------------------------------------------------------ backward, splat-parallel (fp32)
-// Taming-style: one warp per (tile, 32-splat bucket); lane l owns slot
-// 32b+l and accumulates its 9 gradient terms in registers while the bucket's
-// live pixels stream through the warp as a systolic pipeline: at step i lane
-// l handles live pixel i-l and receives that pixel's running (T, H = w.C_front)
-// from lane l-1 by shuffle.  Lane 0 seeds each pixel from the forward's
-// bucket checkpoint.  No atomics; each instance row is written once.
+// Taming-style: one warp per (tile, 64-splat bucket); lane l owns slots
+// 64b+2l and 64b+2l+1 and accumulates their 9 gradient terms in registers
+// while the bucket's live pixels stream through the warp as a systolic
+// pipeline: at step i lane l handles live pixel i-l and receives that pixel's
+// running (T, H = w.C_front) from lane l-1 by shuffle.  Lane 0 seeds each pixel
+// from the forward's checkpoint at the bucket start.  No atomics; each
+// instance row is written once.
 //
 // The pixel list of a bucket is padded with 32 sentinel entries on both sides
 // (pixel 256: blend limit 0), so the stream needs no bounds checks.  The mean
 // gradient is accumulated as sum(gp dx), sum(gp dy) and mapped through the
 // conic once per row (linear), so a contributing pair costs ~30 instructions.
-constexpr int BW2_MIN_BLOCKS = 3;  // 80 registers: 24 warps per SM (2 blocks: 125 registers, no faster)
+//
+// Without a soft-count gradient: 80 registers, 24 warps per SM (2 blocks:
+// 125 registers, no faster).  With one the soft pair block needs more: 125
+// registers, 16 warps per SM (3 blocks rematerialise addresses in the loop:
+// 2.6 % slower; the former one-slot kernel with 32-slot buckets: 1.3 %).
+constexpr int BW2_MIN_BLOCKS = 3;
+constexpr int BW2_SOFT_MIN_BLOCKS = 2;
 constexpr int BW_PAD = 32;
 constexpr int BW_LIST = BW_PAD + TILE_PX + BW_PAD;
 
@@ -601,7 +608,7 @@ struct BwAcc {
 // alpha below the cap adds its soft term.  The pixel list holds byte offsets
 // (p * 16) shared by both per-pixel arrays; the next step's records are
 // fetched one step ahead.
-// Per-pixel records of the tile being differentiated (k_backward_splat), at
+// Per-pixel records of the tile being differentiated (k_backward_splat2), at
 // file scope so the stream addresses them as list offset + constant base.
 // sPA: dL/dr, dL/dg, dL/db, dL/dsoft; sPB: pixel x, y (tile-relative),
 // w . image, walk limit; entry [256] = sentinel.  One array, so a pixel's two
@@ -683,38 +690,10 @@ __device__ __forceinline__ void bw_pair(const float4& PB, const float4& w, int k
   }
 }
 
-template <bool SOFT>
-__device__ __forceinline__ void bw_stream(
-                                          const uint16_t* __restrict__ list, const float2* __restrict__ seed,
-                                          int n_live, int lane, int k, const BwSplat& s, BwAcc& g) {
-  float T = 1.f, H = 0.f;
-  const int n_steps = n_live + 31;
-  const bool lane0 = lane == 0;
-  int jn = BW_PAD - lane;  // padded list index of step 0
-  int on = list[jn];       // byte offset of the pixel's record in sPA / sPB
-  const char* sPixb = reinterpret_cast<const char*>(sPix);
-  constexpr int B_OFF = (TILE_PX + 1) * sizeof(float4);
-  float4 PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF), PAn = *reinterpret_cast<const float4*>(sPixb + on);
-#pragma unroll 2
-  for (int i = 0; i < n_steps; i++) {
-    float Tin = __shfl_up_sync(FULL, T, 1);
-    float Hin = __shfl_up_sync(FULL, H, 1);
-    const float2 sd = seed[i];  // broadcast read (garbage past n_live: sentinel steps)
-    T = lane0 ? sd.x : Tin;
-    H = lane0 ? sd.y : Hin;
-    const float4 PB = PBn, w = PAn;
-    jn++;
-    on = list[jn];
-    PBn = *reinterpret_cast<const float4*>(sPixb + on + B_OFF);
-    PAn = *reinterpret_cast<const float4*>(sPixb + on);
-    bw_pair<SOFT>(PB, w, k, s, g, T, H);
-  }
-}
-
 // Two consecutive slots per lane (64-slot buckets, k_backward_splat2): lane l
 // owns slots k and k + 1; each pixel record read from shared memory and each
-// (T, H) hand-off by shuffle serves two pairs (the one-slot stream runs at
-// 86% of the LSU wavefront peak; this one at 49%, limited by occupancy).
+// (T, H) hand-off by shuffle serves two pairs (a one-slot stream ran at 86%
+// of the LSU wavefront peak; this one at 49%, limited by occupancy).
 template <bool SOFT>
 __device__ __forceinline__ void bw_stream2(const uint16_t* __restrict__ list, const float2* __restrict__ seed,
                                            int n_live, int lane, int k, const BwSplat& s0, const BwSplat& s1,
@@ -744,138 +723,8 @@ __device__ __forceinline__ void bw_stream2(const uint16_t* __restrict__ list, co
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_backward_splat(RasterArgs a, const float* __restrict__ d_image,
-                                                        const float* __restrict__ d_soft, float* __restrict__ rows) {
-  griddep_wait();
-  const int t = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int2 rg = a.ranges[t];
-  const int s0 = rg.x, len = rg.y - rg.x;
-  if (len == 0) return;
-  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-  const int x00 = tx * TILE, y00 = ty * TILE;
-  const int maxw = a.tile_info[t].x;
-  const uint32_t gen = rows_generation(rows) + 1;  // k_fix_plan publishes it after this grid
-
-  __shared__ float2 sSeed[8][TILE_PX + 32];  // per warp: (T, H) entering the bucket, i-th live pixel
-  __shared__ uint16_t sList[8][BW_LIST];     // per warp: byte offsets of the bucket's live pixel records, padded
-  bool soft_px = false;
-  {
-    const int px = x00 + (tid & 15), py = y00 + (tid >> 4);
-    int nw = 0, term = 0;
-    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-    float wimg = 0.f;
-    if (px < a.width && py < a.height) {
-      const size_t pix = (size_t)py * a.width + px;
-      if (!a.flagged[pix]) {
-        nw = a.n_walk[pix];
-        term = a.term[pix] ? 1 : 0;
-      } else {
-        nw = fix_kflag(a)[pix];  // slots before the ambiguous one; the fp64 fix-up adds the rest
-      }
-      w = make_float4(d_image[pix * 3], d_image[pix * 3 + 1], d_image[pix * 3 + 2], d_soft ? d_soft[pix] : 0.f);
-      wimg = w.x * a.image[pix * 3] + w.y * a.image[pix * 3 + 1] + w.z * a.image[pix * 3 + 2];
-    }
-    soft_px = w.w != 0.f;
-    sPA[tid] = w;
-    // does any pixel of the tile carry a soft-count gradient?  If not, pairs
-    // with alpha < 1/255 (and terminating slots) contribute exactly nothing.
-    const bool us = __syncthreads_or(soft_px);
-    const int lim = us ? ((nw << 1) | term) : nw - term;
-    sPB[tid] = make_float4((float)(tid & 15), (float)(tid >> 4), wimg, __int_as_float(lim));
-    if (tid < 8)
-      for (int e = 0; e < BW_PAD; e++) {
-        sList[tid][e] = TILE_PX * sizeof(float4);
-        sList[tid][BW_PAD + TILE_PX + e] = TILE_PX * sizeof(float4);
-      }
-    if (tid == 0) {
-      sPA[TILE_PX] = make_float4(0.f, 0.f, 0.f, 0.f);
-      sPB[TILE_PX] = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
-    }
-    soft_px = us;
-  }
-  __syncthreads();
-  const bool use_soft = soft_px;
-
-  const int nb = (maxw + 31) >> 5;
-  const float4* ckt = a.ckpt + ckpt_base(s0, t);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  uint16_t* const myList = sList[warp] + BW_PAD;
-  float2* const mySeed = sSeed[warp];
-  // buckets over the CTA's warps and, for images of few tiles, over gridDim.y
-  // CTAs of the same tile (each a copy of the pixel set-up)
-  for (int b = warp + 8 * (int)blockIdx.y; b < nb; b += 8 * (int)gridDim.y) {
-    const int kb = b * 32;
-    // live pixels of this bucket: the walk reaches slot kb (compacted, pixel order)
-    int n_live = 0;
-#pragma unroll
-    for (int c = 0; c < 8; c++) {
-      const int p = c * 32 + lane;
-      const int lim = __float_as_int(sPB[p].w);
-      const bool lv = (use_soft ? (lim >> 1) : lim) > kb;
-      const unsigned msk = __ballot_sync(FULL, lv);
-      if (lv) myList[n_live + __popc(msk & lt_mask)] = (uint16_t)(p * sizeof(float4));
-      n_live += __popc(msk);
-    }
-    // sentinels after the live pixels (the padding after 256 entries is fixed)
-    if (n_live + lane < TILE_PX) myList[n_live + lane] = TILE_PX * sizeof(float4);
-    __syncwarp();
-    for (int j = lane; j < n_live; j += 32) {
-      const int p = myList[j] / sizeof(float4);
-      float2 sd = make_float2(1.f, 0.f);
-      if (b > 0) {
-        const float4 c = ckt[(size_t)b * TILE_PX + p];
-        const float4 w = sPA[p];
-        sd = make_float2(c.x, w.x * c.y + w.y * c.z + w.z * c.w);
-      }
-      mySeed[j] = sd;
-    }
-    // the sentinel steps after the live pixels read finite seeds: the
-    // branch-free pair blocks multiply them by zero
-    mySeed[n_live + lane] = make_float2(1.f, 0.f);
-    __syncwarp();
-    const int k = kb + lane;
-    const bool live = k < maxw;
-    BwSplat s;
-    s.sm = {0.f, 0.f, 0.f, 0.f};
-    s.q = {0.f, 0.f, 0.f};
-    s.opa = s.cr = s.cg = s.cbl = 0.f;
-    s.p2_min = __int_as_float(0x7f800000);  // +inf: lanes past the walks never contribute
-    float ca = 0.f, cb = 0.f, cc = 0.f;
-    uint32_t orow = 0;
-    if (live) {
-      const uint32_t g = a.inst[s0 + k];
-      const double2 m = a.mean[g];
-      const float4 co = a.conic_opa[g];
-      const float4 col = a.color[g];
-      s.sm = stage_mean(m.x, m.y, x00, y00);
-      ca = co.x;
-      cb = co.y;
-      cc = co.z;
-      s.opa = fabsf(co.w);
-      s.q = stage_conic(ca, cb, cc);
-      s.cr = col.x;
-      s.cg = col.y;
-      s.cbl = col.z;
-      orow = inst_row(a, g, tx, ty);
-      // without soft gradients only alpha >= 1/255 matters: alpha < 0.999/255
-      // is certain below log2(0.999 / (255 opacity))
-      s.p2_min = use_soft ? FAR_POWER2 : fmaxf(FAR_POWER2, __log2f(0.999f * ALPHA_MIN_F / s.opa));
-    }
-    BwAcc g = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (use_soft)
-      bw_stream<true>(sList[warp], mySeed, n_live, lane, k, s, g);
-    else
-      bw_stream<false>(sList[warp], mySeed, n_live, lane, k, s, g);
-    if (live)
-      store_row(rows, orow, g.g0, g.g1, g.g2, g.g3 * (1.f - s.opa), ca * g.sx + cb * g.sy, cb * g.sx + cc * g.sy,
-                -0.5f * g.g6, -g.g7, -0.5f * g.g8, gen);
-    __syncwarp();
-  }
-  // slots k >= maxw: no row (their tag stays stale, ssr_common.cuh)
-}
-
-__global__ void __launch_bounds__(256, BW2_MIN_BLOCKS) k_backward_splat2(RasterArgs a, const float* __restrict__ d_image,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_backward_splat2(RasterArgs a, const float* __restrict__ d_image,
                                                         const float* __restrict__ d_soft, float* __restrict__ rows) {
   griddep_wait();
   const int t = blockIdx.x;
@@ -1405,8 +1254,7 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
     return SSR_ERR_INVALID;
   }
   if (d_soft && !frame.soft_count && layout == 0) {
-    set_error("ssr_backward: a soft-count gradient needs a frame rendered with soft counts "
-              "(without them the forward keeps 64-slot checkpoints only)");
+    set_error("ssr_backward: a soft-count gradient needs a frame rendered with soft counts");
     return SSR_ERR_INVALID;
   }
   if (!frame.fix_list || !inst_rows) {
@@ -1418,20 +1266,19 @@ extern "C" int ssr_backward(int32_t layout, int64_t m, ssr_splats splats, const 
   // the grid still fills the GPU (bucket rows are disjoint: no conflicts)
   const int split = max(1, min(8, (num_sms() * 4 + n_tiles - 1) / n_tiles));
   if (layout == 0) {
-    // no soft-count gradient (d_soft NULL): two slots per lane, 64-slot buckets
-    // (fewer shared-memory and shuffle wavefronts per pair, -1.4%); with one,
-    // the soft pair block needs the registers of the one-slot kernel
+    // two slots per lane, 64-slot buckets; the soft pair block (d_soft given)
+    // needs more registers
     if (!d_soft)
-      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2, dim3(n_tiles, split), dim3(TILE_PX), 0, st, a,
-                         d_image, d_soft, inst_rows));
+      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2<BW2_MIN_BLOCKS>, dim3(n_tiles, split), dim3(TILE_PX), 0,
+                         st, a, d_image, d_soft, inst_rows));
     else
-      SSR_TRY(launch_pdl("k_backward_splat", k_backward_splat, dim3(n_tiles, split), dim3(TILE_PX), 0, st, a,
-                         d_image, d_soft, inst_rows));
+      SSR_TRY(launch_pdl("k_backward_splat2", k_backward_splat2<BW2_SOFT_MIN_BLOCKS>, dim3(n_tiles, split),
+                         dim3(TILE_PX), 0, st, a, d_image, d_soft, inst_rows));
   }
   else
     SSR_TRY(launch_pdl("k_backward_pixel", k_backward_pixel, dim3(n_tiles), dim3(TILE_PX), 0, st, a, d_image, d_soft,
                        inst_rows));
-  SSR_TRY(check_launch(layout == 0 ? "k_backward_splat" : "k_backward_pixel"));
+  SSR_TRY(check_launch(layout == 0 ? "k_backward_splat2" : "k_backward_pixel"));
   SSR_TRY(launch_pdl("k_fix_plan", k_fix_plan, dim3(1), dim3(1024), 0, st, a, inst_rows));
   return launch_pdl("k_backward_fixup", k_backward_fixup, dim3(num_sms() * 2), dim3(256), 0, st, a, d_image, d_soft,
                     inst_rows);

@@ -73,19 +73,19 @@ def test_render_without_soft_counts(cfg, n, w, h, oracle_lib):
     st = TrainState(field=GaussianField.from_host(hp), optimizer=None, weights=bw, densify_enabled=False)
     st.optimizer = FieldOptimizer(st.field, 3.0)
     assert np.isfinite(train_iteration(st, cam, tgt, 1e-4).total)
-    # d_soft all zero (one-slot backward) vs d_soft None (two-slot backward):
-    # the same decisions and contributions, summed with a different rounding of
-    # the carried w . C_front (Adam's per-element normalisation would amplify
-    # that on near-zero gradients, so the gradients are compared, not trajectories)
+    # d_soft all zero on a soft-count frame vs d_soft None on a frame without
+    # soft counts: the same decisions and contributions (the gradients are
+    # compared, not trajectories: Adam's per-element normalisation would
+    # amplify any rounding difference on near-zero gradients)
     from paper_2503_13086_b200.rasterize import backward
 
     f2 = GaussianField.from_host(hp)
     o1 = render(f2, cam)
     o2 = render(f2, cam, soft_count=False)
     d = torch.randn(o2.image.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(5)) * 1e-3
-    g1 = backward(f2, o1, d, torch.zeros(o1.image.shape[:2], device="cuda"))  # one-slot kernel
-    g2 = backward(f2, o2, d, None)  # two-slot kernel
-    # a frame without soft counts keeps 64-slot checkpoints only: no soft-count gradient
+    g1 = backward(f2, o1, d, torch.zeros(o1.image.shape[:2], device="cuda"))
+    g2 = backward(f2, o2, d, None)
+    # a frame without soft counts takes no soft-count gradient
     with pytest.raises(InvalidParameter):
         backward(f2, o2, d, torch.zeros(o2.image.shape[:2], device="cuda"))
     for k in ("positions", "rotations", "log_scales", "opacity_logits", "sh", "screen_norms"):

@@ -59,7 +59,7 @@ def test_mixed_layouts_and_soft_gradient_share_the_workspace():
     out_a, out_b = render(f, ca), render(f, cb)
     da = torch.full_like(out_a.image, 2e-3)
     db = torch.full_like(out_b.image, -1e-3)
-    sb = torch.full_like(out_b.t_final, 1e-4)  # soft-count gradient: the one-slot kernel
+    sb = torch.full_like(out_b.t_final, 1e-4)  # soft-count gradient: the soft pair block
     ref = {lay: _fresh(lambda: backward(f, out_b, db, sb, layout=lay)).flat.clone() for lay in ("splat", "pixel")}
     for lay_a in ("pixel", "splat"):
         for lay_b in ("splat", "pixel"):
