@@ -191,7 +191,10 @@ __device__ __forceinline__ bool fwd_walk(FwdState& q, const float4* sP, const fl
 }
 
 // Splats staged per batch: two per thread (half the barriers of one per thread).
-constexpr int FWD_BATCH = 2 * TILE_PX;
+#ifndef SSR_FWD_PER
+#define SSR_FWD_PER 2
+#endif
+constexpr int FWD_BATCH = SSR_FWD_PER * TILE_PX;
 
 // CK = false: render-only (view_psnr, pipeline.py:180-182): no bucket
 // checkpoints are written (the backward's seeds, ~16 B per live pixel-bucket).
